@@ -1,0 +1,350 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 Lu-Liu grid-graph LCS hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+One step = one exact LCS solve (leaf step -> every combine level -> recovery
+walk -> assembly, results back on the host) of BASELINE.json config C
+(default 5: m = n = 16384 over 26 letters, the largest config and the one the
+roofline target is quoted on; configs 1-4 are parity cases, selectable here).
+Inputs are seeded synthetic strings (workloads.py = SURVEY.md Appendix C); no
+dataset exists for this path.
+
+value  = m*n / device time per solve, strings already resident in HBM,
+         CUDA events on the solve stream, L2 flushed (256 MiB write) between
+         steps, max over ranks.
+e2e    = same metric through the public API ``lcs(a, b)`` with HOST bytes in
+         and LcsResult out (H2D of strings + plan, D2H of results timed).
+roofline: dominant kernel = the combine levels; algorithmic bytes per solve =
+         4*G + 8*OUT + 4*IN from the reference's own work counters
+         (tests/golden/config_digests.json, counted by the C oracle /
+         SURVEY.md 8(d)), / the combine time measured live with CUDA events.
+cpu_baseline: the real reference (oracle/_ref, Cython backend) timed on this
+         host on a bounded sample (leading sub-strings), else the C oracle port.
+
+--impl reference runs the reference's own CPU path (oracle/_ref, all host
+threads) on the same config's bounded sample; rank 0 only.
+N > 1 (torchrun): each rank solves its own instance (seed + rank) of the same
+config on its own GPU -- weak scaling; the split-tree multi-GPU schedule is
+described in DESIGN.md and exercised by tests/test_distributed.py.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import workloads  # noqa: E402
+
+METRIC = "exact LCS cell-equivalents/sec (m*n/s)"
+UNIT = "cells/s"
+REF_SAMPLE = {1: 256, 2: 2048, 3: 2048, 4: 512, 5: 2048}  # leading-prefix length of the CPU sample
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU baseline work")
+    return p.parse_args()
+
+
+def load_counters(cfg, seed):
+    with open(os.path.join(ROOT, "tests", "golden", "config_digests.json")) as f:
+        d = json.load(f)
+    return d.get(f"cfg{cfg}/seed{seed}", {}).get("counters")
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)["hbm_gbs"], "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (reference / oracle port): bounded samples
+# ---------------------------------------------------------------------------
+def cpu_impl():
+    ref_dir = os.path.join(ROOT, "oracle", "_ref")
+    if os.path.isdir(os.path.join(ref_dir, "lcsgrid_ref")):
+        sys.path.insert(0, ref_dir)
+        try:
+            import lcsgrid_ref
+
+            if lcsgrid_ref.active_backend() == "cython":
+                return "reference", lambda a, b, t: lcsgrid_ref.lcs(a, b, threads=t).length
+        except Exception:
+            pass
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+
+    return "port", lambda a, b, t: O.lcs(a, b, threads=t)[0]
+
+
+def cpu_sample(cfg, seed):
+    a, b = workloads.generate(cfg, seed)
+    k = REF_SAMPLE[cfg]
+    if cfg == 4:  # query x text: keep the query, take a text window
+        return a[:k], b[: 64 * k]
+    return a[:k], b[:k]
+
+
+def cpu_baseline(cfg, seed, threads, budget_s):
+    kind, fn = cpu_impl()
+    a, b = cpu_sample(cfg, seed)
+    times = []
+    t_end = time.perf_counter() + budget_s
+    while True:
+        t0 = time.perf_counter()
+        fn(a, b, threads)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() > t_end or len(times) >= 50:
+            break
+    t = statistics.median(times)
+    return {"value": len(a) * len(b) / t, "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"cfg{cfg} seed {seed} leading {len(a)}x{len(b)} sub-strings, "
+                      f"median of {len(times)} solves ({t:.3f} s each)",
+            "seconds_per_solve": t}
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0))
+    kind, fn = cpu_impl()
+    a, b = cpu_sample(args.config, args.seed)
+    for _ in range(args.warmup):
+        fn(a, b, threads)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        fn(a, b, threads)
+        times.append(time.perf_counter() - t0)
+    t = statistics.mean(times)
+    value = len(a) * len(b) / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": workloads.CONFIGS[args.config]["name"] + "_cpu_sample",
+                   "m": len(a), "n": len(b), "seed": args.seed},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"cfg{args.config} leading {len(a)}x{len(b)} sub-strings"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU leg
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in (self.out or "").strip().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def run_ours(args, rank, world, dist):
+    import torch
+
+    from paper_2309_09072_b200 import _lib
+    import paper_2309_09072_b200 as lcsgrid
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    lib = _lib.load()
+    seed = args.seed + rank
+    a, b = workloads.generate(args.config, seed)
+    rows, cols = (b, a) if len(a) > len(b) else (a, b)
+    m, n = len(rows), len(cols)
+    d_rows = torch.frombuffer(bytearray(rows), dtype=torch.uint8).to(dev)
+    d_cols = torch.frombuffer(bytearray(cols), dtype=torch.uint8).to(dev)
+    stream = torch.cuda.current_stream(dev)
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    k = min(m, n)
+    sub = np.empty(k, np.uint8)
+    rp = np.empty(k, np.int32)
+    cp = np.empty(k, np.int32)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=dev)  # 256 MiB > L2
+    flags = _lib.LCSG_WITH_TRACE | _lib.LCSG_TIMING
+
+    def solve():
+        h = ctypes.c_void_p()
+        _lib.check(lib.lcsg_build_device(d_rows.data_ptr(), m, d_cols.data_ptr(), n, 1, m + 1,
+                                         flags, local, sp, ctypes.byref(h)), "build")
+        length = ctypes.c_int32()
+        _lib.check(lib.lcsg_extract(h, -1, ctypes.byref(length), sub.ctypes.data,
+                                    rp.ctypes.data, cp.ctypes.data), "extract")
+        st = [ctypes.c_int64(), ctypes.c_double(), ctypes.c_double(), ctypes.c_double(),
+              ctypes.c_int64(), ctypes.c_int64()]
+        _lib.check(lib.lcsg_stats(h, *[ctypes.byref(x) for x in st]), "stats")
+        lib.lcsg_free(h)
+        return int(length.value), st[0].value, st[1].value, st[4].value, st[5].value
+
+    for _ in range(args.warmup):
+        solve()
+    torch.cuda.synchronize()
+    step_ms, comb_ms, launches = [], [], 0
+    h2d = d2h = 0
+    length = None
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            if dist is not None:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            length, nl, cms, h2d, d2h = solve()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+            comb_ms.append(cms)
+            launches += nl
+    t_ms = statistics.mean(step_ms)
+    if dist is not None:
+        tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    value = world * m * n / (t_ms / 1e3)
+
+    # e2e: public API, host bytes in / LcsResult out, same stream + events
+    e2e_ms = []
+    for it in range(max(2, min(args.steps, 5))):
+        flush.zero_()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        r = lcsgrid.lcs(a, b, device=local, stream=stream.cuda_stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if it > 0:  # first call is a warm-up of the host-input path
+            e2e_ms.append(e0.elapsed_time(e1))
+    assert r.length == length
+    e2e_t = statistics.mean(e2e_ms)
+    if dist is not None:
+        tt = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_t = float(tt.item())
+
+    if rank != 0:
+        return
+    peak, peak_kind = measured_peaks()
+    counters = load_counters(args.config, seed)
+    comb = statistics.mean(comb_ms)
+    roof = None
+    if counters:
+        alg = 4 * counters["G"] + 8 * counters["OUT"] + 4 * counters["IN"]
+        achieved = alg / (comb / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None,
+                "kernel": "combine levels (all heights)", "combine_ms": comb,
+                "algorithmic_bytes": alg, "peak_source": peak_kind,
+                "compulsory_frac": (8 * counters["OUT"] + 4 * counters["IN"]) / (comb / 1e3) / 1e9 / peak}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": {"workload": workloads.CONFIGS[args.config]["name"], "m": m, "n": n,
+                   "seed": args.seed, "lcs_length": length, "l2": "flushed (256 MiB) between steps",
+                   "parallelism": f"replicas x{world}"},
+        "roofline": roof,
+        "e2e": {"value": world * m * n / (e2e_t / 1e3), "unit": UNIT,
+                "h2d_bytes_per_step": int(h2d + m + n), "d2h_bytes_per_step": int(d2h)},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline(args.config, args.seed, 1, args.cpu_budget)
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = None
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+        tdist.init_process_group("nccl")
+        dist = tdist
+    try:
+        run_ours(args, rank, world, dist)
+    finally:
+        if dist is not None:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,141 @@
+"""Loader and ctypes bindings of the C-ABI library (include/lcsgrid_b200.h).
+
+The library is built in-tree (``paper_2309_09072_b200/lib/liblcsgrid_b200.so``)
+by :func:`build_library` / ``__graft_entry__.build()``.  There is no CPU
+fallback: if the shared object is missing or no GPU is visible every solve
+raises, loudly.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_ROOT = os.path.dirname(_PKG)
+LIB_DIR = os.path.join(_PKG, "lib")
+LIB_PATH = os.path.join(LIB_DIR, "liblcsgrid_b200.so")
+CSRC = os.path.join(_PKG, "csrc")
+SOURCES = ["lcsg_api.cu", "lcsg_kernels.cu", "lcsg_refine.cu"]
+NVCC_FLAGS = [
+    "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+    "-Xcompiler", "-fPIC", "-shared",
+]
+
+LCSG_OK = 0
+LCSG_EINVAL = -1
+LCSG_ECUDA = -2
+LCSG_ENOMEM = -3
+LCSG_ENODEV = -4
+LCSG_ERANGE = -5
+LCSG_WITH_TRACE = 1
+LCSG_TIMING = 2
+
+_lib = None
+_lock = threading.Lock()
+
+_i32p = ctypes.POINTER(ctypes.c_int32)
+_u8p = ctypes.POINTER(ctypes.c_uint8)
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int32
+
+# name -> (restype, argtypes); every symbol declared in include/lcsgrid_b200.h
+SIGNATURES = {
+    "lcsg_last_error": (ctypes.c_char_p, []),
+    "lcsg_abi_version": (ctypes.c_int, []),
+    "lcsg_device_count": (ctypes.c_int, []),
+    "lcsg_build": (ctypes.c_int, [_vp, _i64, _vp, _i64, _i32, _i32, ctypes.c_uint32, ctypes.c_int,
+                                  _vp, ctypes.POINTER(_vp)]),
+    "lcsg_build_device": (ctypes.c_int, [_vp, _i64, _vp, _i64, _i32, _i32, ctypes.c_uint32,
+                                         ctypes.c_int, _vp, ctypes.POINTER(_vp)]),
+    "lcsg_free": (ctypes.c_int, [_vp]),
+    "lcsg_sync": (ctypes.c_int, [_vp]),
+    "lcsg_num_nodes": (_i32, [_vp]),
+    "lcsg_root": (_i32, [_vp]),
+    "lcsg_node_info": (ctypes.c_int, [_vp, _i32, _i32p]),
+    "lcsg_node_wstar": (ctypes.c_int, [_vp, _i32, _i32p]),
+    "lcsg_node_reach": (ctypes.c_int, [_vp, _i32, _vp]),
+    "lcsg_node_trace": (ctypes.c_int, [_vp, _i32, _vp]),
+    "lcsg_node_kmax": (ctypes.c_int, [_vp, _i32, _vp]),
+    "lcsg_node_reach_device": (ctypes.c_int, [_vp, _i32, ctypes.POINTER(_vp)]),
+    "lcsg_length": (ctypes.c_int, [_vp, _i32p]),
+    "lcsg_recover": (ctypes.c_int, [_vp, _i32, _vp]),
+    "lcsg_extract": (ctypes.c_int, [_vp, _i32, _i32p, _vp, _vp, _vp]),
+    "lcsg_assemble": (ctypes.c_int, [_vp, _i64, _vp, _i64, _vp, ctypes.c_int, _i32p, _vp, _vp,
+                                     _vp]),
+    "lcsg_lcs": (ctypes.c_int, [_vp, _i64, _vp, _i64, ctypes.c_uint32, ctypes.c_int, _vp, _i32p,
+                                _vp, _vp, _vp]),
+    "lcsg_lcs_device": (ctypes.c_int, [_vp, _i64, _vp, _i64, ctypes.c_uint32, ctypes.c_int, _vp,
+                                       _i32p, _vp, _vp, _vp]),
+    "lcsg_combine_level": (ctypes.c_int, [_vp, _i32, _vp, _vp, _i32, _i32, _vp, _vp, _i32,
+                                          ctypes.c_int, _i32, _i64, _i64, _i64, _vp]),
+    "lcsg_base_case_row": (ctypes.c_int, [_vp, _i64, ctypes.c_uint8, _vp, _vp]),
+    "lcsg_stats": (ctypes.c_int, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_double),
+                                  ctypes.POINTER(ctypes.c_double),
+                                  ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64),
+                                  ctypes.POINTER(_i64)]),
+}
+
+
+def build_library(verbose: bool = False) -> str:
+    """Compile the CUDA sources for sm_100a into the in-tree shared object."""
+    os.makedirs(LIB_DIR, exist_ok=True)
+    srcs = [os.path.join(CSRC, s) for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
+    cmd = ["nvcc", *NVCC_FLAGS, "-o", LIB_PATH, *srcs]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
+    if verbose:
+        print(res.stdout + res.stderr)
+    return LIB_PATH
+
+
+def load():
+    """Load the shared object (once).  Raises if it is absent: no fallback."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise ImportError(
+                    f"{LIB_PATH} is missing; build it with __graft_entry__.build() "
+                    "(the CUDA path has no CPU fallback)")
+            lib = ctypes.CDLL(LIB_PATH)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def available() -> bool:
+    try:
+        load()
+        return True
+    except OSError:
+        return False
+    except ImportError:
+        return False
+
+
+def last_error() -> str:
+    return load().lcsg_last_error().decode("utf-8", "replace")
+
+
+def check(rc: int, what: str = "") -> None:
+    """Map a C-ABI status to the reference's exception types."""
+    if rc == LCSG_OK:
+        return
+    msg = last_error()
+    if what:
+        msg = f"{what}: {msg}"
+    if rc == LCSG_ERANGE or rc == LCSG_EINVAL:
+        raise ValueError(msg)
+    if rc == LCSG_ENOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError(msg)

@@ -1,0 +1,846 @@
+// lcsg_api.cu -- C-ABI (include/lcsgrid_b200.h) and the device-resident level
+// scheduler of the Lu-Liu recursion.
+//
+// The reference builds its tree depth-first and sequentially, one combine at
+// a time through a CPU thread pool (solver.py:113-119, parallel.py:50-66).
+// Here the whole tree is laid out in ONE HBM arena up front and every
+// combine of one height is launched as a single batched grid, in height
+// order, on one stream: leaf step -> height 1 .. H -> walk -> assemble.
+// The node numbering equals the reference's creation order (post-order), so
+// per-node fixtures compare node by node.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/lcsgrid_b200.h"
+#include "lcsg_internal.cuh"
+
+using namespace lcsg;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CK(call)                                                                            \
+    do {                                                                                    \
+        cudaError_t e__ = (call);                                                           \
+        if (e__ != cudaSuccess)                                                             \
+            return fail(e__ == cudaErrorMemoryAllocation ? LCSG_ENOMEM : LCSG_ECUDA,        \
+                        std::string(#call) + ": " + cudaGetErrorString(e__));               \
+    } while (0)
+
+#define CKL(call)                                                                           \
+    do {                                                                                    \
+        int e__ = (call);                                                                   \
+        if (e__ != 0)                                                                       \
+            return fail(LCSG_ECUDA, std::string("kernel launch ") + #call + ": " +          \
+                                        cudaGetErrorString((cudaError_t)e__));              \
+    } while (0)
+
+int bits_for(int64_t x) {
+    if (x <= 0) return 1;
+    int b = 0;
+    while (x > 0) { ++b; x >>= 1; }
+    return b;
+}
+
+std::mutex g_pool_mu;
+bool g_pool_ready[64] = {};
+
+int prepare_device(int device) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+        return fail(LCSG_ENODEV, "no CUDA device visible");
+    if (device < 0 || device >= count) return fail(LCSG_EINVAL, "device index out of range");
+    CK(cudaSetDevice(device));
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    if (device < 64 && !g_pool_ready[device]) {
+        // stream-ordered allocator that keeps freed blocks: repeated solves
+        // reuse the same HBM without cudaMalloc/cudaFree round trips.
+        cudaMemPool_t pool;
+        CK(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t thr = UINT64_MAX;
+        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+        g_pool_ready[device] = true;
+    }
+    return LCSG_OK;
+}
+
+// thread-per-row bisection below this table width, warp-per-row above
+constexpr int32_t THREAD_KERNEL_MAX_W1 = 65;
+
+struct NodeH {
+    int32_t top_row, bottom_row, w1, upper, lower, height, depth, leaf_row;
+    int64_t reach_off = -1, trace_off = -1, kmax_off = -1;  // int32 element offsets
+};
+
+struct LaunchH {
+    int kind;
+    int32_t desc_off, count;
+    int shift;
+    bool key64;
+};
+
+size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+struct lcsg_tree_s {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int64_t m_grid = 0, m_slab = 0, n = 0;
+    int32_t inf = 0, top_row = 1, bottom_row = 2;
+    bool with_trace = true, timing = false;
+    std::vector<NodeH> nodes;
+    int32_t root = -1;
+    std::vector<LaunchH> plan;
+    std::vector<std::pair<int32_t, int32_t>> depth_ranges;  // (offset, count) into walk ids
+    int walk_shift = 1;
+    bool walk_key64 = false;
+    // device
+    char *arena = nullptr;
+    size_t arena_bytes = 0;
+    uint8_t *d_rows = nullptr, *d_cols = nullptr, *d_subseq = nullptr;
+    int32_t *d_nx = nullptr, *d_sym_wstar = nullptr, *d_node_wstar = nullptr, *d_tables = nullptr;
+    CombineDesc *d_descs = nullptr;
+    WalkNode *d_walk = nullptr;
+    int32_t *d_walk_ids = nullptr, *d_leaf_nodes = nullptr, *d_leaf_rows = nullptr;
+    int32_t *d_wi = nullptr, *d_wj = nullptr, *d_path = nullptr, *d_out = nullptr;
+    int32_t nleaves = 0;
+    std::map<int32_t, int32_t *> leaf_cache;
+    int64_t launches = 0, h2d_bytes = 0, d2h_bytes = 0;
+    cudaEvent_t ev[5] = {};
+    bool ev_ok = false;
+
+    Ctx ctx() const {
+        Ctx c;
+        c.rows = d_rows;
+        c.nx = d_nx;
+        c.n = (int32_t)n;
+        c.inf = inf;
+        return c;
+    }
+    TabDev tab(int32_t id) const {
+        const NodeH &nd = nodes[id];
+        TabDev t;
+        t.w1 = nd.w1;
+        t.wstar = d_node_wstar + id;
+        if (nd.upper < 0) {
+            t.reach = nullptr;
+            t.kmax = nullptr;
+            t.leaf_row = nd.leaf_row;
+        } else {
+            t.reach = d_tables + nd.reach_off;
+            t.kmax = d_tables + nd.kmax_off;
+            t.leaf_row = -1;
+        }
+        return t;
+    }
+};
+
+namespace {
+
+// solver.py:113-119 -- same split, same (post-)order of node creation.
+int32_t build_tree(lcsg_tree_s *t, int32_t top, int32_t bottom, int32_t depth) {
+    NodeH nd;
+    nd.top_row = top;
+    nd.bottom_row = bottom;
+    nd.depth = depth;
+    int64_t w = std::min<int64_t>(bottom - top, t->n);
+    nd.w1 = (int32_t)(w + 1);
+    if (bottom == top + 1) {
+        nd.upper = nd.lower = -1;
+        nd.height = 0;
+        nd.leaf_row = top - t->top_row;
+        t->nodes.push_back(nd);
+        return (int32_t)t->nodes.size() - 1;
+    }
+    int32_t mid = (top + bottom) / 2;
+    int32_t up = build_tree(t, top, mid, depth + 1);
+    int32_t lo = build_tree(t, mid, bottom, depth + 1);
+    nd.upper = up;
+    nd.lower = lo;
+    nd.leaf_row = -1;
+    nd.height = 1 + std::max(t->nodes[up].height, t->nodes[lo].height);
+    t->nodes.push_back(nd);
+    return (int32_t)t->nodes.size() - 1;
+}
+
+void destroy(lcsg_tree_s *t) {
+    if (!t) return;
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(t->device);
+    for (auto &kv : t->leaf_cache) cudaFreeAsync(kv.second, t->stream);
+    if (t->arena) cudaFreeAsync(t->arena, t->stream);
+    if (t->ev_ok)
+        for (auto &e : t->ev) cudaEventDestroy(e);
+    if (t->own_stream) {
+        cudaStreamSynchronize(t->stream);
+        cudaStreamDestroy(t->stream);
+    }
+    if (prev >= 0) cudaSetDevice(prev);
+    delete t;
+}
+
+int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *cols, bool cols_dev,
+               int64_t n, int32_t top_row, int32_t bottom_row, uint32_t flags, int device,
+               void *stream, lcsg_handle *out) {
+    if (!out) return fail(LCSG_EINVAL, "null output handle");
+    *out = nullptr;
+    if (m < 0 || n < 0) return fail(LCSG_EINVAL, "negative length");
+    if (!(1 <= top_row && top_row < bottom_row && (int64_t)bottom_row <= m + 1))
+        return fail(LCSG_EINVAL, "1 <= top_row < bottom_row <= m + 1");
+    if (n > (int64_t)INT32_MAX - 4) return fail(LCSG_EINVAL, "column string too long for int32 tables");
+    int rc = prepare_device(device);
+    if (rc) return rc;
+
+    lcsg_tree_s *t = new lcsg_tree_s();
+    t->device = device;
+    t->m_grid = m;
+    t->m_slab = bottom_row - top_row;
+    t->n = n;
+    t->inf = (int32_t)(n + 2);
+    t->top_row = top_row;
+    t->bottom_row = bottom_row;
+    t->with_trace = (flags & LCSG_WITH_TRACE) != 0;
+    t->timing = (flags & LCSG_TIMING) != 0;
+    if (stream) {
+        t->stream = (cudaStream_t)stream;
+    } else {
+        if (cudaStreamCreateWithFlags(&t->stream, cudaStreamNonBlocking) != cudaSuccess) {
+            delete t;
+            return fail(LCSG_ECUDA, "cudaStreamCreate failed");
+        }
+        t->own_stream = true;
+    }
+    if (t->timing) {
+        t->ev_ok = true;
+        for (auto &e : t->ev)
+            if (cudaEventCreate(&e) != cudaSuccess) t->ev_ok = false;
+    }
+
+    t->nodes.reserve(2 * t->m_slab);
+    t->root = build_tree(t, top_row, bottom_row, 0);
+    const int32_t nn = (int32_t)t->nodes.size();
+    const int64_t n1 = n + 1;
+
+    // ---- arena layout ----
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off = align_up(off + bytes);
+        return o;
+    };
+    const int64_t kmin = std::min<int64_t>(t->m_slab, n);
+    size_t o_rows = take((size_t)t->m_slab);
+    size_t o_cols = take((size_t)std::max<int64_t>(n, 1));
+    size_t o_nx = take((size_t)256 * n1 * 4);
+    size_t o_symw = take(256 * 4);
+    size_t o_nodew = take((size_t)nn * 4);
+    size_t o_wi = take((size_t)nn * 4), o_wj = take((size_t)nn * 4);
+    size_t o_path = take((size_t)(t->m_slab + 1) * 4);
+    size_t o_out = take((size_t)(1 + 2 * std::max<int64_t>(kmin, 1)) * 4);
+    size_t o_sub = take((size_t)std::max<int64_t>(kmin, 1));
+    // int32 tables of every combine node
+    size_t o_tab = off;
+    int64_t tab_elems = 0;
+    int32_t ncomb = 0;
+    for (auto &nd : t->nodes) {
+        if (nd.upper < 0) { t->nleaves++; continue; }
+        ++ncomb;
+        nd.reach_off = tab_elems;
+        tab_elems += n1 * nd.w1;
+        if (t->with_trace) {
+            nd.trace_off = tab_elems;
+            tab_elems += n1 * nd.w1;
+        }
+        nd.kmax_off = tab_elems;
+        tab_elems += (n1 + 63) / 64 * 64;
+    }
+    off = align_up(o_tab + (size_t)tab_elems * 4);
+    // metadata region (uploaded with one copy)
+    size_t o_meta = off;
+    size_t o_desc = take((size_t)std::max(ncomb, 1) * sizeof(CombineDesc));
+    size_t o_walk = take((size_t)nn * sizeof(WalkNode));
+    size_t o_wids = take((size_t)std::max(ncomb, 1) * 4);
+    size_t o_lnodes = take((size_t)std::max(t->nleaves, 1) * 4);
+    size_t o_lrows = take((size_t)std::max(t->nleaves, 1) * 4);
+    size_t meta_end = off;
+    t->arena_bytes = off;
+
+    cudaError_t ae = cudaMallocAsync((void **)&t->arena, t->arena_bytes, t->stream);
+    if (ae != cudaSuccess) {
+        t->arena = nullptr;
+        destroy(t);
+        return fail(LCSG_ENOMEM, std::string("cudaMallocAsync(") + std::to_string(off) +
+                                     " B): " + cudaGetErrorString(ae));
+    }
+    char *A = t->arena;
+    t->d_rows = (uint8_t *)(A + o_rows);
+    t->d_cols = (uint8_t *)(A + o_cols);
+    t->d_nx = (int32_t *)(A + o_nx);
+    t->d_sym_wstar = (int32_t *)(A + o_symw);
+    t->d_node_wstar = (int32_t *)(A + o_nodew);
+    t->d_wi = (int32_t *)(A + o_wi);
+    t->d_wj = (int32_t *)(A + o_wj);
+    t->d_path = (int32_t *)(A + o_path);
+    t->d_out = (int32_t *)(A + o_out);
+    t->d_subseq = (uint8_t *)(A + o_sub);
+    t->d_tables = (int32_t *)(A + o_tab);
+    t->d_descs = (CombineDesc *)(A + o_desc);
+    t->d_walk = (WalkNode *)(A + o_walk);
+    t->d_walk_ids = (int32_t *)(A + o_wids);
+    t->d_leaf_nodes = (int32_t *)(A + o_lnodes);
+    t->d_leaf_rows = (int32_t *)(A + o_lrows);
+
+    // ---- host-side metadata: level plan, descriptors, walk nodes ----
+    std::vector<char> meta(meta_end - o_meta, 0);
+    CombineDesc *hd = (CombineDesc *)(meta.data() + (o_desc - o_meta));
+    WalkNode *hw = (WalkNode *)(meta.data() + (o_walk - o_meta));
+    int32_t *hids = (int32_t *)(meta.data() + (o_wids - o_meta));
+    int32_t *hln = (int32_t *)(meta.data() + (o_lnodes - o_meta));
+    int32_t *hlr = (int32_t *)(meta.data() + (o_lrows - o_meta));
+
+    int32_t maxh = 0;
+    for (auto &nd : t->nodes) maxh = std::max(maxh, nd.height);
+    const int vbits = bits_for(t->inf);
+    int32_t di = 0;
+    for (int32_t h = 1; h <= maxh; ++h) {
+        for (int kind = 0; kind < 2; ++kind) {
+            int32_t start = di;
+            int32_t maxk = 0;
+            for (int32_t id = 0; id < nn; ++id) {
+                const NodeH &nd = t->nodes[id];
+                if (nd.height != h) continue;
+                int k = nd.w1 <= THREAD_KERNEL_MAX_W1 ? 0 : 1;
+                if (k != kind) continue;
+                CombineDesc &d = hd[di++];
+                d.U = t->tab(nd.upper);
+                d.L = t->tab(nd.lower);
+                d.out_reach = t->d_tables + nd.reach_off;
+                d.out_trace = t->with_trace ? t->d_tables + nd.trace_off : nullptr;
+                d.out_kmax = t->d_tables + nd.kmax_off;
+                d.out_wstar = t->d_node_wstar + id;
+                d.w1 = nd.w1;
+                d.node = id;
+                maxk = std::max(maxk, t->nodes[nd.upper].w1 - 1);
+            }
+            if (di > start) {
+                LaunchH L;
+                L.kind = kind;
+                L.desc_off = start;
+                L.count = di - start;
+                L.shift = bits_for(maxk);
+                L.key64 = vbits + L.shift > 32;
+                t->plan.push_back(L);
+            }
+        }
+    }
+    // walk nodes + depth lists of internal nodes
+    int32_t maxd = 0, maxku = 0;
+    for (int32_t id = 0; id < nn; ++id) {
+        const NodeH &nd = t->nodes[id];
+        WalkNode &w = hw[id];
+        w.top_row = nd.top_row;
+        w.bottom_row = nd.bottom_row;
+        w.upper = nd.upper;
+        w.lower = nd.lower;
+        w.w1 = nd.w1;
+        w.is_leaf = nd.upper < 0;
+        w.trace = (nd.upper >= 0 && t->with_trace) ? t->d_tables + nd.trace_off : nullptr;
+        if (nd.upper >= 0) {
+            w.U = t->tab(nd.upper);
+            w.L = t->tab(nd.lower);
+            maxku = std::max(maxku, t->nodes[nd.upper].w1 - 1);
+        }
+        maxd = std::max(maxd, nd.depth);
+    }
+    t->walk_shift = bits_for(maxku);
+    t->walk_key64 = vbits + t->walk_shift > 32;
+    int32_t wpos = 0;
+    for (int32_t dd = 0; dd <= maxd; ++dd) {
+        int32_t start = wpos;
+        for (int32_t id = 0; id < nn; ++id)
+            if (t->nodes[id].upper >= 0 && t->nodes[id].depth == dd) hids[wpos++] = id;
+        if (wpos > start) t->depth_ranges.push_back({start, wpos - start});
+    }
+    int32_t li = 0;
+    for (int32_t id = 0; id < nn; ++id)
+        if (t->nodes[id].upper < 0) {
+            hln[li] = id;
+            hlr[li] = t->nodes[id].leaf_row;
+            ++li;
+        }
+
+    // ---- enqueue: inputs, metadata, leaf step, levels ----
+    const cudaStream_t s = t->stream;
+#define BCK(call)                            \
+    do {                                     \
+        int r__ = 0;                         \
+        cudaError_t e__ = (call);            \
+        if (e__ != cudaSuccess) {            \
+            r__ = fail(LCSG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e__)); \
+            destroy(t);                      \
+            return r__;                      \
+        }                                    \
+    } while (0)
+#define BCKL(call)                           \
+    do {                                     \
+        int e__ = (call);                    \
+        if (e__ != 0) {                      \
+            int r__ = fail(LCSG_ECUDA, std::string("launch ") + #call + ": " +      \
+                                           cudaGetErrorString((cudaError_t)e__));   \
+            destroy(t);                      \
+            return r__;                      \
+        }                                    \
+        ++t->launches;                       \
+    } while (0)
+
+    if (t->timing && t->ev_ok) BCK(cudaEventRecord(t->ev[0], s));
+    const uint8_t *rows_slab = rows + (top_row - 1);
+    if (t->m_slab > 0)
+        BCK(cudaMemcpyAsync(t->d_rows, rows_slab, (size_t)t->m_slab,
+                            rows_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    if (n > 0)
+        BCK(cudaMemcpyAsync(t->d_cols, cols, (size_t)n,
+                            cols_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    BCK(cudaMemcpyAsync(A + o_meta, meta.data(), meta.size(), cudaMemcpyHostToDevice, s));
+    t->h2d_bytes = (int64_t)meta.size() + (rows_dev ? 0 : t->m_slab) + (cols_dev ? 0 : n);
+    // the pageable-host copy above is staged synchronously, so `meta` may die
+    BCK(cudaMemsetAsync(t->d_node_wstar, 0, (size_t)nn * 4, s));
+    BCKL(launch_nx(t->d_cols, (int32_t)n, t->d_nx, t->d_sym_wstar, s));
+    BCKL(launch_leaf_wstar(t->d_rows, t->d_leaf_nodes, t->d_leaf_rows, t->nleaves,
+                           t->d_sym_wstar, t->d_node_wstar, s));
+    if (t->timing && t->ev_ok) BCK(cudaEventRecord(t->ev[1], s));
+    const Ctx c = t->ctx();
+    for (const LaunchH &L : t->plan)
+        BCKL(launch_combine(L.kind, t->d_descs + L.desc_off, L.count, c, L.shift, L.key64, s));
+    if (t->timing && t->ev_ok) BCK(cudaEventRecord(t->ev[2], s));
+#undef BCK
+#undef BCKL
+    *out = t;
+    return LCSG_OK;
+}
+
+bool full_grid(const lcsg_tree_s *t) { return t->top_row == 1 && t->bottom_row == t->m_grid + 1; }
+
+// recovery walk for weight j (j < 0: the LCS length, read on the device)
+int run_walk(lcsg_tree_s *t, int32_t j) {
+    const cudaStream_t s = t->stream;
+    const Ctx c = t->ctx();
+    const TabDev rt = t->tab(t->root);
+    CKL(launch_walk_root(t->d_walk, t->root, c, rt, j, (int32_t)t->m_slab, t->d_wi, t->d_wj,
+                         t->d_path, s));
+    ++t->launches;
+    const bool retrace = !t->with_trace;
+    for (auto &dr : t->depth_ranges) {
+        CKL(launch_walk_level(t->d_walk, t->d_walk_ids + dr.first, dr.second, c, t->d_wi, t->d_wj,
+                              t->d_path, retrace, t->walk_shift, t->walk_key64, s));
+        ++t->launches;
+    }
+    CKL(launch_walk_final(c, rt, j, (int32_t)t->m_slab, t->d_wj + t->root, t->d_path, s));
+    ++t->launches;
+    return LCSG_OK;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+int lcs_impl(const uint8_t *a, int64_t la, const uint8_t *b, int64_t lb, bool dev, uint32_t flags,
+             int device, void *stream, int32_t *length, uint8_t *subseq, int32_t *pos_a,
+             int32_t *pos_b) {
+    if (!length) return fail(LCSG_EINVAL, "null length pointer");
+    *length = 0;
+    if (la == 0 || lb == 0) return LCSG_OK;  // solver.py:255-256
+    const bool swapped = la > lb;             // solver.py:257-258
+    const uint8_t *rows = swapped ? b : a, *cols = swapped ? a : b;
+    const int64_t m = swapped ? lb : la, n = swapped ? la : lb;
+    lcsg_handle h = nullptr;
+    int rc = build_impl(rows, dev, m, cols, dev, n, 1, (int32_t)(m + 1), flags, device, stream, &h);
+    if (rc) return rc;
+    DeviceGuard g(h->device);
+    rc = run_walk(h, -1);
+    if (rc == 0) {
+        int r2 = launch_assemble(h->d_rows, (int32_t)m, h->d_cols, (int32_t)n, h->d_path, h->d_out,
+                                 h->d_out + 1, h->d_out + 1 + std::min(m, n), h->d_subseq,
+                                 h->stream);
+        if (r2) rc = fail(LCSG_ECUDA, std::string("assemble: ") + cudaGetErrorString((cudaError_t)r2));
+        ++h->launches;
+    }
+    if (rc == 0) {
+        const int64_t k = std::min(m, n);
+        std::vector<int32_t> hb((size_t)(1 + 2 * k));
+        std::vector<uint8_t> hs((size_t)k);
+        cudaError_t e = cudaMemcpyAsync(hb.data(), h->d_out, hb.size() * 4, cudaMemcpyDeviceToHost, h->stream);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(hs.data(), h->d_subseq, (size_t)k, cudaMemcpyDeviceToHost, h->stream);
+        if (e == cudaSuccess && h->timing && h->ev_ok) e = cudaEventRecord(h->ev[3], h->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+        if (e != cudaSuccess) {
+            rc = fail(LCSG_ECUDA, std::string("lcs result copy: ") + cudaGetErrorString(e));
+        } else {
+            const int32_t len = hb[0];
+            *length = len;
+            int32_t *rp = swapped ? pos_b : pos_a, *cp = swapped ? pos_a : pos_b;
+            if (subseq) std::memcpy(subseq, hs.data(), (size_t)len);
+            if (rp) std::memcpy(rp, hb.data() + 1, (size_t)len * 4);
+            if (cp) std::memcpy(cp, hb.data() + 1 + k, (size_t)len * 4);
+        }
+    }
+    destroy(h);
+    return rc;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *lcsg_last_error(void) { return g_err.c_str(); }
+int lcsg_abi_version(void) { return 100; }
+
+int lcsg_device_count(void) {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return c;
+}
+
+int lcsg_build(const uint8_t *rows, int64_t m, const uint8_t *cols, int64_t n, int32_t top_row,
+               int32_t bottom_row, uint32_t flags, int device, void *stream, lcsg_handle *out) {
+    return build_impl(rows, false, m, cols, false, n, top_row, bottom_row, flags, device, stream, out);
+}
+
+int lcsg_build_device(const uint8_t *rows_dev, int64_t m, const uint8_t *cols_dev, int64_t n,
+                      int32_t top_row, int32_t bottom_row, uint32_t flags, int device,
+                      void *stream, lcsg_handle *out) {
+    return build_impl(rows_dev, true, m, cols_dev, true, n, top_row, bottom_row, flags, device,
+                      stream, out);
+}
+
+int lcsg_free(lcsg_handle h) {
+    destroy(h);
+    return LCSG_OK;
+}
+
+int lcsg_sync(lcsg_handle h) {
+    if (!h) return fail(LCSG_EINVAL, "null handle");
+    DeviceGuard g(h->device);
+    CK(cudaStreamSynchronize(h->stream));
+    return LCSG_OK;
+}
+
+int32_t lcsg_num_nodes(lcsg_handle h) { return h ? (int32_t)h->nodes.size() : -1; }
+int32_t lcsg_root(lcsg_handle h) { return h ? h->root : -1; }
+
+int lcsg_node_info(lcsg_handle h, int32_t node, int32_t *info) {
+    if (!h || node < 0 || node >= (int32_t)h->nodes.size()) return fail(LCSG_EINVAL, "bad node");
+    const NodeH &nd = h->nodes[node];
+    info[0] = nd.top_row;
+    info[1] = nd.bottom_row;
+    info[2] = nd.w1;
+    info[3] = nd.upper;
+    info[4] = nd.lower;
+    info[5] = (nd.upper >= 0 && h->with_trace) ? 1 : 0;
+    info[6] = (int32_t)h->n;
+    info[7] = h->inf;
+    return LCSG_OK;
+}
+
+int lcsg_node_wstar(lcsg_handle h, int32_t node, int32_t *wstar) {
+    if (!h || node < 0 || node >= (int32_t)h->nodes.size()) return fail(LCSG_EINVAL, "bad node");
+    DeviceGuard g(h->device);
+    CK(cudaMemcpyAsync(wstar, h->d_node_wstar + node, 4, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return LCSG_OK;
+}
+
+static int leaf_device(lcsg_handle h, int32_t node, int32_t **reach) {
+    auto it = h->leaf_cache.find(node);
+    if (it != h->leaf_cache.end()) {
+        *reach = it->second;
+        return LCSG_OK;
+    }
+    const NodeH &nd = h->nodes[node];
+    const int64_t n1 = h->n + 1;
+    int32_t *buf = nullptr;
+    CK(cudaMallocAsync((void **)&buf, (size_t)(n1 * nd.w1 + n1) * 4, h->stream));
+    h->leaf_cache[node] = buf;
+    CKL(launch_leaf_table(h->ctx(), nd.leaf_row, nd.w1, buf, buf + n1 * nd.w1, h->stream));
+    ++h->launches;
+    *reach = buf;
+    return LCSG_OK;
+}
+
+int lcsg_node_reach_device(lcsg_handle h, int32_t node, void **dev_ptr) {
+    if (!h || node < 0 || node >= (int32_t)h->nodes.size()) return fail(LCSG_EINVAL, "bad node");
+    DeviceGuard g(h->device);
+    const NodeH &nd = h->nodes[node];
+    if (nd.upper < 0) {
+        int32_t *p = nullptr;
+        int rc = leaf_device(h, node, &p);
+        if (rc) return rc;
+        *dev_ptr = p;
+    } else {
+        *dev_ptr = h->d_tables + nd.reach_off;
+    }
+    return LCSG_OK;
+}
+
+static int copy_node(lcsg_handle h, int32_t node, int which, int32_t *host_out) {
+    if (!h || node < 0 || node >= (int32_t)h->nodes.size()) return fail(LCSG_EINVAL, "bad node");
+    DeviceGuard g(h->device);
+    const NodeH &nd = h->nodes[node];
+    const int64_t n1 = h->n + 1;
+    const int32_t *src = nullptr;
+    size_t elems = 0;
+    if (nd.upper < 0) {
+        if (which == 1) return fail(LCSG_EINVAL, "leaf tables carry no trace");
+        int32_t *p = nullptr;
+        int rc = leaf_device(h, node, &p);
+        if (rc) return rc;
+        src = which == 0 ? p : p + n1 * nd.w1;
+        elems = which == 0 ? (size_t)(n1 * nd.w1) : (size_t)n1;
+    } else if (which == 0) {
+        src = h->d_tables + nd.reach_off;
+        elems = (size_t)(n1 * nd.w1);
+    } else if (which == 1) {
+        if (!h->with_trace) return fail(LCSG_EINVAL, "table was built without traces");
+        src = h->d_tables + nd.trace_off;
+        elems = (size_t)(n1 * nd.w1);
+    } else {
+        src = h->d_tables + nd.kmax_off;
+        elems = (size_t)n1;
+    }
+    CK(cudaMemcpyAsync(host_out, src, elems * 4, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return LCSG_OK;
+}
+
+int lcsg_node_reach(lcsg_handle h, int32_t node, int32_t *o) { return copy_node(h, node, 0, o); }
+int lcsg_node_trace(lcsg_handle h, int32_t node, int32_t *o) { return copy_node(h, node, 1, o); }
+int lcsg_node_kmax(lcsg_handle h, int32_t node, int32_t *o) { return copy_node(h, node, 2, o); }
+
+int lcsg_length(lcsg_handle h, int32_t *length) {
+    if (!h) return fail(LCSG_EINVAL, "null handle");
+    DeviceGuard g(h->device);
+    const NodeH &r = h->nodes[h->root];
+    if (r.upper < 0) {
+        int32_t *p = nullptr;
+        int rc = leaf_device(h, h->root, &p);
+        if (rc) return rc;
+        CK(cudaMemcpyAsync(length, p + (h->n + 1) * r.w1, 4, cudaMemcpyDeviceToHost, h->stream));
+    } else {
+        CK(cudaMemcpyAsync(length, h->d_tables + r.kmax_off, 4, cudaMemcpyDeviceToHost, h->stream));
+    }
+    CK(cudaStreamSynchronize(h->stream));
+    return LCSG_OK;
+}
+
+int lcsg_recover(lcsg_handle h, int32_t j, int32_t *cols_out) {
+    if (!h) return fail(LCSG_EINVAL, "null handle");
+    if (!full_grid(h)) return fail(LCSG_EINVAL, "recovery needs the full-grid table");
+    int32_t len = 0;
+    int rc = lcsg_length(h, &len);
+    if (rc) return rc;
+    if (j > len) return fail(LCSG_ERANGE, "no path of weight " + std::to_string(j) +
+                                              " exists (max " + std::to_string(len) + ")");
+    if (j < 0) return fail(LCSG_EINVAL, "negative weight");
+    DeviceGuard g(h->device);
+    rc = run_walk(h, j);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(cols_out, h->d_path, (size_t)(h->m_slab + 1) * 4, cudaMemcpyDeviceToHost,
+                       h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return LCSG_OK;
+}
+
+int lcsg_extract(lcsg_handle h, int32_t j, int32_t *length, uint8_t *subseq, int32_t *row_pos,
+                 int32_t *col_pos) {
+    if (!h) return fail(LCSG_EINVAL, "null handle");
+    if (!full_grid(h)) return fail(LCSG_EINVAL, "recovery needs the full-grid table");
+    DeviceGuard g(h->device);
+    if (j >= 0) {
+        int32_t len = 0;
+        int rc = lcsg_length(h, &len);
+        if (rc) return rc;
+        if (j > len) return fail(LCSG_ERANGE, "no path of weight " + std::to_string(j) +
+                                                  " exists (max " + std::to_string(len) + ")");
+    }
+    int rc = run_walk(h, j);
+    if (rc) return rc;
+    const int64_t m = h->m_slab, n = h->n, k = std::min(m, n);
+    CKL(launch_assemble(h->d_rows, (int32_t)m, h->d_cols, (int32_t)n, h->d_path, h->d_out,
+                        h->d_out + 1, h->d_out + 1 + std::max<int64_t>(k, 1), h->d_subseq, h->stream));
+    ++h->launches;
+    std::vector<int32_t> hb((size_t)(1 + 2 * std::max<int64_t>(k, 1)));
+    CK(cudaMemcpyAsync(hb.data(), h->d_out, hb.size() * 4, cudaMemcpyDeviceToHost, h->stream));
+    std::vector<uint8_t> hs((size_t)std::max<int64_t>(k, 1));
+    CK(cudaMemcpyAsync(hs.data(), h->d_subseq, hs.size(), cudaMemcpyDeviceToHost, h->stream));
+    if (h->timing && h->ev_ok) CK(cudaEventRecord(h->ev[3], h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    h->d2h_bytes += (int64_t)(hb.size() * 4 + hs.size());
+    const int32_t len = hb[0];
+    *length = len;
+    if (subseq) std::memcpy(subseq, hs.data(), (size_t)len);
+    if (row_pos) std::memcpy(row_pos, hb.data() + 1, (size_t)len * 4);
+    if (col_pos) std::memcpy(col_pos, hb.data() + 1 + std::max<int64_t>(k, 1), (size_t)len * 4);
+    return LCSG_OK;
+}
+
+int lcsg_assemble(const uint8_t *rows, int64_t m, const uint8_t *cols, int64_t n,
+                  const int32_t *path, int device, int32_t *length, uint8_t *subseq,
+                  int32_t *row_pos, int32_t *col_pos) {
+    if (!length) return fail(LCSG_EINVAL, "null length pointer");
+    *length = 0;
+    if (m == 0 || n == 0) return LCSG_OK;  // solver.py:219-220
+    int rc = prepare_device(device);
+    if (rc) return rc;
+    DeviceGuard g(device);
+    const int64_t k = std::min(m, n);
+    size_t bytes = align_up(m) + align_up(n) + align_up((m + 1) * 4) + align_up((1 + 2 * k) * 4) + align_up(k);
+    char *buf = nullptr;
+    cudaStream_t s = nullptr;
+    CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    cudaError_t e = cudaMallocAsync((void **)&buf, bytes, s);
+    if (e != cudaSuccess) {
+        cudaStreamDestroy(s);
+        return fail(LCSG_ENOMEM, cudaGetErrorString(e));
+    }
+    uint8_t *d_rows = (uint8_t *)buf;
+    uint8_t *d_cols = (uint8_t *)(buf + align_up(m));
+    int32_t *d_path = (int32_t *)(buf + align_up(m) + align_up(n));
+    int32_t *d_out = (int32_t *)((char *)d_path + align_up((m + 1) * 4));
+    uint8_t *d_sub = (uint8_t *)((char *)d_out + align_up((1 + 2 * k) * 4));
+    std::vector<int32_t> hb((size_t)(1 + 2 * k));
+    e = cudaMemcpyAsync(d_rows, rows, m, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_cols, cols, n, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_path, path, (m + 1) * 4, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) {
+        int r = launch_assemble(d_rows, (int32_t)m, d_cols, (int32_t)n, d_path, d_out, d_out + 1,
+                                d_out + 1 + k, d_sub, s);
+        if (r) e = (cudaError_t)r;
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hb.data(), d_out, hb.size() * 4, cudaMemcpyDeviceToHost, s);
+    std::vector<uint8_t> hs((size_t)k);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(hs.data(), d_sub, (size_t)k, cudaMemcpyDeviceToHost, s);
+    cudaFreeAsync(buf, s);
+    cudaError_t e2 = cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    if (e == cudaSuccess) e = e2;
+    if (e != cudaSuccess) return fail(LCSG_ECUDA, std::string("assemble: ") + cudaGetErrorString(e));
+    *length = hb[0];
+    if (subseq) std::memcpy(subseq, hs.data(), (size_t)hb[0]);
+    if (row_pos) std::memcpy(row_pos, hb.data() + 1, (size_t)hb[0] * 4);
+    if (col_pos) std::memcpy(col_pos, hb.data() + 1 + k, (size_t)hb[0] * 4);
+    return LCSG_OK;
+}
+
+int lcsg_lcs(const uint8_t *a, int64_t la, const uint8_t *b, int64_t lb, uint32_t flags,
+             int device, void *stream, int32_t *length, uint8_t *subseq, int32_t *pos_a,
+             int32_t *pos_b) {
+    return lcs_impl(a, la, b, lb, false, flags, device, stream, length, subseq, pos_a, pos_b);
+}
+
+int lcsg_lcs_device(const uint8_t *a_dev, int64_t la, const uint8_t *b_dev, int64_t lb,
+                    uint32_t flags, int device, void *stream, int32_t *length, uint8_t *subseq,
+                    int32_t *pos_a, int32_t *pos_b) {
+    return lcs_impl(a_dev, la, b_dev, lb, true, flags, device, stream, length, subseq, pos_a, pos_b);
+}
+
+int lcsg_combine_level(const int32_t *upper_reach, int32_t wu1, const int32_t *upper_kmax,
+                       const int32_t *lower_reach, int32_t wl1, int32_t lower_wstar,
+                       int32_t *out_reach, int32_t *out_trace, int32_t w1, int with_trace,
+                       int32_t inf, int64_t n1, int64_t i_lo, int64_t i_hi, void *stream) {
+    if (i_lo < 0 || i_hi > n1 || i_lo > i_hi) return fail(LCSG_EINVAL, "bad row range");
+    if (i_hi == i_lo) return LCSG_OK;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    int rc = prepare_device(dev);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t rows = i_hi - i_lo;
+    struct Scratch {
+        CombineDesc d;
+        int32_t wstar_l, wstar_out;
+    };
+    char *buf = nullptr;
+    CK(cudaMallocAsync((void **)&buf, sizeof(Scratch) + 256 + (size_t)rows * 4, s));
+    Scratch *sc = (Scratch *)buf;
+    int32_t *kmax_scratch = (int32_t *)(buf + align_up(sizeof(Scratch)));
+    Scratch hs;
+    std::memset(&hs, 0, sizeof(hs));
+    hs.d.U = TabDev{upper_reach + i_lo * wu1, upper_kmax + i_lo, nullptr, wu1, -1};
+    hs.d.L = TabDev{lower_reach, nullptr, &sc->wstar_l, wl1, -1};
+    hs.d.out_reach = out_reach + i_lo * w1;
+    hs.d.out_trace = with_trace ? out_trace + i_lo * w1 : nullptr;
+    hs.d.out_kmax = kmax_scratch;
+    hs.d.out_wstar = &sc->wstar_out;
+    hs.d.w1 = w1;
+    hs.wstar_l = lower_wstar;
+    CK(cudaMemcpyAsync(sc, &hs, sizeof(hs), cudaMemcpyHostToDevice, s));
+    Ctx c;
+    c.rows = nullptr;
+    c.nx = nullptr;
+    c.n = (int32_t)(rows - 1);
+    c.inf = inf;
+    const int shift = bits_for(wu1 - 1);
+    const bool key64 = bits_for(inf) + shift > 32;
+    CKL(launch_combine(w1 <= THREAD_KERNEL_MAX_W1 ? 0 : 1, &sc->d, 1, c, shift, key64, s));
+    CK(cudaFreeAsync(buf, s));
+    CK(cudaStreamSynchronize(s));
+    return LCSG_OK;
+}
+
+int lcsg_base_case_row(const uint8_t *cols_dev, int64_t n, uint8_t sym, int32_t *out_dev,
+                       void *stream) {
+    if (n <= 0) return LCSG_OK;
+    CKL(launch_base_case_row(cols_dev, (int32_t)n, sym, out_dev, (cudaStream_t)stream));
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    return LCSG_OK;
+}
+
+int lcsg_stats(lcsg_handle h, int64_t *launches, double *combine_ms, double *leaf_ms,
+               double *total_ms, int64_t *h2d_bytes, int64_t *d2h_bytes) {
+    if (!h) return fail(LCSG_EINVAL, "null handle");
+    DeviceGuard g(h->device);
+    if (launches) *launches = h->launches;
+    float a = 0, b = 0, c = 0;
+    if (h->timing && h->ev_ok) {
+        CK(cudaStreamSynchronize(h->stream));
+        cudaEventElapsedTime(&a, h->ev[1], h->ev[2]);
+        cudaEventElapsedTime(&b, h->ev[0], h->ev[1]);
+        if (cudaEventQuery(h->ev[3]) == cudaSuccess) cudaEventElapsedTime(&c, h->ev[0], h->ev[3]);
+        cudaGetLastError();
+    }
+    if (combine_ms) *combine_ms = a;
+    if (leaf_ms) *leaf_ms = b;
+    if (total_ms) *total_ms = c;
+    if (h2d_bytes) *h2d_bytes = h->h2d_bytes;
+    if (d2h_bytes) *d2h_bytes = h->d2h_bytes;
+    return LCSG_OK;
+}
+
+}  // extern "C"

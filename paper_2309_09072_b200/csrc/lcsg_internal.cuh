@@ -1,0 +1,105 @@
+// lcsg_internal.cuh -- device-side data layout shared by the kernels and the
+// host scheduler of the B200 Lu-Liu LCS path.  See DESIGN.md "Data layout".
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace lcsg {
+
+// A reach table of one slab in HBM (solver.py:32-62 CostTable.reach/kmax):
+// (n+1) x w1 int32, row r = start column r+1, column d = weight d.  Leaves
+// (single string row, solver.py:72-88) are never materialised on the hot
+// path: their weight-1 column is the next-occurrence row NX[sym] (built once
+// per solve by the leaf kernel) and their weight-0 column is r+1.
+struct TabDev {
+    const int32_t *reach;  // nullptr for a leaf
+    const int32_t *kmax;   // nullptr for a leaf
+    const int32_t *wstar;  // device scalar (node_wstar[node])
+    int32_t w1;            // table width = min(slab rows, n) + 1
+    int32_t leaf_row;      // leaf: 0-based index into the slab's row string; else -1
+};
+
+// Per-solve constants, passed by value to every kernel.
+struct Ctx {
+    const uint8_t *rows;  // slab row string (device)
+    const int32_t *nx;    // 256 x (n+1): NX[s][r] = (first q >= r with cols[q]==s) + 2, else n+2
+    int32_t n;
+    int32_t inf;  // n + 2 (seqcore.py:37-39)
+};
+
+// One combine of the recursion (solver.py:91-110): U = upper slab, L = lower.
+struct CombineDesc {
+    TabDev U, L;
+    int32_t *out_reach;  // (n+1) x w1
+    int32_t *out_trace;  // (n+1) x w1 or nullptr (with_trace=False)
+    int32_t *out_kmax;   // n+1
+    int32_t *out_wstar;  // scalar, zero-initialised, atomicMax'ed
+    int32_t w1;
+    int32_t node;
+};
+
+// Resolved accessor of a table inside a kernel.
+struct TabAcc {
+    const int32_t *reach;
+    const int32_t *kmax;
+    const int32_t *nx;  // leaf only
+    int32_t w1;
+};
+
+__device__ __forceinline__ TabAcc resolve(const TabDev &t, const Ctx &c) {
+    TabAcc a;
+    a.reach = t.reach;
+    a.kmax = t.kmax;
+    a.w1 = t.w1;
+    a.nx = t.leaf_row >= 0 ? c.nx + (size_t)c.rows[t.leaf_row] * (size_t)(c.n + 1) : nullptr;
+    return a;
+}
+
+// Entry (r, d) of a table, d <= w1-1 (breakout.py:37-55 for leaves).
+__device__ __forceinline__ int32_t tab_get(const TabAcc &t, int64_t r, int32_t d) {
+    if (t.nx) return d == 0 ? (int32_t)(r + 1) : __ldg(t.nx + r);
+    return __ldg(t.reach + r * (int64_t)t.w1 + d);
+}
+
+// kmax of row r (solver.py:84,104: (reach < inf).sum - 1).
+__device__ __forceinline__ int32_t tab_kmax(const TabAcc &t, int64_t r, int32_t inf) {
+    if (t.nx) return (t.w1 == 2 && __ldg(t.nx + r) < inf) ? 1 : 0;
+    return __ldg(t.kmax + r);
+}
+
+// Recovery walk node (solver.py:180-207).
+struct WalkNode {
+    int32_t top_row, bottom_row;  // absolute 1-based vertex rows
+    int32_t upper, lower;         // child ids (-1 for a leaf)
+    int32_t w1;                   // this node's table width
+    int32_t is_leaf;
+    const int32_t *trace;         // this node's trace (nullptr: retrace)
+    TabDev U, L;                  // children tables (for x = U.reach[i-1,k], retrace)
+};
+
+}  // namespace lcsg
+
+// ---- launchers implemented in lcsg_kernels.cu ------------------------------
+namespace lcsg {
+int launch_nx(const uint8_t *cols, int32_t n, int32_t *nx, int32_t *sym_wstar, cudaStream_t s);
+int launch_leaf_wstar(const uint8_t *rows, const int32_t *leaf_nodes, const int32_t *leaf_rows,
+                      int32_t nleaves, const int32_t *sym_wstar, int32_t *node_wstar,
+                      cudaStream_t s);
+int launch_leaf_table(Ctx c, int32_t leaf_row, int32_t w1, int32_t *reach, int32_t *kmax,
+                      cudaStream_t s);
+int launch_base_case_row(const uint8_t *cols, int32_t n, uint8_t sym, int32_t *out,
+                         cudaStream_t s);
+// kind: 0 = thread-per-row bisection, 1 = warp-per-row bisection
+int launch_combine(int kind, const CombineDesc *descs, int32_t ndesc, Ctx c, int key_shift,
+                   bool key64, cudaStream_t s);
+int launch_walk_level(const WalkNode *nodes, const int32_t *ids, int32_t count, Ctx c,
+                      int32_t *wi, int32_t *wj, int32_t *cols_out, bool retrace, int key_shift,
+                      bool key64, cudaStream_t s);
+int launch_walk_root(const WalkNode *nodes, int32_t root, Ctx c, TabDev root_tab, int32_t j,
+                     int32_t m, int32_t *wi, int32_t *wj, int32_t *cols_out, cudaStream_t s);
+int launch_walk_final(Ctx c, TabDev root_tab, int32_t j, int32_t m, const int32_t *wj_root,
+                      int32_t *cols_out, cudaStream_t s);
+int launch_assemble(const uint8_t *rows, int32_t m, const uint8_t *cols, int32_t n,
+                    const int32_t *path, int32_t *out_len, int32_t *row_pos, int32_t *col_pos,
+                    uint8_t *subseq, cudaStream_t s);
+}  // namespace lcsg

@@ -1,0 +1,545 @@
+// lcsg_kernels.cu -- sm_100a kernels of the Lu-Liu grid-graph LCS hot path.
+//
+//   nx_kernel            leaf step (breakout.py:37-55): per-symbol next-match
+//                        suffix-min with warp shuffles; leaves are read from it
+//   combine_*            recursive combine (_kernel.pyx:14-82): exact emulation
+//                        of the Alg. 1 bisection with packed first-wins keys
+//   walk_* / assemble    extraction (solver.py:160-234)
+//
+// All arithmetic is int32 compare/min; nothing here is GEMM-shaped, so no
+// tensor cores are involved.
+#include <cub/block/block_scan.cuh>
+
+#include "lcsg_internal.cuh"
+
+namespace lcsg {
+
+#define LCSG_LAUNCH_CHECK()                         \
+    do {                                            \
+        cudaError_t e__ = cudaGetLastError();       \
+        if (e__ != cudaSuccess) return (int)e__;    \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// Leaf step: NX[s][r] = (min{q >= r : cols[q] == s}) + 2, INF = n + 2 if none,
+// NX[s][n] = INF.  Entry r is the reference's base_case_row value for start
+// column r+1 (breakout.py:51-55: suffix-min of scattered match positions, +1).
+// One CTA per symbol walks the string right-to-left in 4096-column chunks;
+// inside a chunk each thread takes 4 columns, then a warp-shuffle suffix-min
+// and a cross-warp suffix-min over shared memory build the chunk suffix.
+// ---------------------------------------------------------------------------
+constexpr int NX_THREADS = 1024;
+constexpr int NX_PER_THREAD = 4;
+constexpr int NX_CHUNK = NX_THREADS * NX_PER_THREAD;
+
+__global__ void __launch_bounds__(NX_THREADS) nx_kernel(const uint8_t *__restrict__ cols,
+                                                        int32_t n, int32_t *__restrict__ nx,
+                                                        int32_t *__restrict__ sym_wstar) {
+    const int s = blockIdx.x;
+    const int32_t inf = n + 2;
+    int32_t *row = nx + (size_t)s * (size_t)(n + 1);
+    __shared__ int32_t warp_min[NX_THREADS / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int32_t carry = inf;  // min over everything right of the current chunk
+    if (threadIdx.x == 0) row[n] = inf;
+    for (int64_t base = ((int64_t)(n > 0 ? n - 1 : 0) / NX_CHUNK) * NX_CHUNK; n > 0 && base >= 0;
+         base -= NX_CHUNK) {
+        const int64_t q0 = base + (int64_t)threadIdx.x * NX_PER_THREAD;
+        int32_t v[NX_PER_THREAD];
+#pragma unroll
+        for (int t = NX_PER_THREAD - 1; t >= 0; --t) {
+            const int64_t q = q0 + t;
+            int32_t x = (q < n && cols[q] == (uint8_t)s) ? (int32_t)q + 2 : inf;
+            v[t] = (t == NX_PER_THREAD - 1) ? x : min(x, v[t + 1]);  // thread-local suffix
+        }
+        // warp suffix-min of the thread aggregates (v[0]) via shuffles
+        int32_t agg = v[0];
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            int32_t o = __shfl_down_sync(0xffffffffu, agg, d);
+            if (lane + d < 32) agg = min(agg, o);
+        }
+        // agg = min over lanes [lane, 31]; exclusive = over lanes (lane, 31]
+        int32_t excl = __shfl_down_sync(0xffffffffu, agg, 1);
+        if (lane == 31) excl = inf;
+        if (lane == 0) warp_min[wid] = agg;
+        __syncthreads();
+        int32_t right_warps = inf;  // min over warps > wid
+        for (int w = wid + 1; w < NX_THREADS / 32; ++w) right_warps = min(right_warps, warp_min[w]);
+        const int32_t right = min(min(excl, right_warps), carry);
+#pragma unroll
+        for (int t = 0; t < NX_PER_THREAD; ++t) {
+            const int64_t q = q0 + t;
+            if (q < n) row[q] = min(v[t], right);
+        }
+        int32_t chunk_min = inf;
+        for (int w = 0; w < NX_THREADS / 32; ++w) chunk_min = min(chunk_min, warp_min[w]);
+        carry = min(carry, chunk_min);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) sym_wstar[s] = (n >= 1 && carry < inf) ? 1 : 0;
+}
+
+int launch_nx(const uint8_t *cols, int32_t n, int32_t *nx, int32_t *sym_wstar, cudaStream_t s) {
+    nx_kernel<<<256, NX_THREADS, 0, s>>>(cols, n, nx, sym_wstar);
+    LCSG_LAUNCH_CHECK();
+    return 0;
+}
+
+// wstar of every leaf (solver.py:88): 1 iff its symbol occurs in cols.
+__global__ void leaf_wstar_kernel(const uint8_t *__restrict__ rows,
+                                  const int32_t *__restrict__ leaf_nodes,
+                                  const int32_t *__restrict__ leaf_rows, int32_t nleaves,
+                                  const int32_t *__restrict__ sym_wstar,
+                                  int32_t *__restrict__ node_wstar) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < nleaves) node_wstar[leaf_nodes[t]] = sym_wstar[rows[leaf_rows[t]]];
+}
+
+int launch_leaf_wstar(const uint8_t *rows, const int32_t *leaf_nodes, const int32_t *leaf_rows,
+                      int32_t nleaves, const int32_t *sym_wstar, int32_t *node_wstar,
+                      cudaStream_t s) {
+    if (nleaves <= 0) return 0;
+    leaf_wstar_kernel<<<(nleaves + 255) / 256, 256, 0, s>>>(rows, leaf_nodes, leaf_rows, nleaves,
+                                                            sym_wstar, node_wstar);
+    LCSG_LAUNCH_CHECK();
+    return 0;
+}
+
+// Materialise one leaf table (solver.py:72-88) -- only for API copy-out.
+__global__ void leaf_table_kernel(Ctx c, int32_t leaf_row, int32_t w1, int32_t *reach,
+                                  int32_t *kmax) {
+    int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (r > c.n) return;
+    const int32_t *nx = c.nx + (size_t)c.rows[leaf_row] * (size_t)(c.n + 1);
+    reach[r * w1] = (int32_t)r + 1;
+    int32_t k = 0;
+    if (w1 == 2) {
+        int32_t v = nx[r];
+        reach[r * w1 + 1] = v;
+        k = v < c.inf ? 1 : 0;
+    }
+    kmax[r] = k;
+}
+
+int launch_leaf_table(Ctx c, int32_t leaf_row, int32_t w1, int32_t *reach, int32_t *kmax,
+                      cudaStream_t s) {
+    int64_t n1 = (int64_t)c.n + 1;
+    leaf_table_kernel<<<(unsigned)((n1 + 255) / 256), 256, 0, s>>>(c, leaf_row, w1, reach, kmax);
+    LCSG_LAUNCH_CHECK();
+    return 0;
+}
+
+__global__ void base_case_row_kernel(const uint8_t *cols, int32_t n, uint8_t sym, int32_t *out) {
+    // single-symbol variant of nx_kernel, used by the lcsg_base_case_row mirror
+    __shared__ int32_t warp_min[NX_THREADS / 32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int32_t inf = n + 2;
+    int32_t carry = inf;
+    for (int64_t base = ((int64_t)(n > 0 ? n - 1 : 0) / NX_CHUNK) * NX_CHUNK; n > 0 && base >= 0;
+         base -= NX_CHUNK) {
+        const int64_t q0 = base + (int64_t)threadIdx.x * NX_PER_THREAD;
+        int32_t v[NX_PER_THREAD];
+#pragma unroll
+        for (int t = NX_PER_THREAD - 1; t >= 0; --t) {
+            const int64_t q = q0 + t;
+            int32_t x = (q < n && cols[q] == sym) ? (int32_t)q + 2 : inf;
+            v[t] = (t == NX_PER_THREAD - 1) ? x : min(x, v[t + 1]);
+        }
+        int32_t agg = v[0];
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            int32_t o = __shfl_down_sync(0xffffffffu, agg, d);
+            if (lane + d < 32) agg = min(agg, o);
+        }
+        int32_t excl = __shfl_down_sync(0xffffffffu, agg, 1);
+        if (lane == 31) excl = inf;
+        if (lane == 0) warp_min[wid] = agg;
+        __syncthreads();
+        int32_t right_warps = inf;
+        for (int w = wid + 1; w < NX_THREADS / 32; ++w) right_warps = min(right_warps, warp_min[w]);
+        const int32_t right = min(min(excl, right_warps), carry);
+#pragma unroll
+        for (int t = 0; t < NX_PER_THREAD; ++t) {
+            const int64_t q = q0 + t;
+            if (q < n) out[q] = min(v[t], right);
+        }
+        int32_t chunk_min = inf;
+        for (int w = 0; w < NX_THREADS / 32; ++w) chunk_min = min(chunk_min, warp_min[w]);
+        carry = min(carry, chunk_min);
+        __syncthreads();
+    }
+}
+
+int launch_base_case_row(const uint8_t *cols, int32_t n, uint8_t sym, int32_t *out,
+                         cudaStream_t s) {
+    base_case_row_kernel<<<1, NX_THREADS, 0, s>>>(cols, n, sym, out);
+    LCSG_LAUNCH_CHECK();
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Combine.  Packed first-wins key: (value << shift) | k.  The minimum key is
+// the minimum value and, among ties, the smallest split weight k -- exactly
+// the reference's strict-< linear scan (_kernel.pyx:38-44).
+// ---------------------------------------------------------------------------
+template <typename Key>
+__device__ __forceinline__ Key pack(int32_t v, int32_t k, int shift) {
+    return ((Key)(uint32_t)v << shift) | (Key)(uint32_t)k;
+}
+template <typename Key>
+__device__ __forceinline__ int32_t key_val(Key key, int shift) {
+    return (int32_t)(key >> shift);
+}
+template <typename Key>
+__device__ __forceinline__ int32_t key_k(Key key, int shift) {
+    return (int32_t)(key & (((Key)1 << shift) - 1));
+}
+
+__device__ __forceinline__ uint32_t warp_min(uint32_t v) { return __reduce_min_sync(0xffffffffu, v); }
+__device__ __forceinline__ uint64_t warp_min(uint64_t v) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+        uint64_t o = __shfl_xor_sync(0xffffffffu, v, d);
+        v = o < v ? o : v;
+    }
+    return v;
+}
+
+// cell_value (_kernel.pyx:14-25) for start row i (0-based) with x = U[i,k].
+__device__ __forceinline__ int32_t cell(const TabAcc &L, int32_t x, int32_t k, int32_t j,
+                                        int32_t inf, int32_t wl) {
+    if (k > j) return inf;
+    if (x >= inf) return inf;
+    if (j - k > wl) return inf;
+    return tab_get(L, (int64_t)x - 1, j - k);
+}
+
+// Thread-per-row exact bisection (small tables): the reference's col_mins
+// (_kernel.pyx:28-60) as an iterative DFS with an explicit right-sibling stack.
+constexpr int STACK = 24;
+
+template <typename Key>
+__global__ void __launch_bounds__(256) combine_thread_kernel(const CombineDesc *__restrict__ descs,
+                                                             int32_t ndesc, Ctx c, int shift,
+                                                             int64_t rows_pad) {
+    const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t di = gid / rows_pad;  // warp-uniform: rows_pad % 32 == 0
+    if (di >= ndesc) return;
+    const int64_t i = gid - di * rows_pad;
+    const int64_t n1 = (int64_t)c.n + 1;
+    const CombineDesc &d = descs[di];
+    const int32_t inf = c.inf;
+    int32_t kfin = -1;
+    if (i < n1) {
+        const TabAcc U = resolve(d.U, c), L = resolve(d.L, c);
+        const int32_t w = d.w1 - 1, wl = L.w1 - 1;
+        const int32_t kmaxU = tab_kmax(U, i, inf);
+        const int32_t wstarL = *d.L.wstar;
+        int32_t colhi = min(w, kmaxU + wstarL);
+        int32_t *reach = d.out_reach + i * d.w1;
+        int32_t *trace = d.out_trace ? d.out_trace + i * d.w1 : nullptr;
+        uint64_t stk[STACK];
+        int sp = 0;
+        int32_t left = 0, right = colhi, top = 0, bottom = kmaxU;
+        for (;;) {
+            while (right >= left) {
+                const int32_t mid = (left + right + 1) >> 1;
+                Key best = ~(Key)0;
+                for (int32_t k = top; k <= bottom; ++k) {
+                    const int32_t x = tab_get(U, i, k);
+                    const Key key = pack<Key>(cell(L, x, k, mid, inf, wl), k, shift);
+                    best = key < best ? key : best;
+                }
+                const int32_t bv = key_val<Key>(best, shift), bk = key_k<Key>(best, shift);
+                reach[mid] = bv;
+                if (trace) trace[mid] = bk;
+                if (bv != inf) {
+                    kfin = max(kfin, mid);
+                    if (mid + 1 <= right && sp < STACK)
+                        stk[sp++] = ((uint64_t)(uint16_t)(mid + 1) << 48) |
+                                    ((uint64_t)(uint16_t)right << 32) |
+                                    ((uint64_t)(uint16_t)bk << 16) | (uint64_t)(uint16_t)bottom;
+                    right = mid - 1;
+                    bottom = bk;
+                } else {
+                    for (int32_t q = mid + 1; q <= right; ++q) {
+                        reach[q] = inf;
+                        if (trace) trace[q] = top;
+                    }
+                    right = mid - 1;
+                }
+            }
+            if (sp == 0) break;
+            const uint64_t e = stk[--sp];
+            left = (int32_t)(uint16_t)(e >> 48);
+            right = (int32_t)(uint16_t)(e >> 32);
+            top = (int32_t)(uint16_t)(e >> 16);
+            bottom = (int32_t)(uint16_t)e;
+        }
+        for (int32_t q = colhi + 1; q <= w; ++q) {
+            reach[q] = inf;
+            if (trace) trace[q] = 0;
+        }
+        d.out_kmax[i] = kfin;
+    }
+    // kfin == last finite column == kmax of the row (finite prefix property)
+    const int32_t wmax = __reduce_max_sync(0xffffffffu, kfin);
+    if ((threadIdx.x & 31) == 0 && wmax >= 0) atomicMax(d.out_wstar, wmax);
+}
+
+// Warp-per-row exact bisection: the warp evaluates one Alg. 1 node at a time,
+// lanes striding over its row range [top..bottom] and reducing packed keys
+// with a warp min (REDUX.MIN for 32-bit keys).  The DFS stack is warp-uniform
+// and lives in shared memory.
+constexpr int WARP_KERNEL_WARPS = 8;
+constexpr int WSTACK = 34;  // > log2(max colhi) + 1 for colhi < 2^32
+
+template <typename Key>
+__global__ void __launch_bounds__(32 * WARP_KERNEL_WARPS)
+    combine_warp_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int shift) {
+    __shared__ int4 stk_all[WARP_KERNEL_WARPS][WSTACK];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    int4 *stk = stk_all[wid];
+    const int64_t n1 = (int64_t)c.n + 1;
+    const int64_t gw = blockIdx.x * (int64_t)WARP_KERNEL_WARPS + wid;
+    const int64_t di = gw / n1;
+    if (di >= ndesc) return;
+    const int64_t i = gw - di * n1;
+    const CombineDesc &d = descs[di];
+    const int32_t inf = c.inf;
+    const TabAcc U = resolve(d.U, c), L = resolve(d.L, c);
+    const int32_t w = d.w1 - 1, wl = L.w1 - 1;
+    const int32_t kmaxU = tab_kmax(U, i, inf);
+    const int32_t wstarL = *d.L.wstar;
+    const int32_t colhi = min(w, kmaxU + wstarL);
+    int32_t *reach = d.out_reach + i * d.w1;
+    int32_t *trace = d.out_trace ? d.out_trace + i * d.w1 : nullptr;
+    int sp = 0;
+    int32_t kfin = -1;
+    int32_t left = 0, right = colhi, top = 0, bottom = kmaxU;
+    for (;;) {
+        while (right >= left) {
+            const int32_t mid = (left + right + 1) >> 1;
+            Key best = ~(Key)0;
+            for (int32_t k = top + lane; k <= bottom; k += 32) {
+                const int32_t x = tab_get(U, i, k);
+                const Key key = pack<Key>(cell(L, x, k, mid, inf, wl), k, shift);
+                best = key < best ? key : best;
+            }
+            best = warp_min(best);
+            const int32_t bv = key_val<Key>(best, shift), bk = key_k<Key>(best, shift);
+            if (lane == 0) {
+                reach[mid] = bv;
+                if (trace) trace[mid] = bk;
+            }
+            if (bv != inf) {
+                kfin = max(kfin, mid);
+                if (mid + 1 <= right) {
+                    if (lane == 0) stk[sp] = make_int4(mid + 1, right, bk, bottom);
+                    ++sp;
+                }
+                right = mid - 1;
+                bottom = bk;
+            } else {
+                for (int32_t q = mid + 1 + lane; q <= right; q += 32) {
+                    reach[q] = inf;
+                    if (trace) trace[q] = top;
+                }
+                right = mid - 1;
+            }
+        }
+        if (sp == 0) break;
+        __syncwarp();
+        const int4 e = stk[--sp];
+        __syncwarp();
+        left = e.x;
+        right = e.y;
+        top = e.z;
+        bottom = e.w;
+    }
+    for (int32_t q = colhi + 1 + lane; q <= w; q += 32) {
+        reach[q] = inf;
+        if (trace) trace[q] = 0;
+    }
+    if (lane == 0) {
+        d.out_kmax[i] = kfin;
+        atomicMax(d.out_wstar, kfin);
+    }
+}
+
+int launch_combine(int kind, const CombineDesc *descs, int32_t ndesc, Ctx c, int key_shift,
+                   bool key64, cudaStream_t s) {
+    if (ndesc <= 0) return 0;
+    const int64_t n1 = (int64_t)c.n + 1;
+    if (kind == 0) {
+        const int64_t rows_pad = (n1 + 31) / 32 * 32;
+        const int64_t threads = rows_pad * ndesc;
+        const unsigned blocks = (unsigned)((threads + 255) / 256);
+        if (key64)
+            combine_thread_kernel<uint64_t><<<blocks, 256, 0, s>>>(descs, ndesc, c, key_shift, rows_pad);
+        else
+            combine_thread_kernel<uint32_t><<<blocks, 256, 0, s>>>(descs, ndesc, c, key_shift, rows_pad);
+    } else {
+        const int64_t warps = n1 * ndesc;
+        const unsigned blocks = (unsigned)((warps + WARP_KERNEL_WARPS - 1) / WARP_KERNEL_WARPS);
+        if (key64)
+            combine_warp_kernel<uint64_t><<<blocks, 32 * WARP_KERNEL_WARPS, 0, s>>>(descs, ndesc, c, key_shift);
+        else
+            combine_warp_kernel<uint32_t><<<blocks, 32 * WARP_KERNEL_WARPS, 0, s>>>(descs, ndesc, c, key_shift);
+    }
+    LCSG_LAUNCH_CHECK();
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Extraction.  Recovery walk (solver.py:180-207), one launch per tree depth:
+// node (i, jj) -> k = trace[i-1, jj] (or the low-memory first-wins retrace,
+// solver.py:165-177), x = U.reach[i-1, k]; children get (i, k) and (x, jj-k);
+// a leaf child records cols[top_row-1] = i.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void walk_children(const WalkNode &nd, const WalkNode *nodes, Ctx c,
+                                              int32_t i, int32_t jj, int32_t k, int32_t *wi,
+                                              int32_t *wj, int32_t *cols_out) {
+    const TabAcc U = resolve(nd.U, c);
+    const int32_t x = tab_get(U, (int64_t)i - 1, k);
+    const WalkNode &up = nodes[nd.upper];
+    const WalkNode &lo = nodes[nd.lower];
+    if (up.is_leaf) cols_out[up.top_row - 1] = i;
+    else { wi[nd.upper] = i; wj[nd.upper] = k; }
+    if (lo.is_leaf) cols_out[lo.top_row - 1] = x;
+    else { wi[nd.lower] = x; wj[nd.lower] = jj - k; }
+}
+
+__global__ void walk_trace_kernel(const WalkNode *__restrict__ nodes, const int32_t *__restrict__ ids,
+                                  int32_t count, Ctx c, int32_t *wi, int32_t *wj, int32_t *cols_out) {
+    int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= count) return;
+    const int32_t id = ids[t];
+    const WalkNode nd = nodes[id];
+    const int32_t i = wi[id], jj = wj[id];
+    const int32_t k = nd.trace[((int64_t)i - 1) * nd.w1 + jj];
+    walk_children(nd, nodes, c, i, jj, k, wi, wj, cols_out);
+}
+
+template <typename Key>
+__global__ void walk_retrace_kernel(const WalkNode *__restrict__ nodes, const int32_t *__restrict__ ids,
+                                    int32_t count, Ctx c, int32_t *wi, int32_t *wj,
+                                    int32_t *cols_out, int shift) {
+    const int lane = threadIdx.x & 31;
+    const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    if (t >= count) return;
+    const int32_t id = ids[t];
+    const WalkNode nd = nodes[id];
+    const int32_t i = wi[id], jj = wj[id];
+    const TabAcc U = resolve(nd.U, c), L = resolve(nd.L, c);
+    const int32_t inf = c.inf;
+    const int32_t hi = min(jj, tab_kmax(U, (int64_t)i - 1, inf));
+    Key best = ~(Key)0;
+    for (int32_t k = lane; k <= hi; k += 32) {
+        // compose_cell (monotone.py:46-63)
+        const int32_t x = tab_get(U, (int64_t)i - 1, k);
+        int32_t v = inf;
+        const int32_t dd = jj - k;
+        if (x < inf && dd < L.w1) v = tab_get(L, (int64_t)x - 1, dd);
+        const Key key = pack<Key>(v, k, shift);
+        best = key < best ? key : best;
+    }
+    best = warp_min(best);
+    if (lane == 0) walk_children(nd, nodes, c, i, jj, key_k<Key>(best, shift), wi, wj, cols_out);
+}
+
+int launch_walk_level(const WalkNode *nodes, const int32_t *ids, int32_t count, Ctx c,
+                      int32_t *wi, int32_t *wj, int32_t *cols_out, bool retrace, int key_shift,
+                      bool key64, cudaStream_t s) {
+    if (count <= 0) return 0;
+    if (!retrace) {
+        walk_trace_kernel<<<(count + 127) / 128, 128, 0, s>>>(nodes, ids, count, c, wi, wj, cols_out);
+    } else {
+        const unsigned blocks = (unsigned)(((int64_t)count * 32 + 127) / 128);
+        if (key64)
+            walk_retrace_kernel<uint64_t><<<blocks, 128, 0, s>>>(nodes, ids, count, c, wi, wj, cols_out, key_shift);
+        else
+            walk_retrace_kernel<uint32_t><<<blocks, 128, 0, s>>>(nodes, ids, count, c, wi, wj, cols_out, key_shift);
+    }
+    LCSG_LAUNCH_CHECK();
+    return 0;
+}
+
+// Root of the walk: j < 0 means "the LCS length" = kmax[0] of the root
+// (solver.py:160-162), read on the device so no host round trip is needed.
+__global__ void walk_root_kernel(const WalkNode *nodes, int32_t root, Ctx c, TabDev root_tab,
+                                 int32_t j, int32_t *wi, int32_t *wj, int32_t *cols_out) {
+    const TabAcc R = resolve(root_tab, c);
+    const int32_t jj = j >= 0 ? j : tab_kmax(R, 0, c.inf);
+    wi[root] = 1;
+    wj[root] = jj;
+    if (nodes[root].is_leaf) cols_out[nodes[root].top_row - 1] = 1;
+}
+
+int launch_walk_root(const WalkNode *nodes, int32_t root, Ctx c, TabDev root_tab, int32_t j,
+                     int32_t m, int32_t *wi, int32_t *wj, int32_t *cols_out, cudaStream_t s) {
+    (void)m;
+    walk_root_kernel<<<1, 1, 0, s>>>(nodes, root, c, root_tab, j, wi, wj, cols_out);
+    LCSG_LAUNCH_CHECK();
+    return 0;
+}
+
+// cols[m] = table.reach[0, j] (solver.py:206)
+__global__ void walk_final_kernel(Ctx c, TabDev root_tab, int32_t m, const int32_t *wj_root,
+                                  int32_t *cols_out) {
+    const TabAcc R = resolve(root_tab, c);
+    cols_out[m] = tab_get(R, 0, *wj_root);
+}
+
+int launch_walk_final(Ctx c, TabDev root_tab, int32_t j, int32_t m, const int32_t *wj_root,
+                      int32_t *cols_out, cudaStream_t s) {
+    (void)j;
+    walk_final_kernel<<<1, 1, 0, s>>>(c, root_tab, m, wj_root, cols_out);
+    LCSG_LAUNCH_CHECK();
+    return 0;
+}
+
+// assemble_lcs (solver.py:210-234): mark + block scan + compact, one CTA.
+constexpr int ASM_THREADS = 1024;
+__global__ void __launch_bounds__(ASM_THREADS)
+    assemble_kernel(const uint8_t *__restrict__ rows, int32_t m, const uint8_t *__restrict__ cols,
+                    int32_t n, const int32_t *__restrict__ path, int32_t *out_len,
+                    int32_t *row_pos, int32_t *col_pos, uint8_t *subseq) {
+    using Scan = cub::BlockScan<int32_t, ASM_THREADS>;
+    __shared__ typename Scan::TempStorage tmp;
+    int32_t carry = 0;
+    if (m > 0 && n > 0) {
+        for (int32_t base = 0; base < m; base += ASM_THREADS) {
+            const int32_t r = base + threadIdx.x;
+            int32_t mark = 0, cur = 0;
+            if (r < m) {
+                const int32_t prev = path[r];
+                cur = path[r + 1];
+                int32_t land = cur - 2;
+                land = land < 0 ? 0 : (land > n - 1 ? n - 1 : land);
+                mark = (cur > prev) && (rows[r] == cols[land]);
+            }
+            int32_t pos, total;
+            Scan(tmp).ExclusiveSum(mark, pos, total);
+            if (mark) {
+                subseq[carry + pos] = rows[r];
+                row_pos[carry + pos] = r + 1;
+                col_pos[carry + pos] = cur - 1;
+            }
+            carry += total;
+            __syncthreads();
+        }
+    }
+    if (threadIdx.x == 0) *out_len = carry;
+}
+
+int launch_assemble(const uint8_t *rows, int32_t m, const uint8_t *cols, int32_t n,
+                    const int32_t *path, int32_t *out_len, int32_t *row_pos, int32_t *col_pos,
+                    uint8_t *subseq, cudaStream_t s) {
+    assemble_kernel<<<1, ASM_THREADS, 0, s>>>(rows, m, cols, n, path, out_len, row_pos, col_pos, subseq);
+    LCSG_LAUNCH_CHECK();
+    return 0;
+}
+
+}  // namespace lcsg

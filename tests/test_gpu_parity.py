@@ -1,0 +1,257 @@
+"""Parity of the CUDA path (through the C-ABI) against the oracle / reference
+goldens -- the parity tests proper.  Bit-exact: integer work.
+
+Every comparison below is against (a) fixtures produced by the REAL
+reference (tests/golden/, make_golden.py) or (b) the C oracle, which
+tests/test_oracle.py pins to those fixtures.
+"""
+
+import ctypes
+import hashlib
+import json
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2309_09072_b200 as L
+import workloads
+from paper_2309_09072_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+PAPER_COLS, PAPER_ROWS = "gatttatgcagg", "tcaggatt"
+
+
+def gpu_tree_nodes(table):
+    """Post-order (upper, lower, self) list of a device CostTable tree."""
+    out = []
+
+    def rec(t):
+        if t.upper is not None:
+            rec(t.upper)
+            rec(t.lower)
+        out.append(t)
+
+    rec(table)
+    return out
+
+
+def compare_nodes(gpu_nodes, exp_nodes, trace=True):
+    assert len(gpu_nodes) == len(exp_nodes)
+    for idx, (g, e) in enumerate(zip(gpu_nodes, exp_nodes)):
+        assert (g.top_row, g.bottom_row) == (e["top"], e["bottom"]), idx
+        np.testing.assert_array_equal(g.reach, e["reach"], err_msg=f"reach node {idx}")
+        np.testing.assert_array_equal(g.kmax, e["kmax"], err_msg=f"kmax node {idx}")
+        assert g.wstar == e["wstar"], idx
+        if trace and e["trace"] is not None:
+            np.testing.assert_array_equal(g.trace, e["trace"], err_msg=f"trace node {idx}")
+
+
+def test_device_visible():
+    assert _lib.load().lcsg_device_count() >= 1
+
+
+def test_paper_grid(paper_tree, spec_examples):
+    trees, _, extra = paper_tree
+    g = L.GridModel(PAPER_ROWS, PAPER_COLS)
+    tab = L.build_cost_table(g, 1, g.m + 1)
+    compare_nodes(gpu_tree_nodes(tab), trees["paper"])
+    assert L.lcs_length(tab) == spec_examples["paper_length"]
+    assert int(L.recover_cross_vertices(g, tab, 5)[-1]) == spec_examples["paper_end_column"]
+    assert L.recover_cross_vertices(g, tab, 0).tolist() == [1] * 9
+    exp = json.loads(bytes(extra["paper/lcs"]).decode())
+    r = L.lcs(PAPER_COLS, PAPER_ROWS)
+    assert (r.length, r.subsequence.hex(), list(r.row_positions), list(r.col_positions)) == (
+        exp["length"], exp["subsequence"], exp["row_positions"], exp["col_positions"])
+
+
+def test_reference_trees_every_node(ref_trees):
+    trees, meta, _ = ref_trees
+    for idx, mt in enumerate(meta):
+        g = L.GridModel(bytes.fromhex(mt["rows"]), bytes.fromhex(mt["cols"]))
+        tab = L.build_cost_table(g, mt["top"], mt["bottom"])
+        compare_nodes(gpu_tree_nodes(tab), trees[f"t{idx}"])
+
+
+def test_reference_cfg1_tree_every_node(ref_trees):
+    trees, _, _ = ref_trees
+    a, b = workloads.generate(1)
+    g = L.GridModel(a, b)
+    compare_nodes(gpu_tree_nodes(L.build_cost_table(g, 1, g.m + 1)), trees["cfg1"])
+
+
+def test_reference_lcs_pairs(ref_lcs_pairs):
+    for p in ref_lcs_pairs:
+        a, b = bytes.fromhex(p["a"]), bytes.fromhex(p["b"])
+        for low in (False, True):
+            r = L.lcs(a, b, low_memory=low)
+            assert (r.length, r.subsequence.hex(), list(r.row_positions),
+                    list(r.col_positions)) == (p["length"], p["subsequence"],
+                                               p["row_positions"], p["col_positions"]), (p, low)
+
+
+def test_random_against_oracle_trees():
+    rng = np.random.default_rng(11)
+    for it in range(60):
+        m = int(rng.integers(1, 200))
+        n = int(rng.integers(0, 300))
+        sigma = int(rng.choice([2, 4, 20, 26, 200]))
+        a, b = workloads.random_pair(rng, m, n, sigma, base=int(rng.integers(0, 50)))
+        g = L.GridModel(a, b)
+        tab = L.build_cost_table(g, 1, m + 1)
+        t = O.OracleTree(a, b)
+        root = t.node(t.root)
+        np.testing.assert_array_equal(tab.reach, root.reach)
+        if root.trace is not None:
+            np.testing.assert_array_equal(tab.trace, root.trace)
+        np.testing.assert_array_equal(tab.kmax, root.kmax)
+        length = L.lcs_length(tab)
+        assert length == int(root.kmax[0])
+        for j in sorted({0, length, length // 2, max(0, length - 1)}):
+            np.testing.assert_array_equal(L.recover_cross_vertices(g, tab, j), t.recover(j))
+
+
+def test_low_memory_tables_and_retrace():
+    rng = np.random.default_rng(12)
+    for _ in range(20):
+        m, n = int(rng.integers(2, 150)), int(rng.integers(2, 200))
+        a, b = workloads.random_pair(rng, m, n, int(rng.choice([2, 4, 26])))
+        g = L.GridModel(a, b)
+        lo = L.build_cost_table(g, 1, m + 1, with_trace=False)
+        hi = L.build_cost_table(g, 1, m + 1, with_trace=True)
+        assert lo.trace is None
+        np.testing.assert_array_equal(lo.reach, hi.reach)
+        length = L.lcs_length(lo)
+        for j in (0, length):
+            np.testing.assert_array_equal(L.recover_cross_vertices(g, lo, j),
+                                          L.recover_cross_vertices(g, hi, j))
+
+
+def test_edge_cases():
+    # n = 0 -> D_G [[1]]; m = 1 single leaf; m > n direct build
+    g = L.GridModel("abc", "")
+    tab = L.build_cost_table(g, 1, 4)
+    assert tab.reach.tolist() == [[1]]
+    g = L.GridModel("a", "xax")
+    tab = L.build_cost_table(g, 1, 2)
+    assert tab.reach.tolist() == [[1, 3], [2, 3], [3, 5], [4, 5]]
+    assert L.recover_cross_vertices(g, tab, 1).tolist() == [1, 3]
+    for a, b in (("zzzzzzzz", "zz"), ("abcdefgh", "hgf"), ("a" * 70, "a" * 90)):
+        g = L.GridModel(a, b)
+        t = O.OracleTree(a, b)
+        np.testing.assert_array_equal(L.build_cost_table(g, 1, g.m + 1).reach,
+                                      t.node(t.root).reach)
+    assert L.lcs("abcabba", "abcabba").subsequence == b"abcabba"
+    assert L.lcs("abcd", "efgh").length == 0
+    full = bytes(range(256))
+    r = L.lcs(full, full[::-1] + full)
+    assert r.length == 256 and r.subsequence == full
+    g = L.GridModel(PAPER_ROWS, PAPER_COLS)
+    tab = L.build_cost_table(g, 1, g.m + 1)
+    with pytest.raises(ValueError, match="no path of weight 6"):
+        L.recover_cross_vertices(g, tab, 6)
+    sub = L.build_cost_table(g, 2, 6)
+    with pytest.raises(ValueError, match="full-grid"):
+        L.recover_cross_vertices(g, sub, 1)
+
+
+def test_kernel_mirrors():
+    import torch
+
+    rng = np.random.default_rng(5)
+    for _ in range(10):
+        n = int(rng.integers(1, 500))
+        cols = workloads.random_pair(rng, 1, n, 4)[1]
+        d_cols = torch.from_numpy(np.frombuffer(cols, dtype=np.uint8).copy()).cuda()
+        out = torch.empty(n, dtype=torch.int32, device="cuda")
+        for sym in b"abcz":
+            rc = _lib.load().lcsg_base_case_row(d_cols.data_ptr(), n, sym, out.data_ptr(), None)
+            _lib.check(rc)
+            np.testing.assert_array_equal(out.cpu().numpy(), O.base_case_row(cols, sym))
+    # combine_level mirror on real upper/lower tables of an oracle tree
+    for _ in range(6):
+        m, n = int(rng.integers(4, 120)), int(rng.integers(4, 260))
+        a, b = workloads.random_pair(rng, m, n, int(rng.choice([2, 4, 26])))
+        t = O.OracleTree(a, b)
+        root = t.node(t.root)
+        U, Lo = t.node(root.upper), t.node(root.lower)
+        exp_r, exp_t, _ = O.combine_level(U.reach, U.kmax, Lo.reach, Lo.wstar, root.reach.shape[1],
+                                          t.inf)
+        dU = torch.from_numpy(U.reach).cuda()
+        dK = torch.from_numpy(U.kmax).cuda()
+        dL = torch.from_numpy(Lo.reach).cuda()
+        r = torch.zeros_like(torch.from_numpy(exp_r)).cuda()
+        tr = torch.zeros_like(r)
+        i_lo, i_hi = 1, n + 1
+        rc = _lib.load().lcsg_combine_level(
+            dU.data_ptr(), U.reach.shape[1], dK.data_ptr(), dL.data_ptr(), Lo.reach.shape[1],
+            Lo.wstar, r.data_ptr(), tr.data_ptr(), exp_r.shape[1], 1, t.inf, n + 1, i_lo, i_hi,
+            None)
+        _lib.check(rc)
+        np.testing.assert_array_equal(r.cpu().numpy()[i_lo:i_hi], exp_r[i_lo:i_hi])
+        np.testing.assert_array_equal(tr.cpu().numpy()[i_lo:i_hi], exp_t[i_lo:i_hi])
+
+
+def test_assemble_and_device_view():
+    rng = np.random.default_rng(6)
+    for _ in range(10):
+        m, n = int(rng.integers(1, 90)), int(rng.integers(1, 120))
+        a, b = workloads.random_pair(rng, m, n, 4)
+        g = L.GridModel(a, b)
+        tab = L.build_cost_table(g, 1, m + 1)
+        path = L.recover_cross_vertices(g, tab, L.lcs_length(tab))
+        r = L.assemble_lcs(g, path)
+        assert (r.length, r.subsequence, r.row_positions, r.col_positions) == O.assemble(a, b, path)
+        np.testing.assert_array_equal(tab.reach_device.cpu().numpy(), tab.reach)
+
+
+def _check_digest(exp, a, b, low_memory=False):
+    r = L.lcs(a, b, low_memory=low_memory)
+    assert r.length == exp["length"]
+    assert hashlib.sha256(r.subsequence).hexdigest() == exp["subsequence_sha256"]
+    pos = np.array(r.row_positions + r.col_positions, dtype=np.int64).tobytes()
+    assert hashlib.sha256(pos).hexdigest() == exp["positions_sha256"]
+    rows, cols = (b, a) if len(a) > len(b) else (a, b)
+    g = L.GridModel(rows, cols)
+    tab = L.build_cost_table(g, 1, g.m + 1, with_trace=False)
+    assert hashlib.sha256(tab.reach.tobytes()).hexdigest() == exp["dg_sha256"]
+
+
+@pytest.mark.parametrize("key", ["cfg1/seed0", "cfg1/seed1", "cfg1/seed2", "cfg2/seed0",
+                                 "cfg2/seed1", "cfg2/seed2", "cfg3/seed0", "cfg3/seed1",
+                                 "cfg3/seed2", "cfg4/seed0", "cfg5/seed0"])
+def test_config_digests(config_digests, key):
+    if key not in config_digests:
+        pytest.skip(f"{key} digest not generated")
+    cfg, seed = int(key[3]), int(key.split("seed")[1])
+    a, b = workloads.generate(cfg, seed)
+    _check_digest(config_digests[key], a, b, low_memory=(cfg == 5))
+
+
+def _dg_row_by_definition(rows: bytes, cols: bytes, i: int, w1: int) -> np.ndarray:
+    """Independent D_G row: D(i,j) = i + min{t :
+    LCS(rows, cols[i-1:i-1+t]) >= j}, INF if none -- one numpy DP sweep."""
+    from paper_2309_09072_b200.dp import _table
+    n = len(cols)
+    H = _table(rows, cols[i - 1:])[-1]  # H[t] = LCS(rows, cols[i-1:i-1+t])
+    out = np.full(w1, n + 2, dtype=np.int64)
+    for j in range(w1):
+        hit = np.flatnonzero(H >= j)
+        if len(hit):
+            out[j] = i + hit[0]
+    return out
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_dg_rows_by_definition(cfg):
+    """Size-independent property at config scale: random rows of the final
+    D_G equal the breakout definition computed by a plain DP."""
+    a, b = workloads.generate(cfg)
+    rows, cols = (b, a) if len(a) > len(b) else (a, b)
+    g = L.GridModel(rows, cols)
+    tab = L.build_cost_table(g, 1, g.m + 1, with_trace=False)
+    R = tab.reach
+    rng = np.random.default_rng(cfg)
+    for i in [1, len(cols) + 1] + [int(x) for x in rng.integers(1, len(cols) + 2, 3)]:
+        np.testing.assert_array_equal(R[i - 1], _dg_row_by_definition(rows, cols, i, R.shape[1]))
