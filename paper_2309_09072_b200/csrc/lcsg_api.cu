@@ -77,19 +77,32 @@ int prepare_device(int device) {
     return LCSG_OK;
 }
 
-// thread-per-row bisection below this table width, warp-per-row above
+// Kernel choice per combine:
+//   kind 0: thread-per-row exact bisection        (w1 <= THREAD_KERNEL_MAX_W1)
+//   kind 2: skeleton (exact bisection, CTA/row) + refinement passes (wider)
+//   kind 1: warp-per-row exact bisection          (fallback: U row too big for smem)
 constexpr int32_t THREAD_KERNEL_MAX_W1 = 65;
+constexpr int64_t REFINE_MAX_USTRIDE = 200 * 1024 / 4;
+
+int env_int(const char *name, int def) {
+    const char *v = getenv(name);
+    return v && *v ? atoi(v) : def;
+}
 
 struct NodeH {
     int32_t top_row, bottom_row, w1, upper, lower, height, depth, leaf_row;
     int64_t reach_off = -1, trace_off = -1, kmax_off = -1;  // int32 element offsets
+    int kind = 0;
 };
 
 struct LaunchH {
-    int kind;
+    int kind;  // 0 thread, 1 warp, 3 skeleton, 4 refine pass
     int32_t desc_off, count;
     int shift;
     bool key64;
+    int32_t stride_or_delta = 0;
+    int wpr_log2 = 0;
+    int32_t ustride = 0;
 };
 
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
@@ -255,12 +268,18 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     size_t o_out = take((size_t)(1 + 2 * std::max<int64_t>(kmin, 1)) * 4);
     size_t o_sub = take((size_t)std::max<int64_t>(kmin, 1));
     // int32 tables of every combine node
+    const int skel_stride = std::max(1, env_int("LCSG_SKELETON_STRIDE", 16));
     size_t o_tab = off;
     int64_t tab_elems = 0;
     int32_t ncomb = 0;
+    int32_t maxh0 = 0;
     for (auto &nd : t->nodes) {
         if (nd.upper < 0) { t->nleaves++; continue; }
         ++ncomb;
+        maxh0 = std::max(maxh0, nd.height);
+        const int32_t wu1 = t->nodes[nd.upper].w1;
+        nd.kind = nd.w1 <= THREAD_KERNEL_MAX_W1 ? 0 : (wu1 <= REFINE_MAX_USTRIDE ? 2 : 1);
+        if (skel_stride == 1 && nd.kind == 2) nd.kind = 1;
         nd.reach_off = tab_elems;
         tab_elems += n1 * nd.w1;
         if (t->with_trace) {
@@ -270,6 +289,20 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
         nd.kmax_off = tab_elems;
         tab_elems += (n1 + 63) / 64 * 64;
     }
+    // low-memory mode: the refinement passes still need this level's traces
+    // (they bound neighbouring rows); one scratch region reused level by level
+    int64_t scratch_elems = 0;
+    std::vector<int64_t> level_scratch(maxh0 + 1, 0);
+    if (!t->with_trace) {
+        for (auto &nd : t->nodes)
+            if (nd.upper >= 0 && nd.kind == 2) {
+                nd.trace_off = level_scratch[nd.height];  // relative to the scratch base
+                level_scratch[nd.height] += n1 * nd.w1;
+            }
+        for (int64_t v : level_scratch) scratch_elems = std::max(scratch_elems, v);
+    }
+    const int64_t scratch_base = tab_elems;
+    tab_elems += scratch_elems;
     off = align_up(o_tab + (size_t)tab_elems * 4);
     // metadata region (uploaded with one copy)
     size_t o_meta = off;
@@ -319,33 +352,52 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     const int vbits = bits_for(t->inf);
     int32_t di = 0;
     for (int32_t h = 1; h <= maxh; ++h) {
-        for (int kind = 0; kind < 2; ++kind) {
+        for (int kind = 0; kind < 3; ++kind) {
             int32_t start = di;
-            int32_t maxk = 0;
+            int32_t maxk = 0, maxw1 = 0;
             for (int32_t id = 0; id < nn; ++id) {
                 const NodeH &nd = t->nodes[id];
-                if (nd.height != h) continue;
-                int k = nd.w1 <= THREAD_KERNEL_MAX_W1 ? 0 : 1;
-                if (k != kind) continue;
+                if (nd.height != h || nd.kind != kind) continue;
                 CombineDesc &d = hd[di++];
                 d.U = t->tab(nd.upper);
                 d.L = t->tab(nd.lower);
                 d.out_reach = t->d_tables + nd.reach_off;
-                d.out_trace = t->with_trace ? t->d_tables + nd.trace_off : nullptr;
+                d.out_trace = t->with_trace ? t->d_tables + nd.trace_off
+                              : (kind == 2 ? t->d_tables + scratch_base + nd.trace_off : nullptr);
                 d.out_kmax = t->d_tables + nd.kmax_off;
                 d.out_wstar = t->d_node_wstar + id;
                 d.w1 = nd.w1;
                 d.node = id;
                 maxk = std::max(maxk, t->nodes[nd.upper].w1 - 1);
+                maxw1 = std::max(maxw1, nd.w1);
             }
-            if (di > start) {
-                LaunchH L;
+            if (di == start) continue;
+            LaunchH L;
+            L.desc_off = start;
+            L.count = di - start;
+            L.shift = bits_for(maxk);
+            L.key64 = vbits + L.shift > 32;
+            if (kind < 2) {
                 L.kind = kind;
-                L.desc_off = start;
-                L.count = di - start;
-                L.shift = bits_for(maxk);
-                L.key64 = vbits + L.shift > 32;
                 t->plan.push_back(L);
+                continue;
+            }
+            // skeleton + refinement passes
+            int32_t S = 1;
+            while (S * 2 <= skel_stride) S *= 2;
+            L.kind = 3;
+            L.stride_or_delta = S;
+            t->plan.push_back(L);
+            const int32_t chunks = (maxw1 + 255) / 256;
+            int wl2 = 0;
+            while ((1 << wl2) < chunks && wl2 < 3) ++wl2;
+            for (int32_t dl = S / 2; dl >= 1; dl /= 2) {
+                LaunchH P = L;
+                P.kind = 4;
+                P.stride_or_delta = dl;
+                P.wpr_log2 = wl2;
+                P.ustride = maxk + 1;
+                t->plan.push_back(P);
             }
         }
     }
@@ -426,8 +478,16 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
                            t->d_sym_wstar, t->d_node_wstar, s));
     if (t->timing && t->ev_ok) BCK(cudaEventRecord(t->ev[1], s));
     const Ctx c = t->ctx();
-    for (const LaunchH &L : t->plan)
-        BCKL(launch_combine(L.kind, t->d_descs + L.desc_off, L.count, c, L.shift, L.key64, s));
+    for (const LaunchH &L : t->plan) {
+        const CombineDesc *dd = t->d_descs + L.desc_off;
+        if (L.kind <= 1)
+            BCKL(launch_combine(L.kind, dd, L.count, c, L.shift, L.key64, s));
+        else if (L.kind == 3)
+            BCKL(launch_skeleton(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s));
+        else if (refine_rows(n1, L.stride_or_delta) > 0)
+            BCKL(launch_refine(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, L.wpr_log2,
+                               L.ustride, s));
+    }
     if (t->timing && t->ev_ok) BCK(cudaEventRecord(t->ev[2], s));
 #undef BCK
 #undef BCKL

@@ -92,6 +92,13 @@ int launch_base_case_row(const uint8_t *cols, int32_t n, uint8_t sym, int32_t *o
 // kind: 0 = thread-per-row bisection, 1 = warp-per-row bisection
 int launch_combine(int kind, const CombineDesc *descs, int32_t ndesc, Ctx c, int key_shift,
                    bool key64, cudaStream_t s);
+// skeleton rows 0, S, 2S, ..., n by exact Alg. 1 (one CTA per row)
+int launch_skeleton(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
+                    int32_t stride, cudaStream_t s);
+// refinement pass: rows (2t+1)*delta from rows (2t)*delta and (2t+2)*delta
+int launch_refine(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
+                  int32_t delta, int wpr_log2, int32_t ustride, cudaStream_t s);
+int refine_rows(int64_t n1, int32_t delta);
 int launch_walk_level(const WalkNode *nodes, const int32_t *ids, int32_t count, Ctx c,
                       int32_t *wi, int32_t *wj, int32_t *cols_out, bool retrace, int key_shift,
                       bool key64, cudaStream_t s);

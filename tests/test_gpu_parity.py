@@ -255,3 +255,35 @@ def test_dg_rows_by_definition(cfg):
     rng = np.random.default_rng(cfg)
     for i in [1, len(cols) + 1] + [int(x) for x in rng.integers(1, len(cols) + 2, 3)]:
         np.testing.assert_array_equal(R[i - 1], _dg_row_by_definition(rows, cols, i, R.shape[1]))
+
+
+@pytest.mark.parametrize("stride", [1, 2, 4, 16, 64])
+def test_skeleton_refine_strides(stride, monkeypatch):
+    """The wide-table combine (skeleton rows by exact bisection + refinement
+    passes bounded by neighbouring rows) is bit-exact -- reach, kmax, wstar
+    and every trace cell incl. INF artifacts -- for any skeleton stride."""
+    monkeypatch.setenv("LCSG_SKELETON_STRIDE", str(stride))
+    rng = np.random.default_rng(100 + stride)
+    for _ in range(12):
+        m = int(rng.integers(66, 330))
+        n = int(rng.integers(40, 420))
+        sigma = int(rng.choice([2, 4, 20, 26]))
+        a, b = workloads.random_pair(rng, m, n, sigma)
+        g = L.GridModel(a, b)
+        t = O.OracleTree(a, b)
+        for with_trace in (True, False):
+            tab = L.build_cost_table(g, 1, m + 1, with_trace=with_trace)
+            nodes = gpu_tree_nodes(tab)
+            for idx in range(len(t)):
+                exp = t.node(idx)
+                if exp.upper < 0:
+                    continue
+                got = nodes[idx]
+                np.testing.assert_array_equal(got.reach, exp.reach, err_msg=f"S={stride} {idx}")
+                np.testing.assert_array_equal(got.kmax, exp.kmax)
+                assert got.wstar == exp.wstar
+                if with_trace:
+                    np.testing.assert_array_equal(got.trace, exp.trace, err_msg=f"S={stride} {idx}")
+            length = L.lcs_length(tab)
+            np.testing.assert_array_equal(L.recover_cross_vertices(g, tab, length),
+                                          t.recover(length))
