@@ -89,9 +89,10 @@ int launch_leaf_table(Ctx c, int32_t leaf_row, int32_t w1, int32_t *reach, int32
                       cudaStream_t s);
 int launch_base_case_row(const uint8_t *cols, int32_t n, uint8_t sym, int32_t *out,
                          cudaStream_t s);
-// kind: 0 = thread-per-row bisection, 1 = warp-per-row bisection
+// kind: 0 = thread-per-row bisection, 1 = warp-per-row bisection; stride > 1
+// restricts the launch to the skeleton rows 0, S, 2S, ..., n
 int launch_combine(int kind, const CombineDesc *descs, int32_t ndesc, Ctx c, int key_shift,
-                   bool key64, cudaStream_t s);
+                   bool key64, cudaStream_t s, int32_t stride = 1);
 // skeleton rows 0, S, 2S, ..., n by exact Alg. 1 (one CTA per row)
 int launch_skeleton(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
                     int32_t stride, cudaStream_t s);

@@ -222,16 +222,19 @@ constexpr int STACK = 24;
 template <typename Key>
 __global__ void __launch_bounds__(256) combine_thread_kernel(const CombineDesc *__restrict__ descs,
                                                              int32_t ndesc, Ctx c, int shift,
-                                                             int64_t rows_pad) {
+                                                             int64_t rows_pad, int32_t stride,
+                                                             int32_t nrows) {
+    // rows r = 0 .. nrows-1 map to i = r*stride, the last one to n (= n1-1)
     const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t di = gid / rows_pad;  // warp-uniform: rows_pad % 32 == 0
     if (di >= ndesc) return;
-    const int64_t i = gid - di * rows_pad;
+    const int64_t r = gid - di * rows_pad;
     const int64_t n1 = (int64_t)c.n + 1;
+    const int64_t i = (r == nrows - 1) ? n1 - 1 : r * stride;
     const CombineDesc &d = descs[di];
     const int32_t inf = c.inf;
     int32_t kfin = -1;
-    if (i < n1) {
+    if (r < nrows) {
         const TabAcc U = resolve(d.U, c), L = resolve(d.L, c);
         const int32_t w = d.w1 - 1, wl = L.w1 - 1;
         const int32_t kmaxU = tab_kmax(U, i, inf);
@@ -297,15 +300,17 @@ constexpr int WSTACK = 34;  // > log2(max colhi) + 1 for colhi < 2^32
 
 template <typename Key>
 __global__ void __launch_bounds__(32 * WARP_KERNEL_WARPS)
-    combine_warp_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int shift) {
+    combine_warp_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int shift,
+                        int32_t stride, int32_t nrows) {
     __shared__ int4 stk_all[WARP_KERNEL_WARPS][WSTACK];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     int4 *stk = stk_all[wid];
     const int64_t n1 = (int64_t)c.n + 1;
     const int64_t gw = blockIdx.x * (int64_t)WARP_KERNEL_WARPS + wid;
-    const int64_t di = gw / n1;
+    const int64_t di = gw / nrows;
     if (di >= ndesc) return;
-    const int64_t i = gw - di * n1;
+    const int64_t r = gw - di * nrows;
+    const int64_t i = (r == nrows - 1) ? n1 - 1 : r * stride;
     const CombineDesc &d = descs[di];
     const int32_t inf = c.inf;
     const TabAcc U = resolve(d.U, c), L = resolve(d.L, c);
@@ -369,24 +374,26 @@ __global__ void __launch_bounds__(32 * WARP_KERNEL_WARPS)
 }
 
 int launch_combine(int kind, const CombineDesc *descs, int32_t ndesc, Ctx c, int key_shift,
-                   bool key64, cudaStream_t s) {
+                   bool key64, cudaStream_t s, int32_t stride) {
     if (ndesc <= 0) return 0;
     const int64_t n1 = (int64_t)c.n + 1;
+    // stride 1: every row; stride S: skeleton rows 0, S, 2S, ..., n
+    const int32_t nrows = stride <= 1 ? (int32_t)n1 : (int32_t)((n1 - 1 + stride - 1) / stride) + 1;
     if (kind == 0) {
-        const int64_t rows_pad = (n1 + 31) / 32 * 32;
+        const int64_t rows_pad = ((int64_t)nrows + 31) / 32 * 32;
         const int64_t threads = rows_pad * ndesc;
         const unsigned blocks = (unsigned)((threads + 255) / 256);
         if (key64)
-            combine_thread_kernel<uint64_t><<<blocks, 256, 0, s>>>(descs, ndesc, c, key_shift, rows_pad);
+            combine_thread_kernel<uint64_t><<<blocks, 256, 0, s>>>(descs, ndesc, c, key_shift, rows_pad, stride, nrows);
         else
-            combine_thread_kernel<uint32_t><<<blocks, 256, 0, s>>>(descs, ndesc, c, key_shift, rows_pad);
+            combine_thread_kernel<uint32_t><<<blocks, 256, 0, s>>>(descs, ndesc, c, key_shift, rows_pad, stride, nrows);
     } else {
-        const int64_t warps = n1 * ndesc;
+        const int64_t warps = (int64_t)nrows * ndesc;
         const unsigned blocks = (unsigned)((warps + WARP_KERNEL_WARPS - 1) / WARP_KERNEL_WARPS);
         if (key64)
-            combine_warp_kernel<uint64_t><<<blocks, 32 * WARP_KERNEL_WARPS, 0, s>>>(descs, ndesc, c, key_shift);
+            combine_warp_kernel<uint64_t><<<blocks, 32 * WARP_KERNEL_WARPS, 0, s>>>(descs, ndesc, c, key_shift, stride, nrows);
         else
-            combine_warp_kernel<uint32_t><<<blocks, 32 * WARP_KERNEL_WARPS, 0, s>>>(descs, ndesc, c, key_shift);
+            combine_warp_kernel<uint32_t><<<blocks, 32 * WARP_KERNEL_WARPS, 0, s>>>(descs, ndesc, c, key_shift, stride, nrows);
     }
     LCSG_LAUNCH_CHECK();
     return 0;

@@ -208,13 +208,20 @@ __global__ void __launch_bounds__(32 * SK_WARPS)
 }
 
 // ---------------------------------------------------------------------------
-// 2. refinement pass: rows c = (2t+1)*delta from rows c-delta and c+delta.
-// A CTA of 8 warps holds R = 8 / wpr rows; wpr warps share one row.
+// 2. refinement pass: rows c = (2t+1)*delta from rows a = c-delta, b = c+delta.
+// A CTA of 8 warps holds R = 8 / wpr rows; wpr warps share one row.  Shared
+// memory holds the U rows of the R rows and of their R+1 neighbours (row b of
+// slot t is row a of slot t+1), so the crossing columns X(a,j) = U[a,T(a,j)],
+// X(b,j) and both binary searches are shared-memory only: per column the
+// dependent global traffic is the two coalesced trace loads and the L
+// gathers.  Each lane handles RF_NB columns at once (independent loads in
+// flight) to cover HBM latency.
 // ---------------------------------------------------------------------------
 constexpr int RF_SEGS = 40;
+constexpr int RF_NB = 4;
 
 template <typename Key>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 2)
     refine_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int shift,
                   int32_t delta, int32_t cnt, int wpr_log2, int32_t ustride) {
     extern __shared__ int32_t sm[];
@@ -227,13 +234,16 @@ __global__ void __launch_bounds__(256)
     const int gt = gw * 32 + lane, gthreads = wpr * 32;
     const int32_t bpd = (cnt + R - 1) / R;
     const int64_t di = blockIdx.x / bpd;
-    const int32_t slot = (int32_t)(blockIdx.x - di * bpd) * R + grp;
+    const int32_t slot0 = (int32_t)(blockIdx.x - di * bpd) * R;
+    const int32_t slot = slot0 + grp;
     const bool active = di < ndesc && slot < cnt;
     const int64_t n1 = (int64_t)c.n + 1;
     const int32_t inf = c.inf;
     int32_t *Uc = sm + grp * ustride;
+    const int32_t *Ua = sm + (R + grp) * ustride;
+    const int32_t *Ub = sm + (R + grp + 1) * ustride;
 
-    const CombineDesc &d = descs[active ? di : 0];
+    const CombineDesc &d = descs[di < ndesc ? di : 0];
     const TabAcc U = resolve(d.U, c), L = resolve(d.L, c);
     const int32_t w = d.w1 - 1, wl = L.w1 - 1;
     const int64_t cr = (2 * (int64_t)slot + 1) * delta;
@@ -243,6 +253,19 @@ __global__ void __launch_bounds__(256)
     int32_t kmaxc = 0, colhi = 0, Ka = 0, Kb = 0;
     int32_t *reach = nullptr, *trace = nullptr;
     const int32_t *trace_a = nullptr, *trace_b = nullptr;
+    // ---- stage U rows: own row, neighbour a (= slot's even row), and b for the last group ----
+    if (di < ndesc && slot0 + grp <= cnt) {
+        const int64_t nb = min(2 * (int64_t)slot * delta, n1 - 1);
+        int32_t *Un = sm + (R + grp) * ustride;
+        const int32_t kn = tab_kmax(U, nb, inf);
+        for (int32_t k = gt; k <= kn; k += gthreads) Un[k] = tab_get(U, nb, k);
+        if (grp == R - 1) {
+            const int64_t nb2 = min(2 * (int64_t)(slot + 1) * delta, n1 - 1);
+            int32_t *Un2 = sm + (R + grp + 1) * ustride;
+            const int32_t kn2 = tab_kmax(U, nb2, inf);
+            for (int32_t k = gt; k <= kn2; k += gthreads) Un2[k] = tab_get(U, nb2, k);
+        }
+    }
     if (active) {
         kmaxc = tab_kmax(U, cr, inf);
         colhi = min(w, kmaxc + *d.L.wstar);
@@ -258,50 +281,79 @@ __global__ void __launch_bounds__(256)
     __syncthreads();
     if (active) {
         // ---- main cells: (b, j) finite => (c, j) finite, bounded k-range ----
-        for (int32_t j = gt; j <= Kb; j += gthreads) {
-            const int32_t Ta = __ldg(trace_a + j), Tb = __ldg(trace_b + j);
-            const int32_t Xa = tab_get(U, ar, Ta), Xb = tab_get(U, br, Tb);
-            int32_t hi = min(Ta, kmaxc);
-            int32_t lo = min(max(0, Ta - (int32_t)delta), hi);
-            while (lo < hi) {  // first k with Uc[k] >= Xa
-                const int32_t md = (lo + hi) >> 1;
-                if (Uc[md] >= Xa) hi = md; else lo = md + 1;
+        for (int32_t j0 = gt; j0 <= Kb; j0 += gthreads * RF_NB) {
+            int32_t Ta[RF_NB], Tb[RF_NB], klo[RF_NB], khi[RF_NB];
+#pragma unroll
+            for (int q = 0; q < RF_NB; ++q) {
+                const int32_t j = j0 + q * gthreads;
+                Ta[q] = j <= Kb ? __ldg(trace_a + j) : 0;
+                Tb[q] = j <= Kb ? __ldg(trace_b + j) : 0;
             }
-            int32_t klo = lo;
-            lo = min(Tb, kmaxc);
-            hi = min(Tb + db, kmaxc);
-            while (lo < hi) {  // last k with Uc[k] <= Xb
-                const int32_t md = (lo + hi + 1) >> 1;
-                if (Uc[md] <= Xb) lo = md; else hi = md - 1;
+            int32_t maxlen = 0;
+#pragma unroll
+            for (int q = 0; q < RF_NB; ++q) {
+                const int32_t j = j0 + q * gthreads;
+                const int32_t Xa = Ua[Ta[q]], Xb = Ub[Tb[q]];
+                int32_t hi = min(Ta[q], kmaxc);
+                int32_t lo = min(max(0, Ta[q] - (int32_t)delta), hi);
+                while (lo < hi) {  // first k with Uc[k] >= Xa
+                    const int32_t md = (lo + hi) >> 1;
+                    if (Uc[md] >= Xa) hi = md; else lo = md + 1;
+                }
+                int32_t kl = max(lo, j - wl);
+                lo = min(Tb[q], kmaxc);
+                hi = min(Tb[q] + db, kmaxc);
+                while (lo < hi) {  // last k with Uc[k] <= Xb
+                    const int32_t md = (lo + hi + 1) >> 1;
+                    if (Uc[md] <= Xb) lo = md; else hi = md - 1;
+                }
+                int32_t kh = min(lo, j);
+                if (kl > kh) {  // safety net: never taken when the bounds hold
+                    kl = max(0, j - wl);
+                    kh = min(j, kmaxc);
+                }
+                if (j > Kb) { kl = 1; kh = 0; }
+                klo[q] = kl;
+                khi[q] = kh;
+                maxlen = max(maxlen, kh - kl + 1);
             }
-            int32_t khi = min(lo, j);
-            klo = max(klo, j - wl);
-            if (klo > khi) {  // safety net: never taken when the bounds hold
-                klo = max(0, j - wl);
-                khi = min(j, kmaxc);
+            Key best[RF_NB];
+#pragma unroll
+            for (int q = 0; q < RF_NB; ++q) best[q] = ~(Key)0;
+            for (int32_t t = 0; t < maxlen; ++t) {
+#pragma unroll
+                for (int q = 0; q < RF_NB; ++q) {
+                    const int32_t k = klo[q] + t;
+                    if (k <= khi[q]) {
+                        const int32_t j = j0 + q * gthreads;
+                        const Key key = rpack<Key>(rcell(L, Uc[k], k, j, inf, wl), k, shift);
+                        best[q] = key < best[q] ? key : best[q];
+                    }
+                }
             }
-            Key best = ~(Key)0;
-            for (int32_t k = klo; k <= khi; ++k) {
-                const Key key = rpack<Key>(rcell(L, Uc[k], k, j, inf, wl), k, shift);
-                best = key < best ? key : best;
+#pragma unroll
+            for (int q = 0; q < RF_NB; ++q) {
+                const int32_t j = j0 + q * gthreads;
+                if (j <= Kb) {
+                    reach[j] = rval<Key>(best[q], shift);
+                    trace[j] = rk<Key>(best[q], shift);
+                }
             }
-            reach[j] = rval<Key>(best, shift);
-            trace[j] = rk<Key>(best, shift);
         }
         // ---- tail: finite in a, INF in b -> lower bound only; one warp per cell ----
         const int32_t jt_hi = min(min(Ka, Kb + db), colhi);
         for (int32_t j = Kb + 1 + gw; j <= jt_hi; j += wpr) {
             const int32_t Ta = __ldg(trace_a + j);
-            const int32_t Xa = tab_get(U, ar, Ta);
+            const int32_t Xa = Ua[Ta];
             int32_t hi = min(Ta, kmaxc);
             int32_t lo = min(max(0, Ta - (int32_t)delta), hi);
             while (lo < hi) {
                 const int32_t md = (lo + hi) >> 1;
                 if (Uc[md] >= Xa) hi = md; else lo = md + 1;
             }
-            const int32_t klo = max(lo, j - wl), khi = min(j, kmaxc);
+            const int32_t kl = max(lo, j - wl), kh = min(j, kmaxc);
             Key best = ~(Key)0;
-            for (int32_t k = klo + lane; k <= khi; k += 32) {
+            for (int32_t k = kl + lane; k <= kh; k += 32) {
                 const Key key = rpack<Key>(rcell(L, Uc[k], k, j, inf, wl), k, shift);
                 best = key < best ? key : best;
             }
@@ -381,7 +433,7 @@ int launch_refine(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, boo
     const int R = 8 >> wpr_log2;
     const int64_t bpd = (cnt + R - 1) / R;
     const unsigned blocks = (unsigned)(bpd * ndesc);
-    const size_t smem = (size_t)R * ustride * 4;
+    const size_t smem = (size_t)(2 * R + 1) * ustride * 4;
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(refine_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
