@@ -78,27 +78,14 @@ int prepare_device(int device) {
 }
 
 // Kernel choice per combine:
-//   kind 0: thread-per-row exact bisection        (w1 <= LCSG_THREAD_MAX_W1, default 17)
+//   kind 0: thread-per-row exact bisection        (w1 <= LCSG_THREAD_MAX_W1, default 65)
 //   kind 2: skeleton rows (exact bisection: thread / warp / CTA per row by
 //           width) + refinement passes             (wider)
 //   kind 1: warp-per-row exact bisection          (fallback: U rows too big for smem)
-constexpr int64_t REFINE_MAX_SMEM = 200 * 1024;
 
 int env_int(const char *name, int def) {
     const char *v = getenv(name);
     return v && *v ? atoi(v) : def;
-}
-
-// refinement-kernel geometry for an output width: warps per row (log2)
-int refine_wpr_log2(int32_t w1) {
-    const int32_t chunks = (w1 + 511) / 512;  // 32 lanes x RF_NB=4 columns x 4 iterations
-    int wl2 = 0;
-    while ((1 << wl2) < chunks && wl2 < 3) ++wl2;
-    return wl2;
-}
-int64_t refine_smem(int32_t w1, int32_t ustride) {
-    const int R = 8 >> refine_wpr_log2(w1);
-    return (int64_t)(2 * R + 1) * ustride * 4;
 }
 
 struct NodeH {
@@ -281,7 +268,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     size_t o_sub = take((size_t)std::max<int64_t>(kmin, 1));
     // int32 tables of every combine node
     const int skel_stride = std::max(1, env_int("LCSG_SKELETON_STRIDE", 16));
-    const int thread_max_w1 = env_int("LCSG_THREAD_MAX_W1", 17);
+    const int thread_max_w1 = env_int("LCSG_THREAD_MAX_W1", 65);
     const int skel_thread_max = env_int("LCSG_SKEL_THREAD_MAX_W1", 257);
     const int skel_warp_max = env_int("LCSG_SKEL_WARP_MAX_W1", 4097);
     size_t o_tab = off;
@@ -293,8 +280,8 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
         ++ncomb;
         maxh0 = std::max(maxh0, nd.height);
         const int32_t wu1 = t->nodes[nd.upper].w1;
-        nd.kind = nd.w1 <= thread_max_w1 ? 0
-                  : (refine_smem(nd.w1, wu1) <= REFINE_MAX_SMEM ? 2 : 1);
+        nd.kind = nd.w1 <= thread_max_w1 ? 0 : 2;
+        (void)wu1;
         if (skel_stride == 1 && nd.kind == 2) nd.kind = 1;
         nd.reach_off = tab_elems;
         tab_elems += n1 * nd.w1;
@@ -406,13 +393,10 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             L.kind = maxw1 <= skel_thread_max ? 5 : (maxw1 <= skel_warp_max ? 6 : 3);
             L.stride_or_delta = S;
             t->plan.push_back(L);
-            const int wl2 = refine_wpr_log2(maxw1);
             for (int32_t dl = S / 2; dl >= 1; dl /= 2) {
                 LaunchH P = L;
                 P.kind = 4;
                 P.stride_or_delta = dl;
-                P.wpr_log2 = wl2;
-                P.ustride = maxk + 1;
                 t->plan.push_back(P);
             }
         }
@@ -504,8 +488,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             BCKL(launch_combine(L.kind == 5 ? 0 : 1, dd, L.count, c, L.shift, L.key64, s,
                                 L.stride_or_delta));
         else if (refine_rows(n1, L.stride_or_delta) > 0)
-            BCKL(launch_refine(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, L.wpr_log2,
-                               L.ustride, s));
+            BCKL(launch_refine(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s));
     }
     if (t->timing && t->ev_ok) BCK(cudaEventRecord(t->ev[2], s));
 #undef BCK

@@ -98,7 +98,7 @@ int launch_skeleton(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, b
                     int32_t stride, cudaStream_t s);
 // refinement pass: rows (2t+1)*delta from rows (2t)*delta and (2t+2)*delta
 int launch_refine(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
-                  int32_t delta, int wpr_log2, int32_t ustride, cudaStream_t s);
+                  int32_t delta, cudaStream_t s);
 int refine_rows(int64_t n1, int32_t delta);
 int launch_walk_level(const WalkNode *nodes, const int32_t *ids, int32_t count, Ctx c,
                       int32_t *wi, int32_t *wj, int32_t *cols_out, bool retrace, int key_shift,

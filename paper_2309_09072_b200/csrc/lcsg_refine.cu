@@ -209,198 +209,179 @@ __global__ void __launch_bounds__(32 * SK_WARPS)
 
 // ---------------------------------------------------------------------------
 // 2. refinement pass: rows c = (2t+1)*delta from rows a = c-delta, b = c+delta.
-// A CTA of 8 warps holds R = 8 / wpr rows; wpr warps share one row.  Shared
-// memory holds the U rows of the R rows and of their R+1 neighbours (row b of
-// slot t is row a of slot t+1), so the crossing columns X(a,j) = U[a,T(a,j)],
-// X(b,j) and both binary searches are shared-memory only: per column the
-// dependent global traffic is the two coalesced trace loads and the L
-// gathers.  Each lane handles RF_NB columns at once (independent loads in
-// flight) to cover HBM latency.
+// One warp per row, rows fully independent (no CTA barriers): a profile of a
+// CTA-synchronised variant showed a quarter of all stall samples parked at the
+// barrier behind the slowest row.  U rows are read straight from HBM/L2 with
+// the read-only path: consecutive lanes touch consecutive k, so each warp
+// load is one or two 128-B lines.  Each lane owns RF_NB columns per step
+// (j = j0 + lane + 32q) so several independent gathers are in flight.
 // ---------------------------------------------------------------------------
 constexpr int RF_SEGS = 40;
 constexpr int RF_NB = 4;
+constexpr int RF_WARPS = 8;
 
 template <typename Key>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(32 * RF_WARPS)
     refine_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int shift,
-                  int32_t delta, int32_t cnt, int wpr_log2, int32_t ustride) {
-    extern __shared__ int32_t sm[];
-    __shared__ int32_t g_kfin[8];
-    __shared__ int4 g_seg[8][RF_SEGS];
-    __shared__ int32_t g_nseg[8];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wpr = 1 << wpr_log2, R = 8 >> wpr_log2;
-    const int grp = warp >> wpr_log2, gw = warp & (wpr - 1);
-    const int gt = gw * 32 + lane, gthreads = wpr * 32;
-    const int32_t bpd = (cnt + R - 1) / R;
-    const int64_t di = blockIdx.x / bpd;
-    const int32_t slot0 = (int32_t)(blockIdx.x - di * bpd) * R;
-    const int32_t slot = slot0 + grp;
-    const bool active = di < ndesc && slot < cnt;
+                  int32_t delta, int32_t cnt) {
+    __shared__ int4 seg_all[RF_WARPS][RF_SEGS];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t gw = blockIdx.x * (int64_t)RF_WARPS + wid;
+    const int64_t di = gw / cnt;
+    if (di >= ndesc) return;  // warp-uniform
+    const int32_t slot = (int32_t)(gw - di * cnt);
+    int4 *seg = seg_all[wid];
     const int64_t n1 = (int64_t)c.n + 1;
     const int32_t inf = c.inf;
-    int32_t *Uc = sm + grp * ustride;
-    const int32_t *Ua = sm + (R + grp) * ustride;
-    const int32_t *Ub = sm + (R + grp + 1) * ustride;
-
-    const CombineDesc &d = descs[di < ndesc ? di : 0];
+    const CombineDesc &d = descs[di];
     const TabAcc U = resolve(d.U, c), L = resolve(d.L, c);
     const int32_t w = d.w1 - 1, wl = L.w1 - 1;
     const int64_t cr = (2 * (int64_t)slot + 1) * delta;
     const int64_t ar = cr - delta;
     const int64_t br = min(cr + delta, n1 - 1);
     const int32_t db = (int32_t)(br - cr);
-    int32_t kmaxc = 0, colhi = 0, Ka = 0, Kb = 0;
-    int32_t *reach = nullptr, *trace = nullptr;
-    const int32_t *trace_a = nullptr, *trace_b = nullptr;
-    // ---- stage U rows: own row, neighbour a (= slot's even row), and b for the last group ----
-    if (di < ndesc && slot0 + grp <= cnt) {
-        const int64_t nb = min(2 * (int64_t)slot * delta, n1 - 1);
-        int32_t *Un = sm + (R + grp) * ustride;
-        const int32_t kn = tab_kmax(U, nb, inf);
-        for (int32_t k = gt; k <= kn; k += gthreads) Un[k] = tab_get(U, nb, k);
-        if (grp == R - 1) {
-            const int64_t nb2 = min(2 * (int64_t)(slot + 1) * delta, n1 - 1);
-            int32_t *Un2 = sm + (R + grp + 1) * ustride;
-            const int32_t kn2 = tab_kmax(U, nb2, inf);
-            for (int32_t k = gt; k <= kn2; k += gthreads) Un2[k] = tab_get(U, nb2, k);
+    const int32_t kmaxc = tab_kmax(U, cr, inf);
+    const int32_t colhi = min(w, kmaxc + *d.L.wstar);
+    const int32_t Ka = d.out_kmax[ar], Kb = d.out_kmax[br];
+    int32_t *reach = d.out_reach + cr * d.w1;
+    int32_t *trace = d.out_trace + cr * d.w1;
+    const int32_t *trace_a = d.out_trace + ar * d.w1;
+    const int32_t *trace_b = d.out_trace + br * d.w1;
+    const int32_t *Ur = U.reach + cr * (int64_t)U.w1;  // U is never a leaf here (w1 > 17)
+    const int32_t *Ua = U.reach + ar * (int64_t)U.w1;
+    const int32_t *Ub = U.reach + br * (int64_t)U.w1;
+
+    // ---- main cells: (b, j) finite => (c, j) finite, bounded k-range ----
+    for (int32_t j0 = 0; j0 <= Kb; j0 += 32 * RF_NB) {
+        int32_t Ta[RF_NB], Tb[RF_NB], klo[RF_NB], khi[RF_NB];
+#pragma unroll
+        for (int q = 0; q < RF_NB; ++q) {
+            const int32_t j = j0 + lane + 32 * q;
+            Ta[q] = j <= Kb ? __ldg(trace_a + j) : 0;
+            Tb[q] = j <= Kb ? __ldg(trace_b + j) : 0;
         }
-    }
-    if (active) {
-        kmaxc = tab_kmax(U, cr, inf);
-        colhi = min(w, kmaxc + *d.L.wstar);
-        Ka = d.out_kmax[ar];
-        Kb = d.out_kmax[br];
-        reach = d.out_reach + cr * d.w1;
-        trace = d.out_trace + cr * d.w1;
-        trace_a = d.out_trace + ar * d.w1;
-        trace_b = d.out_trace + br * d.w1;
-        for (int32_t k = gt; k <= kmaxc; k += gthreads) Uc[k] = tab_get(U, cr, k);
-        if (gt == 0) g_kfin[grp] = Kb;
-    }
-    __syncthreads();
-    if (active) {
-        // ---- main cells: (b, j) finite => (c, j) finite, bounded k-range ----
-        for (int32_t j0 = gt; j0 <= Kb; j0 += gthreads * RF_NB) {
-            int32_t Ta[RF_NB], Tb[RF_NB], klo[RF_NB], khi[RF_NB];
+        int32_t Xa[RF_NB], Xb[RF_NB];
 #pragma unroll
-            for (int q = 0; q < RF_NB; ++q) {
-                const int32_t j = j0 + q * gthreads;
-                Ta[q] = j <= Kb ? __ldg(trace_a + j) : 0;
-                Tb[q] = j <= Kb ? __ldg(trace_b + j) : 0;
-            }
-            int32_t maxlen = 0;
-#pragma unroll
-            for (int q = 0; q < RF_NB; ++q) {
-                const int32_t j = j0 + q * gthreads;
-                const int32_t Xa = Ua[Ta[q]], Xb = Ub[Tb[q]];
-                int32_t hi = min(Ta[q], kmaxc);
-                int32_t lo = min(max(0, Ta[q] - (int32_t)delta), hi);
-                while (lo < hi) {  // first k with Uc[k] >= Xa
-                    const int32_t md = (lo + hi) >> 1;
-                    if (Uc[md] >= Xa) hi = md; else lo = md + 1;
-                }
-                int32_t kl = max(lo, j - wl);
-                lo = min(Tb[q], kmaxc);
-                hi = min(Tb[q] + db, kmaxc);
-                while (lo < hi) {  // last k with Uc[k] <= Xb
-                    const int32_t md = (lo + hi + 1) >> 1;
-                    if (Uc[md] <= Xb) lo = md; else hi = md - 1;
-                }
-                int32_t kh = min(lo, j);
-                if (kl > kh) {  // safety net: never taken when the bounds hold
-                    kl = max(0, j - wl);
-                    kh = min(j, kmaxc);
-                }
-                if (j > Kb) { kl = 1; kh = 0; }
-                klo[q] = kl;
-                khi[q] = kh;
-                maxlen = max(maxlen, kh - kl + 1);
-            }
-            Key best[RF_NB];
-#pragma unroll
-            for (int q = 0; q < RF_NB; ++q) best[q] = ~(Key)0;
-            for (int32_t t = 0; t < maxlen; ++t) {
-#pragma unroll
-                for (int q = 0; q < RF_NB; ++q) {
-                    const int32_t k = klo[q] + t;
-                    if (k <= khi[q]) {
-                        const int32_t j = j0 + q * gthreads;
-                        const Key key = rpack<Key>(rcell(L, Uc[k], k, j, inf, wl), k, shift);
-                        best[q] = key < best[q] ? key : best[q];
-                    }
-                }
-            }
-#pragma unroll
-            for (int q = 0; q < RF_NB; ++q) {
-                const int32_t j = j0 + q * gthreads;
-                if (j <= Kb) {
-                    reach[j] = rval<Key>(best[q], shift);
-                    trace[j] = rk<Key>(best[q], shift);
-                }
-            }
+        for (int q = 0; q < RF_NB; ++q) {
+            Xa[q] = __ldg(Ua + Ta[q]);
+            Xb[q] = __ldg(Ub + Tb[q]);
         }
-        // ---- tail: finite in a, INF in b -> lower bound only; one warp per cell ----
-        const int32_t jt_hi = min(min(Ka, Kb + db), colhi);
-        for (int32_t j = Kb + 1 + gw; j <= jt_hi; j += wpr) {
-            const int32_t Ta = __ldg(trace_a + j);
-            const int32_t Xa = Ua[Ta];
-            int32_t hi = min(Ta, kmaxc);
-            int32_t lo = min(max(0, Ta - (int32_t)delta), hi);
+        int32_t maxlen = 0;
+#pragma unroll
+        for (int q = 0; q < RF_NB; ++q) {
+            const int32_t j = j0 + lane + 32 * q;
+            // klo = first k with U[c,k] >= X(a,j), in [Ta - delta, Ta]
+            int32_t hi = min(Ta[q], kmaxc);
+            int32_t lo = min(max(0, Ta[q] - (int32_t)delta), hi);
             while (lo < hi) {
                 const int32_t md = (lo + hi) >> 1;
-                if (Uc[md] >= Xa) hi = md; else lo = md + 1;
+                if (__ldg(Ur + md) >= Xa[q]) hi = md; else lo = md + 1;
             }
-            const int32_t kl = max(lo, j - wl), kh = min(j, kmaxc);
-            Key best = ~(Key)0;
-            for (int32_t k = kl + lane; k <= kh; k += 32) {
-                const Key key = rpack<Key>(rcell(L, Uc[k], k, j, inf, wl), k, shift);
-                best = key < best ? key : best;
+            int32_t kl = max(lo, j - wl);
+            // khi = last k with U[c,k] <= X(b,j), in [Tb, Tb + (b - c)]
+            lo = min(Tb[q], kmaxc);
+            hi = min(Tb[q] + db, kmaxc);
+            while (lo < hi) {
+                const int32_t md = (lo + hi + 1) >> 1;
+                if (__ldg(Ur + md) <= Xb[q]) lo = md; else hi = md - 1;
             }
-            best = rwarp_min(best);
-            const int32_t bv = rval<Key>(best, shift);
-            if (lane == 0 && bv != inf) {
-                reach[j] = bv;
-                trace[j] = rk<Key>(best, shift);
-                atomicMax(&g_kfin[grp], j);
+            int32_t kh = min(lo, j);
+            if (kl > kh) {  // safety net: never taken when the bounds hold
+                kl = max(0, j - wl);
+                kh = min(j, kmaxc);
+            }
+            if (j > Kb) { kl = 1; kh = 0; }
+            klo[q] = kl;
+            khi[q] = kh;
+            maxlen = max(maxlen, kh - kl + 1);
+        }
+        Key best[RF_NB];
+#pragma unroll
+        for (int q = 0; q < RF_NB; ++q) best[q] = ~(Key)0;
+        for (int32_t t = 0; t < maxlen; ++t) {
+#pragma unroll
+            for (int q = 0; q < RF_NB; ++q) {
+                const int32_t k = klo[q] + t;
+                if (k <= khi[q]) {
+                    const int32_t j = j0 + lane + 32 * q;
+                    const Key key = rpack<Key>(rcell(L, __ldg(Ur + k), k, j, inf, wl), k, shift);
+                    best[q] = key < best[q] ? key : best[q];
+                }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < RF_NB; ++q) {
+            const int32_t j = j0 + lane + 32 * q;
+            if (j <= Kb) {
+                reach[j] = rval<Key>(best[q], shift);
+                trace[j] = rk<Key>(best[q], shift);
             }
         }
     }
-    __syncthreads();
-    // ---- replay Alg. 1 over the INF suffix: trace = `top` of the covering node ----
-    if (active && gt == 0) {
-        const int32_t K = g_kfin[grp];
-        int32_t left = 0, right = colhi, top = 0, ns = 0;
+    // ---- tail: finite in a, INF in b -> lower bound only; whole warp per cell ----
+    int32_t K = Kb;
+    const int32_t jt_hi = min(min(Ka, Kb + db), colhi);
+    for (int32_t j = Kb + 1; j <= jt_hi; ++j) {
+        const int32_t Ta = __ldg(trace_a + j);
+        const int32_t Xa = __ldg(Ua + Ta);
+        int32_t hi = min(Ta, kmaxc);
+        int32_t lo = min(max(0, Ta - (int32_t)delta), hi);
+        while (lo < hi) {
+            const int32_t md = (lo + hi) >> 1;
+            if (__ldg(Ur + md) >= Xa) hi = md; else lo = md + 1;
+        }
+        const int32_t kl = max(lo, j - wl), kh = min(j, kmaxc);
+        Key best = ~(Key)0;
+        for (int32_t k = kl + lane; k <= kh; k += 32) {
+            const Key key = rpack<Key>(rcell(L, __ldg(Ur + k), k, j, inf, wl), k, shift);
+            best = key < best ? key : best;
+        }
+        best = rwarp_min(best);
+        const int32_t bv = rval<Key>(best, shift);
+        if (bv == inf) break;  // finite cells form a prefix
+        if (lane == 0) {
+            reach[j] = bv;
+            trace[j] = rk<Key>(best, shift);
+        }
+        K = j;
+    }
+    // ---- replay Alg. 1 over the INF suffix (K, colhi]: trace = `top` of the
+    // covering node.  Lane 0 walks the path positions (no loads); the `top`
+    // values (traces at finite mids of the path) are then fetched in parallel.
+    int ns = 0;
+    if (lane == 0) {
+        int32_t left = 0, right = colhi, fm = -1;
         while (right >= left) {
             const int32_t mid = (left + right + 1) >> 1;
             if (mid <= K) {
-                top = trace[mid];
+                fm = mid;
                 left = mid + 1;
             } else {
-                if (ns < RF_SEGS) g_seg[grp][ns++] = make_int4(mid, right, top, 0);
+                if (ns < RF_SEGS) seg[ns++] = make_int4(mid, right, fm, 0);
                 right = mid - 1;
             }
         }
-        g_nseg[grp] = ns;
     }
-    __syncthreads();
-    if (active) {
-        const int32_t K = g_kfin[grp];
-        const int ns = g_nseg[grp];
-        for (int32_t q = K + 1 + gt; q <= w; q += gthreads) {
-            int32_t tv = 0;
-            if (q <= colhi)
-                for (int s = 0; s < ns; ++s) {
-                    const int4 sg = g_seg[grp][s];
-                    if (q >= sg.x && q <= sg.y) { tv = sg.z; break; }
-                }
-            reach[q] = inf;
-            trace[q] = tv;
-        }
-        if (gt == 0) {
-            d.out_kmax[cr] = K;
-            atomicMax(d.out_wstar, K);
-        }
+    ns = __shfl_sync(0xffffffffu, ns, 0);
+    __syncwarp();
+    for (int s = lane; s < ns; s += 32) {
+        const int32_t fm = seg[s].z;
+        seg[s].w = fm >= 0 ? trace[fm] : 0;
+    }
+    __syncwarp();
+    for (int32_t q = K + 1 + lane; q <= w; q += 32) {
+        int32_t tv = 0;
+        if (q <= colhi)
+            for (int s = 0; s < ns; ++s) {
+                const int4 sg = seg[s];
+                if (q >= sg.x && q <= sg.y) { tv = sg.w; break; }
+            }
+        reach[q] = inf;
+        trace[q] = tv;
+    }
+    if (lane == 0) {
+        d.out_kmax[cr] = K;
+        atomicMax(d.out_wstar, K);
     }
 }
 
@@ -425,25 +406,17 @@ int refine_rows(int64_t n1, int32_t delta) {
 }
 
 int launch_refine(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
-                  int32_t delta, int wpr_log2, int32_t ustride, cudaStream_t s) {
+                  int32_t delta, cudaStream_t s) {
     if (ndesc <= 0) return 0;
     const int64_t n1 = (int64_t)c.n + 1;
     const int32_t cnt = refine_rows(n1, delta);
     if (cnt <= 0) return 0;
-    const int R = 8 >> wpr_log2;
-    const int64_t bpd = (cnt + R - 1) / R;
-    const unsigned blocks = (unsigned)(bpd * ndesc);
-    const size_t smem = (size_t)(2 * R + 1) * ustride * 4;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(refine_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(refine_kernel<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr_set = true;
-    }
+    const int64_t warps = (int64_t)cnt * ndesc;
+    const unsigned blocks = (unsigned)((warps + RF_WARPS - 1) / RF_WARPS);
     if (key64)
-        refine_kernel<uint64_t><<<blocks, 256, smem, s>>>(descs, ndesc, c, shift, delta, cnt, wpr_log2, ustride);
+        refine_kernel<uint64_t><<<blocks, 32 * RF_WARPS, 0, s>>>(descs, ndesc, c, shift, delta, cnt);
     else
-        refine_kernel<uint32_t><<<blocks, 256, smem, s>>>(descs, ndesc, c, shift, delta, cnt, wpr_log2, ustride);
+        refine_kernel<uint32_t><<<blocks, 32 * RF_WARPS, 0, s>>>(descs, ndesc, c, shift, delta, cnt);
     LCSG_LAUNCH_CHECK();
     return 0;
 }
