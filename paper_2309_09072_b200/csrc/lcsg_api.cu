@@ -271,6 +271,10 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     const int thread_max_w1 = env_int("LCSG_THREAD_MAX_W1", 65);
     const int skel_thread_max = env_int("LCSG_SKEL_THREAD_MAX_W1", 257);
     const int skel_warp_max = env_int("LCSG_SKEL_WARP_MAX_W1", 4097);
+    // refinement mode: tiled (default) or one launch per pass ("LCSG_REFINE_PASSES=1")
+    const bool tiled = env_int("LCSG_REFINE_PASSES", 0) == 0 && skel_stride <= 64;
+    const int tile_j = std::max(32, env_int("LCSG_TILE_J", 128));
+    const int tile_wk = std::max(32, env_int("LCSG_TILE_WK", 256));
     size_t o_tab = off;
     int64_t tab_elems = 0;
     int32_t ncomb = 0;
@@ -289,9 +293,16 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             nd.trace_off = tab_elems;
             tab_elems += n1 * nd.w1;
         }
+    }
+    // kmax rows of every combine, contiguous: initialised to -1 in one memset
+    // (the tiled refinement folds per-tile maxima into it with atomicMax)
+    const int64_t kmax_region = tab_elems;
+    for (auto &nd : t->nodes) {
+        if (nd.upper < 0) continue;
         nd.kmax_off = tab_elems;
         tab_elems += (n1 + 63) / 64 * 64;
     }
+    const int64_t kmax_region_elems = tab_elems - kmax_region;
     // low-memory mode: the refinement passes still need this level's traces
     // (they bound neighbouring rows); one scratch region reused level by level
     int64_t scratch_elems = 0;
@@ -393,6 +404,16 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             L.kind = maxw1 <= skel_thread_max ? 5 : (maxw1 <= skel_warp_max ? 6 : 3);
             L.stride_or_delta = S;
             t->plan.push_back(L);
+            if (tiled) {  // all passes in one tiled kernel + per-row finalize
+                LaunchH P = L;
+                P.kind = 7;
+                P.stride_or_delta = S;
+                P.ustride = maxw1;
+                t->plan.push_back(P);
+                P.kind = 8;
+                t->plan.push_back(P);
+                continue;
+            }
             for (int32_t dl = S / 2; dl >= 1; dl /= 2) {
                 LaunchH P = L;
                 P.kind = 4;
@@ -473,6 +494,8 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     t->h2d_bytes = (int64_t)meta.size() + (rows_dev ? 0 : t->m_slab) + (cols_dev ? 0 : n);
     // the pageable-host copy above is staged synchronously, so `meta` may die
     BCK(cudaMemsetAsync(t->d_node_wstar, 0, (size_t)nn * 4, s));
+    if (kmax_region_elems > 0)
+        BCK(cudaMemsetAsync(t->d_tables + kmax_region, 0xFF, (size_t)kmax_region_elems * 4, s));
     BCKL(launch_nx(t->d_cols, (int32_t)n, t->d_nx, t->d_sym_wstar, s));
     BCKL(launch_leaf_wstar(t->d_rows, t->d_leaf_nodes, t->d_leaf_rows, t->nleaves,
                            t->d_sym_wstar, t->d_node_wstar, s));
@@ -487,6 +510,11 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
         else if (L.kind == 5 || L.kind == 6)
             BCKL(launch_combine(L.kind == 5 ? 0 : 1, dd, L.count, c, L.shift, L.key64, s,
                                 L.stride_or_delta));
+        else if (L.kind == 7)
+            BCKL(launch_block_refine(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, tile_j,
+                                     tile_wk, L.ustride, s));
+        else if (L.kind == 8)
+            BCKL(launch_finalize_rows(dd, L.count, c, L.stride_or_delta, s));
         else if (refine_rows(n1, L.stride_or_delta) > 0)
             BCKL(launch_refine(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s));
     }

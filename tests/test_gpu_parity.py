@@ -287,3 +287,32 @@ def test_skeleton_refine_strides(stride, monkeypatch):
             length = L.lcs_length(tab)
             np.testing.assert_array_equal(L.recover_cross_vertices(g, tab, length),
                                           t.recover(length))
+
+
+@pytest.mark.parametrize("env", [
+    {"LCSG_TILE_J": "32", "LCSG_TILE_WK": "32"},           # many tiles, U window overflow
+    {"LCSG_TILE_J": "512", "LCSG_TILE_WK": "1024", "LCSG_SKELETON_STRIDE": "32"},
+    {"LCSG_REFINE_PASSES": "1"},                            # one launch per refinement pass
+    {"LCSG_THREAD_MAX_W1": "3", "LCSG_SKEL_THREAD_MAX_W1": "3", "LCSG_SKEL_WARP_MAX_W1": "9"},
+])
+def test_refinement_variants(env, monkeypatch):
+    """Every geometry / schedule of the wide-table combine is bit-exact."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(hash(tuple(sorted(env.items()))) % 2**32)
+    for _ in range(8):
+        m = int(rng.integers(40, 300))
+        n = int(rng.integers(20, 500))
+        sigma = int(rng.choice([2, 4, 26]))
+        a, b = workloads.random_pair(rng, m, n, sigma)
+        g = L.GridModel(a, b)
+        t = O.OracleTree(a, b)
+        nodes = gpu_tree_nodes(L.build_cost_table(g, 1, m + 1))
+        for idx in range(len(t)):
+            exp = t.node(idx)
+            if exp.upper < 0:
+                continue
+            np.testing.assert_array_equal(nodes[idx].reach, exp.reach, err_msg=f"{env} {idx}")
+            np.testing.assert_array_equal(nodes[idx].trace, exp.trace, err_msg=f"{env} {idx}")
+            np.testing.assert_array_equal(nodes[idx].kmax, exp.kmax)
+            assert nodes[idx].wstar == exp.wstar
