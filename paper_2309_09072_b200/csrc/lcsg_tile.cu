@@ -1,4 +1,4 @@
-// lcsg_tile.cu -- tiled refinement of the wide combines (the fast path).
+// lcsg_tile.cu -- column-parallel refinement of the wide combines (the fast path).
 //
 // After the skeleton rows i = 0, S, 2S, ..., n of a combine are known (exact
 // Alg. 1, lcsg_refine.cu), every interior row is derived by refinement:
@@ -60,183 +60,138 @@ __device__ __forceinline__ int32_t tcell(const TabAcc &L, int32_t x, int32_t k, 
     return tab_get(L, (int64_t)x - 1, j - k);
 }
 
-struct TileGeo {
-    int32_t S;      // rows per block (power of two, <= BT_MAXS)
-    int32_t TJ;     // columns per tile
-    int32_t WK;     // staged U-window width (k entries per row)
-    int32_t nblk;   // row blocks per combine
-    int32_t ntile;  // column tiles per combine
-};
-
-template <typename Key>
-__global__ void __launch_bounds__(BT_THREADS)
-    block_refine_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int shift,
-                        TileGeo g) {
-    extern __shared__ int32_t smem[];
-    __shared__ int32_t s_kwlo;
-    __shared__ int32_t s_kmaxc[BT_MAXS + 1];
-    __shared__ int32_t s_rowmax[BT_MAXS + 1];
-    __shared__ int32_t s_ntail[2];
-    __shared__ int2 s_tail[BT_TAILCAP];
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int64_t per_desc = (int64_t)g.nblk * g.ntile;
-    const int64_t di = blockIdx.x / per_desc;
+// One lane = one column j of one row block [i0, i0+S]: the block's two
+// skeleton cells of column j are loaded, then the S-1 interior cells are
+// derived in divide-and-conquer order (delta = S/2 ... 1), all in registers
+// (the unrolled passes index R[] / T[] statically).  Neighbouring lanes hold
+// neighbouring columns, so U and L reads of a warp hit few lines and the
+// final writes are coalesced.  A short last block (rb < S rows) treats the
+// local rows >= rb as copies of its bottom skeleton row; the interleave
+// search window then over-covers, which keeps the bound valid.
+template <typename Key, int S>
+__global__ void __launch_bounds__(256)
+    column_refine_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int shift,
+                         int32_t nblk, int32_t w1max, int64_t spd) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t di = gt / spd;  // warp-uniform: spd % 32 == 0
     if (di >= ndesc) return;
-    const int64_t rem = blockIdx.x - di * per_desc;
-    const int32_t blk = (int32_t)(rem / g.ntile), tile = (int32_t)(rem - (int64_t)blk * g.ntile);
+    const int64_t slot = gt - di * spd;
+    const int32_t blk = (int32_t)(slot / w1max);
+    const int32_t j = (int32_t)(slot - (int64_t)blk * w1max);
     const CombineDesc &d = descs[di];
     const int64_t n1 = (int64_t)c.n + 1;
-    const int64_t i0 = (int64_t)blk * g.S;
-    const int32_t rb = (int32_t)min((int64_t)g.S, n1 - 1 - i0);  // local index of the bottom skeleton row
-    const int32_t w1 = d.w1;
-    const int32_t j0 = tile * g.TJ;
-    if (j0 >= w1 || rb <= 1) return;  // block-uniform: nothing interior here
-    const int32_t tw = min(g.TJ, w1 - j0);
-    const int32_t TJ = g.TJ, WK = g.WK;
-    int32_t *tR = smem;
-    int32_t *tT = tR + (g.S + 1) * TJ;
-    int32_t *Uw = tT + (g.S + 1) * TJ;
     const int32_t inf = c.inf;
+    const bool active = blk < nblk && j < d.w1;
+    const int64_t i0 = (int64_t)blk * S;
+    const int32_t rb = active ? (int32_t)min((int64_t)S, n1 - 1 - i0) : 0;
     const TabAcc U = resolve(d.U, c), L = resolve(d.L, c);
     const int32_t wl = L.w1 - 1;
+    const int32_t w1 = d.w1;
 
-    // 1. the two skeleton rows of the block, per-row kmax of U
-    for (int e = tid; e < 2 * tw; e += BT_THREADS) {
-        const int32_t r = e < tw ? 0 : rb, jj = e < tw ? e : e - tw;
-        const int64_t off = (i0 + r) * w1 + j0 + jj;
-        tR[r * TJ + jj] = __ldg(d.out_reach + off);
-        tT[r * TJ + jj] = __ldg(d.out_trace + off);
+    int32_t R[S + 1], T[S + 1];
+#pragma unroll
+    for (int r = 0; r <= S; ++r) {
+        R[r] = inf;
+        T[r] = 0;
     }
-    for (int r = tid; r <= rb; r += BT_THREADS) {
-        s_kmaxc[r] = tab_kmax(U, i0 + r, inf);
-        s_rowmax[r] = -1;
-    }
-    if (tid == 0) {
-        s_kwlo = INT_MAX;
-        s_ntail[0] = s_ntail[1] = 0;
-    }
-    __syncthreads();
-    // 2. U window: k >= min_j T(top skeleton, j) - S covers every bound of the block
-    int32_t m = INT_MAX;
-    for (int jj = tid; jj < tw; jj += BT_THREADS)
-        if (tR[jj] < inf) m = min(m, tT[jj]);
-    m = __reduce_min_sync(0xffffffffu, m);
-    if (lane == 0 && m != INT_MAX) atomicMin(&s_kwlo, m);
-    __syncthreads();
-    if (s_kwlo == INT_MAX) return;  // top row INF on the whole tile => every row is
-    const int32_t kwlo = max(0, s_kwlo - g.S);
-    for (int e = tid; e < (rb + 1) * WK; e += BT_THREADS) {
-        const int32_t r = e / WK, kk = e - r * WK;
-        const int32_t k = kwlo + kk;
-        if (k <= s_kmaxc[r]) Uw[e] = tab_get(U, i0 + r, k);
-    }
-    __syncthreads();
-    auto uget = [&](int32_t r, int32_t k) -> int32_t {
-        const int32_t kk = k - kwlo;
-        if ((unsigned)kk < (unsigned)WK) return Uw[r * WK + kk];
-        return tab_get(U, i0 + r, k);
-    };
-
-    // 3. refinement passes, all in shared memory
-    int pass = 0;
-    for (int32_t dl = g.S >> 1; dl >= 1; dl >>= 1, ++pass) {
-        if (rb <= dl) continue;  // block-uniform
-        const int32_t nr = (rb - dl + 2 * dl - 1) / (2 * dl);
-        const int32_t total = nr * tw;
-        int32_t *ntail = &s_ntail[pass & 1];
-        if (tid == 0) s_ntail[(pass + 1) & 1] = 0;
-        for (int32_t e = tid; e < total; e += BT_THREADS) {
-            const int32_t t = e / tw, jj = e - t * tw;
-            const int32_t r = dl * (2 * t + 1), a = r - dl, b = min(r + dl, rb);
-            const int32_t j = j0 + jj;
-            if (tR[a * TJ + jj] >= inf) {  // (a, j) INF => (c, j) INF
-                tR[r * TJ + jj] = inf;
-                continue;
+    if (active && rb >= 2) {
+        R[0] = __ldg(d.out_reach + i0 * w1 + j);
+        T[0] = __ldg(d.out_trace + i0 * w1 + j);
+        const int32_t rbv = __ldg(d.out_reach + (i0 + rb) * w1 + j);
+        const int32_t rbt = __ldg(d.out_trace + (i0 + rb) * w1 + j);
+#pragma unroll
+        for (int r = 1; r <= S; ++r)
+            if (r >= rb) {
+                R[r] = rbv;
+                T[r] = rbt;
             }
-            if (tR[b * TJ + jj] >= inf) {  // no upper bound: queue for the warps
-                const int q = atomicAdd(ntail, 1);
-                if (q < BT_TAILCAP) {
-                    s_tail[q] = make_int2(r, jj);
-                    continue;
+    }
+#pragma unroll
+    for (int dl = S / 2; dl >= 1; dl >>= 1) {
+#pragma unroll
+        for (int r = dl; r < S; r += 2 * dl) {
+            const int a = r - dl, b = r + dl;  // b <= S; rows >= rb mirror the bottom row
+            const bool real = active && r < rb;
+            const int64_t ci = i0 + r;
+            const int32_t kmc = real ? tab_kmax(U, ci, inf) : -1;
+            bool tail = false;
+            int32_t kl = 0;
+            if (real && R[a] < inf) {
+                const int32_t Ta = T[a];
+                const int32_t Xa = tab_get(U, i0 + a, Ta);
+                int32_t hi = min(Ta, kmc);
+                int32_t lo = min(max(0, Ta - dl), hi);
+                while (lo < hi) {  // first k with U[c,k] >= X(a,j)
+                    const int32_t md = (lo + hi) >> 1;
+                    if (tab_get(U, ci, md) >= Xa) hi = md; else lo = md + 1;
                 }
-            }
-            const int32_t kmc = s_kmaxc[r];
-            const int32_t Ta = tT[a * TJ + jj];
-            const int32_t Xa = uget(a, Ta);
-            int32_t hi = min(Ta, kmc);
-            int32_t lo = min(max(0, Ta - dl), hi);
-            while (lo < hi) {  // first k with U[c,k] >= X(a,j)
-                const int32_t md = (lo + hi) >> 1;
-                if (uget(r, md) >= Xa) hi = md; else lo = md + 1;
-            }
-            int32_t kl = max(lo, j - wl), kh;
-            if (tR[b * TJ + jj] < inf) {
-                const int32_t Tb = tT[b * TJ + jj];
-                const int32_t Xb = uget(b, Tb);
-                lo = min(Tb, kmc);
-                hi = min(Tb + (b - r), kmc);
-                while (lo < hi) {  // last k with U[c,k] <= X(b,j)
-                    const int32_t md = (lo + hi + 1) >> 1;
-                    if (uget(r, md) <= Xb) lo = md; else hi = md - 1;
-                }
-                kh = min(lo, j);
-                if (kl > kh) {  // safety net: never taken when the bounds hold
-                    kl = max(0, j - wl);
-                    kh = min(j, kmc);
+                kl = max(lo, j - wl);
+                if (R[b] < inf) {
+                    const int32_t Tb = T[b];
+                    const int32_t Xb = tab_get(U, min(i0 + b, i0 + rb), Tb);
+                    lo = min(Tb, kmc);
+                    hi = min(Tb + dl, kmc);
+                    while (lo < hi) {  // last k with U[c,k] <= X(b,j)
+                        const int32_t md = (lo + hi + 1) >> 1;
+                        if (tab_get(U, ci, md) <= Xb) lo = md; else hi = md - 1;
+                    }
+                    int32_t kh = min(lo, j);
+                    if (kl > kh) {  // safety net: never taken when the bounds hold
+                        kl = max(0, j - wl);
+                        kh = min(j, kmc);
+                    }
+                    Key best = ~(Key)0;
+                    for (int32_t k = kl; k <= kh; ++k) {
+                        const Key key = tpack<Key>(tcell(L, tab_get(U, ci, k), k, j, inf, wl), k, shift);
+                        best = key < best ? key : best;
+                    }
+                    R[r] = tval<Key>(best, shift);
+                    T[r] = tk<Key>(best, shift);
+                } else {
+                    tail = true;
                 }
             } else {
-                kh = min(j, kmc);  // tail cell, queue overflowed
+                R[r] = inf;
             }
-            Key best = ~(Key)0;
-            for (int32_t k = kl; k <= kh; ++k) {
-                const Key key = tpack<Key>(tcell(L, uget(r, k), k, j, inf, wl), k, shift);
-                best = key < best ? key : best;
+            // tail cells (finite above, INF below: no upper bound): the whole
+            // warp scans each one's range [kl, min(j, kmax_c)] in turn
+            unsigned mask = __ballot_sync(0xffffffffu, tail);
+            while (mask) {
+                const int src = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const int32_t tj = __shfl_sync(0xffffffffu, j, src);
+                const int32_t tkl = __shfl_sync(0xffffffffu, kl, src);
+                const int32_t tkh = min(tj, __shfl_sync(0xffffffffu, kmc, src));
+                const int64_t trow = __shfl_sync(0xffffffffu, ci, src);
+                Key best = ~(Key)0;
+                for (int32_t k = tkl + lane; k <= tkh; k += 32) {
+                    const Key key = tpack<Key>(tcell(L, tab_get(U, trow, k), k, tj, inf, wl), k, shift);
+                    best = key < best ? key : best;
+                }
+                best = twarp_min(best);
+                if (lane == src) {
+                    R[r] = tval<Key>(best, shift);
+                    T[r] = tk<Key>(best, shift);
+                }
             }
-            tR[r * TJ + jj] = tval<Key>(best, shift);
-            tT[r * TJ + jj] = tk<Key>(best, shift);
-        }
-        __syncthreads();
-        const int32_t nt = min(*ntail, BT_TAILCAP);
-        for (int32_t q = wid; q < nt; q += BT_THREADS / 32) {
-            const int2 tc = s_tail[q];
-            const int32_t r = tc.x, jj = tc.y, a = r - dl, j = j0 + jj;
-            const int32_t kmc = s_kmaxc[r];
-            const int32_t Ta = tT[a * TJ + jj];
-            const int32_t Xa = uget(a, Ta);
-            int32_t hi = min(Ta, kmc);
-            int32_t lo = min(max(0, Ta - dl), hi);
-            while (lo < hi) {
-                const int32_t md = (lo + hi) >> 1;
-                if (uget(r, md) >= Xa) hi = md; else lo = md + 1;
-            }
-            const int32_t kl = max(lo, j - wl), kh = min(j, kmc);
-            Key best = ~(Key)0;
-            for (int32_t k = kl + lane; k <= kh; k += 32) {
-                const Key key = tpack<Key>(tcell(L, uget(r, k), k, j, inf, wl), k, shift);
-                best = key < best ? key : best;
-            }
-            best = twarp_min(best);
-            if (lane == 0) {
-                tR[r * TJ + jj] = tval<Key>(best, shift);
-                tT[r * TJ + jj] = tk<Key>(best, shift);
-            }
-        }
-        __syncthreads();
-    }
-    // 4. write the finite cells of the interior rows; per-row max finite column
-    for (int32_t e = tid; e < (rb - 1) * tw; e += BT_THREADS) {
-        const int32_t r = 1 + e / tw, jj = e - (r - 1) * tw;
-        const int32_t v = tR[r * TJ + jj];
-        if (v < inf) {
-            const int64_t off = (i0 + r) * w1 + j0 + jj;
-            d.out_reach[off] = v;
-            d.out_trace[off] = tT[r * TJ + jj];
-            atomicMax(&s_rowmax[r], j0 + jj);
         }
     }
-    __syncthreads();
-    for (int r = 1 + tid; r < rb; r += BT_THREADS)
-        if (s_rowmax[r] >= 0) atomicMax(d.out_kmax + i0 + r, s_rowmax[r]);
+    // write the finite interior cells; report the finite frontier of each row
+#pragma unroll
+    for (int r = 1; r < S; ++r) {
+        const bool fin = active && r < rb && R[r] < inf;
+        if (fin) {
+            const int64_t off = (i0 + r) * w1 + j;
+            d.out_reach[off] = R[r];
+            d.out_trace[off] = T[r];
+        }
+        // frontier: finite here and the next lane's cell (same row) is not
+        const int64_t row = i0 + r;
+        const bool nfin = __shfl_down_sync(0xffffffffu, fin, 1);
+        const int64_t nrow = __shfl_down_sync(0xffffffffu, row, 1);
+        if (fin && (lane == 31 || !nfin || nrow != row)) atomicMax(d.out_kmax + row, j);
+    }
 }
 
 // Per interior row: kmax is final (max over tiles); write the INF suffix
@@ -298,28 +253,30 @@ __global__ void __launch_bounds__(32 * FN_WARPS)
 
 int launch_block_refine(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
                         int32_t S, int32_t TJ, int32_t WK, int32_t maxw1, cudaStream_t s) {
+    (void)TJ;
+    (void)WK;
     if (ndesc <= 0) return 0;
     const int64_t n1 = (int64_t)c.n + 1;
-    if (S < 2 || S > BT_MAXS) return (int)cudaErrorInvalidValue;
-    TileGeo g;
-    g.S = S;
-    g.TJ = TJ;
-    g.WK = WK;
-    g.nblk = (int32_t)((n1 - 1 + S - 1) / S);
-    g.ntile = (maxw1 + TJ - 1) / TJ;
-    if (g.nblk <= 0) return 0;
-    const size_t smem = (size_t)(S + 1) * (2 * TJ + WK) * 4;
-    const unsigned blocks = (unsigned)((int64_t)g.nblk * g.ntile * ndesc);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(block_refine_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-        cudaFuncSetAttribute(block_refine_kernel<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-        attr = true;
+    const int32_t nblk = (int32_t)((n1 - 1 + S - 1) / S);
+    if (nblk <= 0) return 0;
+    const int64_t spd = ((int64_t)nblk * maxw1 + 31) / 32 * 32;
+    const unsigned blocks = (unsigned)((spd * ndesc + 255) / 256);
+#define LCSG_COLREF(SS)                                                                        \
+    if (key64)                                                                                 \
+        column_refine_kernel<uint64_t, SS><<<blocks, 256, 0, s>>>(descs, ndesc, c, shift, nblk, \
+                                                                  maxw1, spd);                 \
+    else                                                                                       \
+        column_refine_kernel<uint32_t, SS><<<blocks, 256, 0, s>>>(descs, ndesc, c, shift, nblk, \
+                                                                  maxw1, spd);
+    switch (S) {
+        case 2: LCSG_COLREF(2) break;
+        case 4: LCSG_COLREF(4) break;
+        case 8: LCSG_COLREF(8) break;
+        case 16: LCSG_COLREF(16) break;
+        case 32: LCSG_COLREF(32) break;
+        default: return (int)cudaErrorInvalidValue;
     }
-    if (key64)
-        block_refine_kernel<uint64_t><<<blocks, BT_THREADS, smem, s>>>(descs, ndesc, c, shift, g);
-    else
-        block_refine_kernel<uint32_t><<<blocks, BT_THREADS, smem, s>>>(descs, ndesc, c, shift, g);
+#undef LCSG_COLREF
     LCSG_LAUNCH_CHECK();
     return 0;
 }
