@@ -272,7 +272,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     const int skel_thread_max = env_int("LCSG_SKEL_THREAD_MAX_W1", 257);
     const int skel_warp_max = env_int("LCSG_SKEL_WARP_MAX_W1", 4097);
     // refinement mode: tiled (default) or one launch per pass ("LCSG_REFINE_PASSES=1")
-    const bool tiled = env_int("LCSG_REFINE_PASSES", 0) == 0 && skel_stride <= 32;
+    const bool tiled = env_int("LCSG_REFINE_PASSES", 0) == 0 && skel_stride <= 64;
     const int tile_j = std::max(32, env_int("LCSG_TILE_J", 128));
     const int tile_wk = std::max(32, env_int("LCSG_TILE_WK", 256));
     size_t o_tab = off;

@@ -62,18 +62,27 @@ __device__ __forceinline__ int32_t tcell(const TabAcc &L, int32_t x, int32_t k, 
 
 // One lane = one column j of one row block [i0, i0+S]: the block's two
 // skeleton cells of column j are loaded, then the S-1 interior cells are
-// derived in divide-and-conquer order (delta = S/2 ... 1), all in registers
-// (the unrolled passes index R[] / T[] statically).  Neighbouring lanes hold
+// derived in divide-and-conquer order (delta = S/2 ... 1).  The column's
+// (reach, trace) values live in a per-thread slice of shared memory (no
+// cross-thread sharing, no barriers); the cell body is a single, non-unrolled
+// copy of code (a fully unrolled variant thrashed the instruction cache: 76%
+// of stall samples were `no_instructions`).  Neighbouring lanes hold
 // neighbouring columns, so U and L reads of a warp hit few lines and the
 // final writes are coalesced.  A short last block (rb < S rows) treats the
 // local rows >= rb as copies of its bottom skeleton row; the interleave
-// search window then over-covers, which keeps the bound valid.
-template <typename Key, int S>
-__global__ void __launch_bounds__(256)
+// search window then over-covers, which keeps the bound valid.  U and L are
+// always materialised slabs here (never leaves), so plain row pointers are used.
+constexpr int CR_THREADS = 256;
+
+template <typename Key>
+__global__ void __launch_bounds__(CR_THREADS)
     column_refine_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int shift,
-                         int32_t nblk, int32_t w1max, int64_t spd) {
+                         int32_t S, int32_t nblk, int32_t w1max, int64_t spd) {
+    extern __shared__ int32_t csm[];
+    int32_t *sR = csm + threadIdx.x;                     // sR[r * CR_THREADS]
+    int32_t *sT = csm + (S + 1) * CR_THREADS + threadIdx.x;
     const int lane = threadIdx.x & 31;
-    const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t gt = blockIdx.x * (int64_t)CR_THREADS + threadIdx.x;
     const int64_t di = gt / spd;  // warp-uniform: spd % 32 == 0
     if (di >= ndesc) return;
     const int64_t slot = gt - di * spd;
@@ -85,56 +94,57 @@ __global__ void __launch_bounds__(256)
     const bool active = blk < nblk && j < d.w1;
     const int64_t i0 = (int64_t)blk * S;
     const int32_t rb = active ? (int32_t)min((int64_t)S, n1 - 1 - i0) : 0;
-    const TabAcc U = resolve(d.U, c), L = resolve(d.L, c);
-    const int32_t wl = L.w1 - 1;
+    const int32_t *__restrict__ Ur = d.U.reach;
+    const int32_t *__restrict__ Uk = d.U.kmax;
+    const int32_t *__restrict__ Lr = d.L.reach;
+    const int32_t uw1 = d.U.w1, lw1 = d.L.w1, wl = lw1 - 1;
     const int32_t w1 = d.w1;
 
-    int32_t R[S + 1], T[S + 1];
-#pragma unroll
-    for (int r = 0; r <= S; ++r) {
-        R[r] = inf;
-        T[r] = 0;
+    {
+        int32_t r0v = inf, r0t = 0, rbv = inf, rbt = 0;
+        if (active && rb >= 2) {
+            r0v = __ldg(d.out_reach + i0 * w1 + j);
+            r0t = __ldg(d.out_trace + i0 * w1 + j);
+            rbv = __ldg(d.out_reach + (i0 + rb) * w1 + j);
+            rbt = __ldg(d.out_trace + (i0 + rb) * w1 + j);
+        }
+        sR[0] = r0v;
+        sT[0] = r0t;
+        for (int r = 1; r <= S; ++r) {
+            sR[r * CR_THREADS] = r >= rb ? rbv : inf;
+            sT[r * CR_THREADS] = r >= rb ? rbt : 0;
+        }
     }
-    if (active && rb >= 2) {
-        R[0] = __ldg(d.out_reach + i0 * w1 + j);
-        T[0] = __ldg(d.out_trace + i0 * w1 + j);
-        const int32_t rbv = __ldg(d.out_reach + (i0 + rb) * w1 + j);
-        const int32_t rbt = __ldg(d.out_trace + (i0 + rb) * w1 + j);
-#pragma unroll
-        for (int r = 1; r <= S; ++r)
-            if (r >= rb) {
-                R[r] = rbv;
-                T[r] = rbt;
-            }
-    }
-#pragma unroll
-    for (int dl = S / 2; dl >= 1; dl >>= 1) {
-#pragma unroll
+#pragma unroll 1
+    for (int dl = S >> 1; dl >= 1; dl >>= 1) {
+#pragma unroll 1
         for (int r = dl; r < S; r += 2 * dl) {
             const int a = r - dl, b = r + dl;  // b <= S; rows >= rb mirror the bottom row
             const bool real = active && r < rb;
             const int64_t ci = i0 + r;
-            const int32_t kmc = real ? tab_kmax(U, ci, inf) : -1;
+            const int32_t *Uc = Ur + ci * uw1;
+            const int32_t kmc = real ? __ldg(Uk + ci) : -1;
+            const int32_t Ra = sR[a * CR_THREADS], Rb = sR[b * CR_THREADS];
             bool tail = false;
-            int32_t kl = 0;
-            if (real && R[a] < inf) {
-                const int32_t Ta = T[a];
-                const int32_t Xa = tab_get(U, i0 + a, Ta);
+            int32_t kl = 0, outv = inf, outk = 0;
+            if (real && Ra < inf) {
+                const int32_t Ta = sT[a * CR_THREADS];
+                const int32_t Xa = __ldg(Ur + (i0 + a) * uw1 + Ta);
                 int32_t hi = min(Ta, kmc);
                 int32_t lo = min(max(0, Ta - dl), hi);
                 while (lo < hi) {  // first k with U[c,k] >= X(a,j)
                     const int32_t md = (lo + hi) >> 1;
-                    if (tab_get(U, ci, md) >= Xa) hi = md; else lo = md + 1;
+                    if (__ldg(Uc + md) >= Xa) hi = md; else lo = md + 1;
                 }
                 kl = max(lo, j - wl);
-                if (R[b] < inf) {
-                    const int32_t Tb = T[b];
-                    const int32_t Xb = tab_get(U, min(i0 + b, i0 + rb), Tb);
+                if (Rb < inf) {
+                    const int32_t Tb = sT[b * CR_THREADS];
+                    const int32_t Xb = __ldg(Ur + min(i0 + b, i0 + rb) * uw1 + Tb);
                     lo = min(Tb, kmc);
                     hi = min(Tb + dl, kmc);
                     while (lo < hi) {  // last k with U[c,k] <= X(b,j)
                         const int32_t md = (lo + hi + 1) >> 1;
-                        if (tab_get(U, ci, md) <= Xb) lo = md; else hi = md - 1;
+                        if (__ldg(Uc + md) <= Xb) lo = md; else hi = md - 1;
                     }
                     int32_t kh = min(lo, j);
                     if (kl > kh) {  // safety net: never taken when the bounds hold
@@ -143,16 +153,20 @@ __global__ void __launch_bounds__(256)
                     }
                     Key best = ~(Key)0;
                     for (int32_t k = kl; k <= kh; ++k) {
-                        const Key key = tpack<Key>(tcell(L, tab_get(U, ci, k), k, j, inf, wl), k, shift);
+                        const int32_t x = __ldg(Uc + k);  // finite: k <= kmax_c
+                        const int32_t v = __ldg(Lr + (int64_t)(x - 1) * lw1 + (j - k));
+                        const Key key = tpack<Key>(v, k, shift);
                         best = key < best ? key : best;
                     }
-                    R[r] = tval<Key>(best, shift);
-                    T[r] = tk<Key>(best, shift);
+                    outv = tval<Key>(best, shift);
+                    outk = tk<Key>(best, shift);
                 } else {
                     tail = true;
                 }
-            } else {
-                R[r] = inf;
+            }
+            if (!tail) {
+                sR[r * CR_THREADS] = outv;
+                sT[r * CR_THREADS] = outk;
             }
             // tail cells (finite above, INF below: no upper bound): the whole
             // warp scans each one's range [kl, min(j, kmax_c)] in turn
@@ -164,30 +178,34 @@ __global__ void __launch_bounds__(256)
                 const int32_t tkl = __shfl_sync(0xffffffffu, kl, src);
                 const int32_t tkh = min(tj, __shfl_sync(0xffffffffu, kmc, src));
                 const int64_t trow = __shfl_sync(0xffffffffu, ci, src);
+                const int32_t *Ut = Ur + trow * uw1;
                 Key best = ~(Key)0;
                 for (int32_t k = tkl + lane; k <= tkh; k += 32) {
-                    const Key key = tpack<Key>(tcell(L, tab_get(U, trow, k), k, tj, inf, wl), k, shift);
+                    int32_t v = inf;
+                    if (tj - k <= wl) v = __ldg(Lr + (int64_t)(__ldg(Ut + k) - 1) * lw1 + (tj - k));
+                    const Key key = tpack<Key>(v, k, shift);
                     best = key < best ? key : best;
                 }
                 best = twarp_min(best);
                 if (lane == src) {
-                    R[r] = tval<Key>(best, shift);
-                    T[r] = tk<Key>(best, shift);
+                    sR[r * CR_THREADS] = tval<Key>(best, shift);
+                    sT[r * CR_THREADS] = tk<Key>(best, shift);
                 }
             }
         }
     }
     // write the finite interior cells; report the finite frontier of each row
-#pragma unroll
+#pragma unroll 1
     for (int r = 1; r < S; ++r) {
-        const bool fin = active && r < rb && R[r] < inf;
+        const int32_t v = sR[r * CR_THREADS];
+        const bool fin = active && r < rb && v < inf;
+        const int64_t row = i0 + r;
         if (fin) {
-            const int64_t off = (i0 + r) * w1 + j;
-            d.out_reach[off] = R[r];
-            d.out_trace[off] = T[r];
+            const int64_t off = row * w1 + j;
+            d.out_reach[off] = v;
+            d.out_trace[off] = sT[r * CR_THREADS];
         }
         // frontier: finite here and the next lane's cell (same row) is not
-        const int64_t row = i0 + r;
         const bool nfin = __shfl_down_sync(0xffffffffu, fin, 1);
         const int64_t nrow = __shfl_down_sync(0xffffffffu, row, 1);
         if (fin && (lane == 31 || !nfin || nrow != row)) atomicMax(d.out_kmax + row, j);
@@ -256,27 +274,25 @@ int launch_block_refine(const CombineDesc *descs, int32_t ndesc, Ctx c, int shif
     (void)TJ;
     (void)WK;
     if (ndesc <= 0) return 0;
+    if (S < 2 || S > 64) return (int)cudaErrorInvalidValue;
     const int64_t n1 = (int64_t)c.n + 1;
     const int32_t nblk = (int32_t)((n1 - 1 + S - 1) / S);
     if (nblk <= 0) return 0;
     const int64_t spd = ((int64_t)nblk * maxw1 + 31) / 32 * 32;
-    const unsigned blocks = (unsigned)((spd * ndesc + 255) / 256);
-#define LCSG_COLREF(SS)                                                                        \
-    if (key64)                                                                                 \
-        column_refine_kernel<uint64_t, SS><<<blocks, 256, 0, s>>>(descs, ndesc, c, shift, nblk, \
-                                                                  maxw1, spd);                 \
-    else                                                                                       \
-        column_refine_kernel<uint32_t, SS><<<blocks, 256, 0, s>>>(descs, ndesc, c, shift, nblk, \
-                                                                  maxw1, spd);
-    switch (S) {
-        case 2: LCSG_COLREF(2) break;
-        case 4: LCSG_COLREF(4) break;
-        case 8: LCSG_COLREF(8) break;
-        case 16: LCSG_COLREF(16) break;
-        case 32: LCSG_COLREF(32) break;
-        default: return (int)cudaErrorInvalidValue;
+    const unsigned blocks = (unsigned)((spd * ndesc + CR_THREADS - 1) / CR_THREADS);
+    const size_t smem = (size_t)2 * (S + 1) * CR_THREADS * 4;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(column_refine_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
+        cudaFuncSetAttribute(column_refine_kernel<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
+        attr = true;
     }
-#undef LCSG_COLREF
+    if (key64)
+        column_refine_kernel<uint64_t><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift, S,
+                                                                       nblk, maxw1, spd);
+    else
+        column_refine_kernel<uint32_t><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift, S,
+                                                                       nblk, maxw1, spd);
     LCSG_LAUNCH_CHECK();
     return 0;
 }
