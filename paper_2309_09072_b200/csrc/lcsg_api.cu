@@ -284,7 +284,10 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
         ++ncomb;
         maxh0 = std::max(maxh0, nd.height);
         const int32_t wu1 = t->nodes[nd.upper].w1;
-        nd.kind = nd.w1 <= thread_max_w1 ? 0 : 2;
+        // the refinement kernels read both children as materialised slabs
+        const bool kids_are_slabs =
+            t->nodes[nd.upper].upper >= 0 && t->nodes[nd.lower].upper >= 0;
+        nd.kind = (nd.w1 <= thread_max_w1 || !kids_are_slabs) ? 0 : 2;
         (void)wu1;
         if (skel_stride == 1 && nd.kind == 2) nd.kind = 1;
         nd.reach_off = tab_elems;
