@@ -517,7 +517,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             BCKL(launch_block_refine(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, tile_j,
                                      tile_wk, L.ustride, s));
         else if (L.kind == 8)
-            BCKL(launch_finalize_rows(dd, L.count, c, L.stride_or_delta, s));
+            BCKL(launch_finalize_rows(dd, L.count, c, L.stride_or_delta, s, L.ustride));
         else if (refine_rows(n1, L.stride_or_delta) > 0)
             BCKL(launch_refine(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s));
     }

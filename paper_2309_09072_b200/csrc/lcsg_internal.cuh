@@ -105,7 +105,7 @@ int launch_block_refine(const CombineDesc *descs, int32_t ndesc, Ctx c, int shif
                         int32_t S, int32_t TJ, int32_t WK, int32_t maxw1, cudaStream_t s);
 // INF suffix + kmax/wstar of the interior rows after the tiled refinement
 int launch_finalize_rows(const CombineDesc *descs, int32_t ndesc, Ctx c, int32_t S,
-                         cudaStream_t s);
+                         cudaStream_t s, int32_t maxw1);
 int launch_walk_level(const WalkNode *nodes, const int32_t *ids, int32_t count, Ctx c,
                       int32_t *wi, int32_t *wj, int32_t *cols_out, bool retrace, int key_shift,
                       bool key64, cudaStream_t s);

@@ -30,8 +30,7 @@ namespace lcsg {
 constexpr int BT_THREADS = 256;
 constexpr int BT_MAXS = 64;
 constexpr int BT_TAILCAP = 512;
-constexpr int FN_SEGS = 40;
-constexpr int FN_WARPS = 8;
+constexpr int FN_WARPS = 4;
 
 template <typename Key>
 __device__ __forceinline__ Key tpack(int32_t v, int32_t k, int shift) {
@@ -212,61 +211,84 @@ __global__ void __launch_bounds__(CR_THREADS)
     }
 }
 
-// Per interior row: kmax is final (max over tiles); write the INF suffix
-// (K, w] -- reach INF, trace = `top` of the Alg. 1 node covering the column
-// (replay of the reference bisection, _kernel.pyx:53-60) or 0 beyond colhi
-// (_kernel.pyx:79-82) -- and fold kmax into wstar.
+// Per interior row: kmax is final (max over column blocks); write the INF
+// suffix (K, w] -- reach INF, trace = `top` of the Alg. 1 node covering the
+// column (replay of the reference bisection, _kernel.pyx:53-60) or 0 beyond
+// colhi (_kernel.pyx:79-82) -- and fold kmax into wstar.  A warp owns RPW
+// consecutive rows: lane r replays row r's path (no gathers; the INF nodes'
+// mids tile (K, colhi] in descending order), then the warp fills the rows
+// one after another with coalesced stores.
+constexpr int FN_MAXSEG = 34;
+
 __global__ void __launch_bounds__(32 * FN_WARPS)
-    finalize_rows_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int32_t S) {
-    __shared__ int4 seg_all[FN_WARPS][FN_SEGS];
+    finalize_rows_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int32_t S,
+                         int rpw) {
+    __shared__ int2 seg_all[FN_WARPS][32][FN_MAXSEG];
+    __shared__ int nseg_all[FN_WARPS][32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t n1 = (int64_t)c.n + 1;
+    const int64_t rows_pd = (n1 + rpw - 1) / rpw * rpw;  // padded rows per desc
     const int64_t gw = blockIdx.x * (int64_t)FN_WARPS + wid;
-    const int64_t di = gw / n1;
-    if (di >= ndesc) return;
-    const int64_t i = gw - di * n1;
-    if (i % S == 0 || i == n1 - 1) return;  // skeleton rows are complete
-    int4 *seg = seg_all[wid];
+    const int64_t di = (gw * rpw) / rows_pd;
+    if (di >= ndesc) return;  // warp-uniform
+    const int64_t r0 = gw * rpw - di * rows_pd;
     const CombineDesc &d = descs[di];
     const int32_t inf = c.inf;
     const TabAcc U = resolve(d.U, c);
     const int32_t w = d.w1 - 1;
-    const int32_t colhi = min(w, tab_kmax(U, i, inf) + *d.L.wstar);
-    const int32_t K = d.out_kmax[i];
-    int32_t *reach = d.out_reach + i * d.w1;
-    int32_t *trace = d.out_trace + i * d.w1;
-    int ns = 0;
-    if (lane == 0) {
+    const int32_t wstarL = *d.L.wstar;
+    // phase 1: lane = row
+    const int64_t i = r0 + lane;
+    const bool act = lane < rpw && i < n1 - 1 && (i % S) != 0;
+    int32_t K = -1, colhi = -1, kmax_warp = -1;
+    if (act) {
+        colhi = min(w, tab_kmax(U, i, inf) + wstarL);
+        K = d.out_kmax[i];
+        const int32_t *trace = d.out_trace + i * d.w1;
         int32_t left = 0, right = colhi, fm = -1;
+        int ns = 0;
         while (right >= left) {
             const int32_t mid = (left + right + 1) >> 1;
             if (mid <= K) {
                 fm = mid;
                 left = mid + 1;
             } else {
-                if (ns < FN_SEGS) seg[ns++] = make_int4(mid, right, fm, 0);
+                if (ns < FN_MAXSEG) seg_all[wid][lane][ns++] = make_int2(mid, fm);
                 right = mid - 1;
             }
         }
+        for (int s = 0; s < ns; ++s) {  // resolve tops (independent loads)
+            const int32_t f = seg_all[wid][lane][s].y;
+            seg_all[wid][lane][s].y = f >= 0 ? __ldg(trace + f) : 0;
+        }
+        nseg_all[wid][lane] = ns;
+        kmax_warp = K;
     }
-    ns = __shfl_sync(0xffffffffu, ns, 0);
+    kmax_warp = __reduce_max_sync(0xffffffffu, kmax_warp);
     __syncwarp();
-    for (int s = lane; s < ns; s += 32) {
-        const int32_t fm = seg[s].z;
-        seg[s].w = fm >= 0 ? trace[fm] : 0;
-    }
-    __syncwarp();
-    for (int32_t q = K + 1 + lane; q <= w; q += 32) {
-        int32_t tv = 0;
-        if (q <= colhi)
-            for (int s = 0; s < ns; ++s) {
-                const int4 sg = seg[s];
-                if (q >= sg.x && q <= sg.y) { tv = sg.w; break; }
+    // phase 2: fill the INF suffix of each row, coalesced
+    for (int rr = 0; rr < rpw; ++rr) {
+        const bool ract = __shfl_sync(0xffffffffu, act, rr);
+        if (!ract) continue;
+        const int32_t Kr = __shfl_sync(0xffffffffu, K, rr);
+        const int32_t ch = __shfl_sync(0xffffffffu, colhi, rr);
+        const int ns = nseg_all[wid][rr];
+        const int2 *sg = seg_all[wid][rr];
+        int32_t *reach = d.out_reach + (r0 + rr) * d.w1;
+        int32_t *trace = d.out_trace + (r0 + rr) * d.w1;
+        for (int32_t q = Kr + 1 + lane; q <= w; q += 32) {
+            int32_t tv = 0;
+            if (q <= ch) {
+                int s = 0;
+                while (s + 1 < ns && sg[s + 1].x > q) ++s;  // mids descend; segment s = [mid_s, prev-1]
+                while (s < ns && sg[s].x > q) ++s;
+                tv = s < ns ? sg[s].y : 0;
             }
-        reach[q] = inf;
-        trace[q] = tv;
+            reach[q] = inf;
+            trace[q] = tv;
+        }
     }
-    if (lane == 0) atomicMax(d.out_wstar, K);
+    if (lane == 0 && kmax_warp >= 0) atomicMax(d.out_wstar, kmax_warp);
 }
 
 int launch_block_refine(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
@@ -298,12 +320,14 @@ int launch_block_refine(const CombineDesc *descs, int32_t ndesc, Ctx c, int shif
 }
 
 int launch_finalize_rows(const CombineDesc *descs, int32_t ndesc, Ctx c, int32_t S,
-                         cudaStream_t s) {
+                         cudaStream_t s, int32_t maxw1) {
     if (ndesc <= 0) return 0;
     const int64_t n1 = (int64_t)c.n + 1;
-    const int64_t warps = n1 * ndesc;
+    const int rpw = maxw1 <= 512 ? 32 : (maxw1 <= 2048 ? 8 : (maxw1 <= 8192 ? 2 : 1));
+    const int64_t rows_pd = (n1 + rpw - 1) / rpw * rpw;
+    const int64_t warps = rows_pd / rpw * ndesc;
     const unsigned blocks = (unsigned)((warps + FN_WARPS - 1) / FN_WARPS);
-    finalize_rows_kernel<<<blocks, 32 * FN_WARPS, 0, s>>>(descs, ndesc, c, S);
+    finalize_rows_kernel<<<blocks, 32 * FN_WARPS, 0, s>>>(descs, ndesc, c, S, rpw);
     LCSG_LAUNCH_CHECK();
     return 0;
 }
