@@ -288,6 +288,8 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
         const bool kids_are_slabs =
             t->nodes[nd.upper].upper >= 0 && t->nodes[nd.lower].upper >= 0;
         nd.kind = (nd.w1 <= thread_max_w1 || !kids_are_slabs) ? 0 : 2;
+        // the refinement kernels use 32-bit element offsets into each table
+        if (nd.kind == 2 && n1 * (int64_t)nd.w1 >= ((int64_t)1 << 32)) nd.kind = 1;
         (void)wu1;
         if (skel_stride == 1 && nd.kind == 2) nd.kind = 1;
         nd.reach_off = tab_elems;
