@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(CR_THREADS)
     column_refine_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int shift,
                          int32_t S, int32_t nblk, int32_t w1max, int64_t spd) {
     extern __shared__ int32_t csm[];
-    int32_t *sR = csm + threadIdx.x;  // sR[r * CR_THREADS]
+    int32_t *sR = csm + threadIdx.x;                     // sR[r * CR_THREADS]
     int32_t *sT = csm + (S + 1) * CR_THREADS + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const int64_t gt = blockIdx.x * (int64_t)CR_THREADS + threadIdx.x;
@@ -87,34 +87,25 @@ __global__ void __launch_bounds__(CR_THREADS)
     const int64_t slot = gt - di * spd;
     const int32_t blk = (int32_t)(slot / w1max);
     const int32_t j = (int32_t)(slot - (int64_t)blk * w1max);
-    // descriptor fields in registers (stores below must not force reloads)
-    const int32_t *__restrict__ Ur = descs[di].U.reach;
-    const int32_t *__restrict__ Uk = descs[di].U.kmax;
-    const int32_t *__restrict__ Lr = descs[di].L.reach;
-    int32_t *const out_reach = descs[di].out_reach;
-    int32_t *const out_trace = descs[di].out_trace;
-    int32_t *const out_kmax = descs[di].out_kmax;
-    const int32_t uw1 = descs[di].U.w1, lw1 = descs[di].L.w1, wl = lw1 - 1;
-    const int32_t w1 = descs[di].w1;
+    const CombineDesc &d = descs[di];
     const int64_t n1 = (int64_t)c.n + 1;
     const int32_t inf = c.inf;
-    const bool active = blk < nblk && j < w1;
+    const bool active = blk < nblk && j < d.w1;
     const int64_t i0 = (int64_t)blk * S;
     const int32_t rb = active ? (int32_t)min((int64_t)S, n1 - 1 - i0) : 0;
-    // 32-bit element offsets from per-block bases (host guarantees every
-    // table has < 2^32 elements)
-    const int32_t *const Ublk = Ur + i0 * uw1;
-    const int32_t *const Kblk = Uk + i0;
-    int32_t *const Rblk = out_reach + i0 * w1 + j;
-    int32_t *const Tblk = out_trace + i0 * w1 + j;
+    const int32_t *__restrict__ Ur = d.U.reach;
+    const int32_t *__restrict__ Uk = d.U.kmax;
+    const int32_t *__restrict__ Lr = d.L.reach;
+    const int32_t uw1 = d.U.w1, lw1 = d.L.w1, wl = lw1 - 1;
+    const int32_t w1 = d.w1;
 
     {
         int32_t r0v = inf, r0t = 0, rbv = inf, rbt = 0;
         if (active && rb >= 2) {
-            r0v = __ldg(Rblk);
-            r0t = __ldg(Tblk);
-            rbv = __ldg(Rblk + (uint32_t)(rb * w1));
-            rbt = __ldg(Tblk + (uint32_t)(rb * w1));
+            r0v = __ldg(d.out_reach + i0 * w1 + j);
+            r0t = __ldg(d.out_trace + i0 * w1 + j);
+            rbv = __ldg(d.out_reach + (i0 + rb) * w1 + j);
+            rbt = __ldg(d.out_trace + (i0 + rb) * w1 + j);
         }
         sR[0] = r0v;
         sT[0] = r0t;
@@ -129,14 +120,15 @@ __global__ void __launch_bounds__(CR_THREADS)
         for (int r = dl; r < S; r += 2 * dl) {
             const int a = r - dl, b = r + dl;  // b <= S; rows >= rb mirror the bottom row
             const bool real = active && r < rb;
-            const int32_t *const Uc = Ublk + (uint32_t)(r * uw1);
-            const int32_t kmc = real ? __ldg(Kblk + r) : -1;
+            const int64_t ci = i0 + r;
+            const int32_t *Uc = Ur + ci * uw1;
+            const int32_t kmc = real ? __ldg(Uk + ci) : -1;
             const int32_t Ra = sR[a * CR_THREADS], Rb = sR[b * CR_THREADS];
             bool tail = false;
             int32_t kl = 0, outv = inf, outk = 0;
             if (real && Ra < inf) {
                 const int32_t Ta = sT[a * CR_THREADS];
-                const int32_t Xa = __ldg(Ublk + (uint32_t)(a * uw1 + Ta));
+                const int32_t Xa = __ldg(Ur + (i0 + a) * uw1 + Ta);
                 int32_t hi = min(Ta, kmc);
                 int32_t lo = min(max(0, Ta - dl), hi);
                 while (lo < hi) {  // first k with U[c,k] >= X(a,j)
@@ -146,7 +138,7 @@ __global__ void __launch_bounds__(CR_THREADS)
                 kl = max(lo, j - wl);
                 if (Rb < inf) {
                     const int32_t Tb = sT[b * CR_THREADS];
-                    const int32_t Xb = __ldg(Ublk + (uint32_t)(min(b, rb) * uw1 + Tb));
+                    const int32_t Xb = __ldg(Ur + min(i0 + b, i0 + rb) * uw1 + Tb);
                     lo = min(Tb, kmc);
                     hi = min(Tb + dl, kmc);
                     while (lo < hi) {  // last k with U[c,k] <= X(b,j)
@@ -161,7 +153,7 @@ __global__ void __launch_bounds__(CR_THREADS)
                     Key best = ~(Key)0;
                     for (int32_t k = kl; k <= kh; ++k) {
                         const int32_t x = __ldg(Uc + k);  // finite: k <= kmax_c
-                        const int32_t v = __ldg(Lr + (uint32_t)((x - 1) * lw1 + (j - k)));
+                        const int32_t v = __ldg(Lr + (int64_t)(x - 1) * lw1 + (j - k));
                         const Key key = tpack<Key>(v, k, shift);
                         best = key < best ? key : best;
                     }
@@ -184,12 +176,12 @@ __global__ void __launch_bounds__(CR_THREADS)
                 const int32_t tj = __shfl_sync(0xffffffffu, j, src);
                 const int32_t tkl = __shfl_sync(0xffffffffu, kl, src);
                 const int32_t tkh = min(tj, __shfl_sync(0xffffffffu, kmc, src));
-                const int32_t tblk = __shfl_sync(0xffffffffu, blk, src);
-                const int32_t *Ut = Ur + ((int64_t)tblk * S + r) * uw1;
+                const int64_t trow = __shfl_sync(0xffffffffu, ci, src);
+                const int32_t *Ut = Ur + trow * uw1;
                 Key best = ~(Key)0;
                 for (int32_t k = tkl + lane; k <= tkh; k += 32) {
                     int32_t v = inf;
-                    if (tj - k <= wl) v = __ldg(Lr + (uint32_t)((__ldg(Ut + k) - 1) * lw1 + (tj - k)));
+                    if (tj - k <= wl) v = __ldg(Lr + (int64_t)(__ldg(Ut + k) - 1) * lw1 + (tj - k));
                     const Key key = tpack<Key>(v, k, shift);
                     best = key < best ? key : best;
                 }
@@ -206,14 +198,16 @@ __global__ void __launch_bounds__(CR_THREADS)
     for (int r = 1; r < S; ++r) {
         const int32_t v = sR[r * CR_THREADS];
         const bool fin = active && r < rb && v < inf;
+        const int64_t row = i0 + r;
         if (fin) {
-            Rblk[(uint32_t)(r * w1)] = v;
-            Tblk[(uint32_t)(r * w1)] = sT[r * CR_THREADS];
+            const int64_t off = row * w1 + j;
+            d.out_reach[off] = v;
+            d.out_trace[off] = sT[r * CR_THREADS];
         }
         // frontier: finite here and the next lane's cell (same row) is not
         const bool nfin = __shfl_down_sync(0xffffffffu, fin, 1);
-        const int32_t nblk2 = __shfl_down_sync(0xffffffffu, blk, 1);
-        if (fin && (lane == 31 || !nfin || nblk2 != blk)) atomicMax(out_kmax + i0 + r, j);
+        const int64_t nrow = __shfl_down_sync(0xffffffffu, row, 1);
+        if (fin && (lane == 31 || !nfin || nrow != row)) atomicMax(d.out_kmax + row, j);
     }
 }
 
