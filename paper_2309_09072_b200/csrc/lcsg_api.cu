@@ -272,9 +272,10 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     const int skel_thread_max = env_int("LCSG_SKEL_THREAD_MAX_W1", 257);
     const int skel_warp_max = env_int("LCSG_SKEL_WARP_MAX_W1", 4097);
     // refinement mode: tiled (default) or one launch per pass ("LCSG_REFINE_PASSES=1")
-    const bool tiled = env_int("LCSG_REFINE_PASSES", 0) == 0 && skel_stride <= 64;
-    const int tile_j = std::max(32, env_int("LCSG_TILE_J", 128));
-    const int tile_wk = std::max(32, env_int("LCSG_TILE_WK", 256));
+    const bool tiled = env_int("LCSG_REFINE_PASSES", 0) == 0;
+    // block size (local rows) of each column-refinement stage, power of two
+    int col_block = 1;
+    while (col_block * 2 <= std::min(64, std::max(2, env_int("LCSG_COL_BLOCK", 16)))) col_block *= 2;
     size_t o_tab = off;
     int64_t tab_elems = 0;
     int32_t ncomb = 0;
@@ -409,14 +410,23 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             L.kind = maxw1 <= skel_thread_max ? 5 : (maxw1 <= skel_warp_max ? 6 : 3);
             L.stride_or_delta = S;
             t->plan.push_back(L);
-            if (tiled) {  // all passes in one tiled kernel + per-row finalize
-                LaunchH P = L;
-                P.kind = 7;
-                P.stride_or_delta = S;
-                P.ustride = maxw1;
-                t->plan.push_back(P);
-                P.kind = 8;
-                t->plan.push_back(P);
+            if (tiled) {  // column-refinement stages (row step S/B, S/B^2, .., 1) + finalize
+                int32_t rem = S;
+                while (rem > 1) {
+                    const int32_t B = std::min<int32_t>(col_block, rem);
+                    LaunchH P = L;
+                    P.kind = 7;
+                    P.stride_or_delta = B;
+                    P.wpr_log2 = rem / B;  // row step of this stage
+                    P.ustride = maxw1;
+                    t->plan.push_back(P);
+                    rem /= B;
+                }
+                LaunchH F = L;
+                F.kind = 8;
+                F.stride_or_delta = S;
+                F.ustride = maxw1;
+                t->plan.push_back(F);
                 continue;
             }
             for (int32_t dl = S / 2; dl >= 1; dl /= 2) {
@@ -516,8 +526,8 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             BCKL(launch_combine(L.kind == 5 ? 0 : 1, dd, L.count, c, L.shift, L.key64, s,
                                 L.stride_or_delta));
         else if (L.kind == 7)
-            BCKL(launch_block_refine(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, tile_j,
-                                     tile_wk, L.ustride, s));
+            BCKL(launch_block_refine(dd, L.count, c, L.shift, L.key64, L.stride_or_delta,
+                                     L.wpr_log2, L.ustride, s));
         else if (L.kind == 8)
             BCKL(launch_finalize_rows(dd, L.count, c, L.stride_or_delta, s, L.ustride));
         else if (refine_rows(n1, L.stride_or_delta) > 0)

@@ -100,9 +100,10 @@ int launch_skeleton(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, b
 int launch_refine(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
                   int32_t delta, cudaStream_t s);
 int refine_rows(int64_t n1, int32_t delta);
-// tiled refinement: all passes of row blocks of S in one launch (lcsg_tile.cu)
+// column refinement stage (lcsg_tile.cu): blocks of S local rows at row step
+// rs; rows at multiples of S*rs (and the last row) must already be known
 int launch_block_refine(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
-                        int32_t S, int32_t TJ, int32_t WK, int32_t maxw1, cudaStream_t s);
+                        int32_t S, int32_t rs, int32_t maxw1, cudaStream_t s);
 // INF suffix + kmax/wstar of the interior rows after the tiled refinement
 int launch_finalize_rows(const CombineDesc *descs, int32_t ndesc, Ctx c, int32_t S,
                          cudaStream_t s, int32_t maxw1);

@@ -76,9 +76,11 @@ constexpr int CR_THREADS = 256;
 template <typename Key>
 __global__ void __launch_bounds__(CR_THREADS)
     column_refine_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int shift,
-                         int32_t S, int32_t nblk, int32_t w1max, int64_t spd) {
+                         int32_t S, int32_t rs, int32_t nblk, int32_t w1max, int64_t spd) {
+    // local row r of block blk is the actual row i0 + r*rs (rs = row step of
+    // this refinement stage); rows 0 and S of the block are already known
     extern __shared__ int32_t csm[];
-    int32_t *sR = csm + threadIdx.x;                     // sR[r * CR_THREADS]
+    int32_t *sR = csm + threadIdx.x;  // sR[r * CR_THREADS]
     int32_t *sT = csm + (S + 1) * CR_THREADS + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const int64_t gt = blockIdx.x * (int64_t)CR_THREADS + threadIdx.x;
@@ -91,8 +93,11 @@ __global__ void __launch_bounds__(CR_THREADS)
     const int64_t n1 = (int64_t)c.n + 1;
     const int32_t inf = c.inf;
     const bool active = blk < nblk && j < d.w1;
-    const int64_t i0 = (int64_t)blk * S;
-    const int32_t rb = active ? (int32_t)min((int64_t)S, n1 - 1 - i0) : 0;
+    const int64_t i0 = (int64_t)blk * S * rs;
+    const int64_t span = n1 - 1 - i0;  // actual rows from i0 to the last row
+    // local rows r < rb are real; r >= rb mirror the bottom row
+    const int32_t rb = active ? (int32_t)min((int64_t)S, (span + rs - 1) / rs) : 0;
+    const int64_t ibot = rb == S ? i0 + (int64_t)S * rs : n1 - 1;
     const int32_t *__restrict__ Ur = d.U.reach;
     const int32_t *__restrict__ Uk = d.U.kmax;
     const int32_t *__restrict__ Lr = d.L.reach;
@@ -104,8 +109,8 @@ __global__ void __launch_bounds__(CR_THREADS)
         if (active && rb >= 2) {
             r0v = __ldg(d.out_reach + i0 * w1 + j);
             r0t = __ldg(d.out_trace + i0 * w1 + j);
-            rbv = __ldg(d.out_reach + (i0 + rb) * w1 + j);
-            rbt = __ldg(d.out_trace + (i0 + rb) * w1 + j);
+            rbv = __ldg(d.out_reach + ibot * w1 + j);
+            rbt = __ldg(d.out_trace + ibot * w1 + j);
         }
         sR[0] = r0v;
         sT[0] = r0t;
@@ -116,11 +121,14 @@ __global__ void __launch_bounds__(CR_THREADS)
     }
 #pragma unroll 1
     for (int dl = S >> 1; dl >= 1; dl >>= 1) {
+        const int32_t dist = dl * rs;  // actual row distance to both bounding rows
 #pragma unroll 1
         for (int r = dl; r < S; r += 2 * dl) {
             const int a = r - dl, b = r + dl;  // b <= S; rows >= rb mirror the bottom row
             const bool real = active && r < rb;
-            const int64_t ci = i0 + r;
+            const int64_t ci = i0 + (int64_t)r * rs;
+            const int64_t ai = i0 + (int64_t)a * rs;
+            const int64_t bi = b < rb ? i0 + (int64_t)b * rs : ibot;
             const int32_t *Uc = Ur + ci * uw1;
             const int32_t kmc = real ? __ldg(Uk + ci) : -1;
             const int32_t Ra = sR[a * CR_THREADS], Rb = sR[b * CR_THREADS];
@@ -128,9 +136,9 @@ __global__ void __launch_bounds__(CR_THREADS)
             int32_t kl = 0, outv = inf, outk = 0;
             if (real && Ra < inf) {
                 const int32_t Ta = sT[a * CR_THREADS];
-                const int32_t Xa = __ldg(Ur + (i0 + a) * uw1 + Ta);
+                const int32_t Xa = __ldg(Ur + ai * uw1 + Ta);
                 int32_t hi = min(Ta, kmc);
-                int32_t lo = min(max(0, Ta - dl), hi);
+                int32_t lo = min(max(0, Ta - dist), hi);
                 while (lo < hi) {  // first k with U[c,k] >= X(a,j)
                     const int32_t md = (lo + hi) >> 1;
                     if (__ldg(Uc + md) >= Xa) hi = md; else lo = md + 1;
@@ -138,9 +146,9 @@ __global__ void __launch_bounds__(CR_THREADS)
                 kl = max(lo, j - wl);
                 if (Rb < inf) {
                     const int32_t Tb = sT[b * CR_THREADS];
-                    const int32_t Xb = __ldg(Ur + min(i0 + b, i0 + rb) * uw1 + Tb);
+                    const int32_t Xb = __ldg(Ur + bi * uw1 + Tb);
                     lo = min(Tb, kmc);
-                    hi = min(Tb + dl, kmc);
+                    hi = min(Tb + dist, kmc);
                     while (lo < hi) {  // last k with U[c,k] <= X(b,j)
                         const int32_t md = (lo + hi + 1) >> 1;
                         if (__ldg(Uc + md) <= Xb) lo = md; else hi = md - 1;
@@ -193,16 +201,18 @@ __global__ void __launch_bounds__(CR_THREADS)
             }
         }
     }
-    // write the finite interior cells; report the finite frontier of each row
+    // write every interior cell's reach (INF included: later stages read these
+    // rows as bounds) and the finite cells' traces; report each row's frontier
 #pragma unroll 1
     for (int r = 1; r < S; ++r) {
         const int32_t v = sR[r * CR_THREADS];
-        const bool fin = active && r < rb && v < inf;
-        const int64_t row = i0 + r;
-        if (fin) {
+        const bool real = active && r < rb;
+        const bool fin = real && v < inf;
+        const int64_t row = i0 + (int64_t)r * rs;
+        if (real) {
             const int64_t off = row * w1 + j;
             d.out_reach[off] = v;
-            d.out_trace[off] = sT[r * CR_THREADS];
+            if (fin) d.out_trace[off] = sT[r * CR_THREADS];
         }
         // frontier: finite here and the next lane's cell (same row) is not
         const bool nfin = __shfl_down_sync(0xffffffffu, fin, 1);
@@ -274,7 +284,6 @@ __global__ void __launch_bounds__(32 * FN_WARPS)
         const int32_t ch = __shfl_sync(0xffffffffu, colhi, rr);
         const int ns = nseg_all[wid][rr];
         const int2 *sg = seg_all[wid][rr];
-        int32_t *reach = d.out_reach + (r0 + rr) * d.w1;
         int32_t *trace = d.out_trace + (r0 + rr) * d.w1;
         for (int32_t q = Kr + 1 + lane; q <= w; q += 32) {
             int32_t tv = 0;
@@ -284,21 +293,18 @@ __global__ void __launch_bounds__(32 * FN_WARPS)
                 while (s < ns && sg[s].x > q) ++s;
                 tv = s < ns ? sg[s].y : 0;
             }
-            reach[q] = inf;
-            trace[q] = tv;
+            trace[q] = tv;  // reach is already INF (column_refine_kernel)
         }
     }
     if (lane == 0 && kmax_warp >= 0) atomicMax(d.out_wstar, kmax_warp);
 }
 
 int launch_block_refine(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
-                        int32_t S, int32_t TJ, int32_t WK, int32_t maxw1, cudaStream_t s) {
-    (void)TJ;
-    (void)WK;
+                        int32_t S, int32_t rs, int32_t maxw1, cudaStream_t s) {
     if (ndesc <= 0) return 0;
-    if (S < 2 || S > 64) return (int)cudaErrorInvalidValue;
+    if (S < 2 || S > 64 || rs < 1) return (int)cudaErrorInvalidValue;
     const int64_t n1 = (int64_t)c.n + 1;
-    const int32_t nblk = (int32_t)((n1 - 1 + S - 1) / S);
+    const int32_t nblk = (int32_t)((n1 - 1 + (int64_t)S * rs - 1) / ((int64_t)S * rs));
     if (nblk <= 0) return 0;
     const int64_t spd = ((int64_t)nblk * maxw1 + 31) / 32 * 32;
     const unsigned blocks = (unsigned)((spd * ndesc + CR_THREADS - 1) / CR_THREADS);
@@ -311,10 +317,10 @@ int launch_block_refine(const CombineDesc *descs, int32_t ndesc, Ctx c, int shif
     }
     if (key64)
         column_refine_kernel<uint64_t><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift, S,
-                                                                       nblk, maxw1, spd);
+                                                                       rs, nblk, maxw1, spd);
     else
         column_refine_kernel<uint32_t><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift, S,
-                                                                       nblk, maxw1, spd);
+                                                                       rs, nblk, maxw1, spd);
     LCSG_LAUNCH_CHECK();
     return 0;
 }

@@ -290,8 +290,10 @@ def test_skeleton_refine_strides(stride, monkeypatch):
 
 
 @pytest.mark.parametrize("env", [
-    {"LCSG_TILE_J": "32", "LCSG_TILE_WK": "32"},           # many tiles, U window overflow
-    {"LCSG_TILE_J": "512", "LCSG_TILE_WK": "1024", "LCSG_SKELETON_STRIDE": "32"},
+    {"LCSG_SKELETON_STRIDE": "64", "LCSG_COL_BLOCK": "8"},   # two stages: step 8, step 1
+    {"LCSG_SKELETON_STRIDE": "32", "LCSG_COL_BLOCK": "4"},   # stages: step 8, 2, 1 (B=4,4,2)
+    {"LCSG_SKELETON_STRIDE": "8", "LCSG_COL_BLOCK": "2"},    # three stages of B=2
+    {"LCSG_SKELETON_STRIDE": "32", "LCSG_COL_BLOCK": "32"},  # one stage of 32 rows
     {"LCSG_REFINE_PASSES": "1"},                            # one launch per refinement pass
     {"LCSG_THREAD_MAX_W1": "3", "LCSG_SKEL_THREAD_MAX_W1": "3", "LCSG_SKEL_WARP_MAX_W1": "9"},
 ])
