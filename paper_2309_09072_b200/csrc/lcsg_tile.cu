@@ -97,7 +97,8 @@ __global__ void __launch_bounds__(CR_THREADS)
     const int64_t span = n1 - 1 - i0;  // actual rows from i0 to the last row
     // local rows r < rb are real; r >= rb mirror the bottom row
     const int32_t rb = active ? (int32_t)min((int64_t)S, (span + rs - 1) / rs) : 0;
-    const int64_t ibot = rb == S ? i0 + (int64_t)S * rs : n1 - 1;
+    // bottom bounding row: the next block boundary if it exists, else the last row
+    const int64_t ibot = span >= (int64_t)S * rs ? i0 + (int64_t)S * rs : n1 - 1;
     const int32_t *__restrict__ Ur = d.U.reach;
     const int32_t *__restrict__ Uk = d.U.kmax;
     const int32_t *__restrict__ Lr = d.L.reach;
