@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(32 * RF_WARPS)
         for (int q = 0; q < RF_NB; ++q) {
             const int32_t j = j0 + lane + 32 * q;
             if (j <= Kb) {
-                reach[j] = rval<Key>(best[q], shift);
+                reach[j] = best[q] == ~(Key)0 ? inf : rval<Key>(best[q], shift);
                 trace[j] = rk<Key>(best[q], shift);
             }
         }
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(32 * RF_WARPS)
             best = key < best ? key : best;
         }
         best = rwarp_min(best);
-        const int32_t bv = rval<Key>(best, shift);
+        const int32_t bv = best == ~(Key)0 ? inf : rval<Key>(best, shift);  // empty range: INF
         if (bv == inf) break;  // finite cells form a prefix
         if (lane == 0) {
             reach[j] = bv;

@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(CR_THREADS)
                         const Key key = tpack<Key>(v, k, shift);
                         best = key < best ? key : best;
                     }
-                    outv = tval<Key>(best, shift);
+                    outv = best == ~(Key)0 ? inf : tval<Key>(best, shift);
                     outk = tk<Key>(best, shift);
                 } else {
                     tail = true;
@@ -195,9 +195,9 @@ __global__ void __launch_bounds__(CR_THREADS)
                     best = key < best ? key : best;
                 }
                 best = twarp_min(best);
-                if (lane == src) {
-                    sR[r * CR_THREADS] = tval<Key>(best, shift);
-                    sT[r * CR_THREADS] = tk<Key>(best, shift);
+                if (lane == src) {  // an empty candidate range means INF
+                    sR[r * CR_THREADS] = best == ~(Key)0 ? inf : tval<Key>(best, shift);
+                    sT[r * CR_THREADS] = best == ~(Key)0 ? 0 : tk<Key>(best, shift);
                 }
             }
         }
