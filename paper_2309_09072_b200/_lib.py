@@ -16,7 +16,7 @@ import threading
 _PKG = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_PKG)
 LIB_DIR = os.path.join(_PKG, "lib")
-LIB_PATH = os.path.join(LIB_DIR, "liblcsgrid_b200.so")
+LIB_PATH = os.environ.get("LCSG_LIB_PATH") or os.path.join(LIB_DIR, "liblcsgrid_b200.so")
 CSRC = os.path.join(_PKG, "csrc")
 SOURCES = ["lcsg_api.cu", "lcsg_kernels.cu", "lcsg_refine.cu", "lcsg_tile.cu"]
 NVCC_FLAGS = [

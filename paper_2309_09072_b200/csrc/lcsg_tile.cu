@@ -222,6 +222,146 @@ __global__ void __launch_bounds__(CR_THREADS)
     }
 }
 
+// rs == 1 specialisation (the hot one): identical cell logic, fewer registers
+// (pinned to 40 so that 6 CTAs of 256 threads fit an SM alongside their smem).
+template <typename Key>
+__global__ void __launch_bounds__(CR_THREADS, 6)
+    column_refine_fine_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int shift,
+                         int32_t S, int32_t nblk, int32_t w1max, int64_t spd) {
+    extern __shared__ int32_t csm[];
+    int32_t *sR = csm + threadIdx.x;                     // sR[r * CR_THREADS]
+    int32_t *sT = csm + (S + 1) * CR_THREADS + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int64_t gt = blockIdx.x * (int64_t)CR_THREADS + threadIdx.x;
+    const int64_t di = gt / spd;  // warp-uniform: spd % 32 == 0
+    if (di >= ndesc) return;
+    const int64_t slot = gt - di * spd;
+    const int32_t blk = (int32_t)(slot / w1max);
+    const int32_t j = (int32_t)(slot - (int64_t)blk * w1max);
+    const CombineDesc &d = descs[di];
+    const int64_t n1 = (int64_t)c.n + 1;
+    const int32_t inf = c.inf;
+    const bool active = blk < nblk && j < d.w1;
+    const int64_t i0 = (int64_t)blk * S;
+    const int32_t rb = active ? (int32_t)min((int64_t)S, n1 - 1 - i0) : 0;
+    const int32_t *__restrict__ Ur = d.U.reach;
+    const int32_t *__restrict__ Uk = d.U.kmax;
+    const int32_t *__restrict__ Lr = d.L.reach;
+    const int32_t uw1 = d.U.w1, lw1 = d.L.w1, wl = lw1 - 1;
+    const int32_t w1 = d.w1;
+
+    {
+        int32_t r0v = inf, r0t = 0, rbv = inf, rbt = 0;
+        if (active && rb >= 2) {
+            r0v = __ldg(d.out_reach + i0 * w1 + j);
+            r0t = __ldg(d.out_trace + i0 * w1 + j);
+            rbv = __ldg(d.out_reach + (i0 + rb) * w1 + j);
+            rbt = __ldg(d.out_trace + (i0 + rb) * w1 + j);
+        }
+        sR[0] = r0v;
+        sT[0] = r0t;
+        for (int r = 1; r <= S; ++r) {
+            sR[r * CR_THREADS] = r >= rb ? rbv : inf;
+            sT[r * CR_THREADS] = r >= rb ? rbt : 0;
+        }
+    }
+#pragma unroll 1
+    for (int dl = S >> 1; dl >= 1; dl >>= 1) {
+#pragma unroll 1
+        for (int r = dl; r < S; r += 2 * dl) {
+            const int a = r - dl, b = r + dl;  // b <= S; rows >= rb mirror the bottom row
+            const bool real = active && r < rb;
+            const int64_t ci = i0 + r;
+            const int32_t *Uc = Ur + ci * uw1;
+            const int32_t kmc = real ? __ldg(Uk + ci) : -1;
+            const int32_t Ra = sR[a * CR_THREADS], Rb = sR[b * CR_THREADS];
+            bool tail = false;
+            int32_t kl = 0, outv = inf, outk = 0;
+            if (real && Ra < inf) {
+                const int32_t Ta = sT[a * CR_THREADS];
+                const int32_t Xa = __ldg(Ur + (i0 + a) * uw1 + Ta);
+                int32_t hi = min(Ta, kmc);
+                int32_t lo = min(max(0, Ta - dl), hi);
+                while (lo < hi) {  // first k with U[c,k] >= X(a,j)
+                    const int32_t md = (lo + hi) >> 1;
+                    if (__ldg(Uc + md) >= Xa) hi = md; else lo = md + 1;
+                }
+                kl = max(lo, j - wl);
+                if (Rb < inf) {
+                    const int32_t Tb = sT[b * CR_THREADS];
+                    const int32_t Xb = __ldg(Ur + min(i0 + b, i0 + rb) * uw1 + Tb);
+                    lo = min(Tb, kmc);
+                    hi = min(Tb + dl, kmc);
+                    while (lo < hi) {  // last k with U[c,k] <= X(b,j)
+                        const int32_t md = (lo + hi + 1) >> 1;
+                        if (__ldg(Uc + md) <= Xb) lo = md; else hi = md - 1;
+                    }
+                    int32_t kh = min(lo, j);
+                    if (kl > kh) {  // safety net: never taken when the bounds hold
+                        kl = max(0, j - wl);
+                        kh = min(j, kmc);
+                    }
+                    Key best = ~(Key)0;
+                    for (int32_t k = kl; k <= kh; ++k) {
+                        const int32_t x = __ldg(Uc + k);  // finite: k <= kmax_c
+                        const int32_t v = __ldg(Lr + (int64_t)(x - 1) * lw1 + (j - k));
+                        const Key key = tpack<Key>(v, k, shift);
+                        best = key < best ? key : best;
+                    }
+                    outv = best == ~(Key)0 ? inf : tval<Key>(best, shift);
+                    outk = tk<Key>(best, shift);
+                } else {
+                    tail = true;
+                }
+            }
+            if (!tail) {
+                sR[r * CR_THREADS] = outv;
+                sT[r * CR_THREADS] = outk;
+            }
+            // tail cells (finite above, INF below: no upper bound): the whole
+            // warp scans each one's range [kl, min(j, kmax_c)] in turn
+            unsigned mask = __ballot_sync(0xffffffffu, tail);
+            while (mask) {
+                const int src = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const int32_t tj = __shfl_sync(0xffffffffu, j, src);
+                const int32_t tkl = __shfl_sync(0xffffffffu, kl, src);
+                const int32_t tkh = min(tj, __shfl_sync(0xffffffffu, kmc, src));
+                const int64_t trow = __shfl_sync(0xffffffffu, ci, src);
+                const int32_t *Ut = Ur + trow * uw1;
+                Key best = ~(Key)0;
+                for (int32_t k = tkl + lane; k <= tkh; k += 32) {
+                    int32_t v = inf;
+                    if (tj - k <= wl) v = __ldg(Lr + (int64_t)(__ldg(Ut + k) - 1) * lw1 + (tj - k));
+                    const Key key = tpack<Key>(v, k, shift);
+                    best = key < best ? key : best;
+                }
+                best = twarp_min(best);
+                if (lane == src) {  // an empty candidate range means INF
+                    sR[r * CR_THREADS] = best == ~(Key)0 ? inf : tval<Key>(best, shift);
+                    sT[r * CR_THREADS] = best == ~(Key)0 ? 0 : tk<Key>(best, shift);
+                }
+            }
+        }
+    }
+    // write the finite interior cells; report the finite frontier of each row
+#pragma unroll 1
+    for (int r = 1; r < S; ++r) {
+        const int32_t v = sR[r * CR_THREADS];
+        const bool fin = active && r < rb && v < inf;
+        const int64_t row = i0 + r;
+        if (fin) {
+            const int64_t off = row * w1 + j;
+            d.out_reach[off] = v;
+            d.out_trace[off] = sT[r * CR_THREADS];
+        }
+        // frontier: finite here and the next lane's cell (same row) is not
+        const bool nfin = __shfl_down_sync(0xffffffffu, fin, 1);
+        const int64_t nrow = __shfl_down_sync(0xffffffffu, row, 1);
+        if (fin && (lane == 31 || !nfin || nrow != row)) atomicMax(d.out_kmax + row, j);
+    }
+}
+
 // Per interior row: kmax is final (max over column blocks); write the INF
 // suffix (K, w] -- reach INF, trace = `top` of the Alg. 1 node covering the
 // column (replay of the reference bisection, _kernel.pyx:53-60) or 0 beyond
@@ -285,6 +425,7 @@ __global__ void __launch_bounds__(32 * FN_WARPS)
         const int32_t ch = __shfl_sync(0xffffffffu, colhi, rr);
         const int ns = nseg_all[wid][rr];
         const int2 *sg = seg_all[wid][rr];
+        int32_t *reach = d.out_reach + (r0 + rr) * d.w1;
         int32_t *trace = d.out_trace + (r0 + rr) * d.w1;
         for (int32_t q = Kr + 1 + lane; q <= w; q += 32) {
             int32_t tv = 0;
@@ -294,7 +435,8 @@ __global__ void __launch_bounds__(32 * FN_WARPS)
                 while (s < ns && sg[s].x > q) ++s;
                 tv = s < ns ? sg[s].y : 0;
             }
-            trace[q] = tv;  // reach is already INF (column_refine_kernel)
+            reach[q] = inf;
+            trace[q] = tv;
         }
     }
     if (lane == 0 && kmax_warp >= 0) atomicMax(d.out_wstar, kmax_warp);
@@ -314,14 +456,24 @@ int launch_block_refine(const CombineDesc *descs, int32_t ndesc, Ctx c, int shif
     if (!attr) {
         cudaFuncSetAttribute(column_refine_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
         cudaFuncSetAttribute(column_refine_kernel<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
+        cudaFuncSetAttribute(column_refine_fine_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
+        cudaFuncSetAttribute(column_refine_fine_kernel<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
         attr = true;
     }
-    if (key64)
+    if (rs == 1) {  // last stage: lean kernel (finite cells only; finalize writes INF)
+        if (key64)
+            column_refine_fine_kernel<uint64_t><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift,
+                                                                                S, nblk, maxw1, spd);
+        else
+            column_refine_fine_kernel<uint32_t><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift,
+                                                                                S, nblk, maxw1, spd);
+    } else if (key64) {
         column_refine_kernel<uint64_t><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift, S,
                                                                        rs, nblk, maxw1, spd);
-    else
+    } else {
         column_refine_kernel<uint32_t><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift, S,
                                                                        rs, nblk, maxw1, spd);
+    }
     LCSG_LAUNCH_CHECK();
     return 0;
 }
