@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(CR_THREADS)
                         const Key key = tpack<Key>(v, k, shift);
                         best = key < best ? key : best;
                     }
-                    outv = best == ~(Key)0 ? inf : tval<Key>(best, shift);
+                    outv = tval<Key>(best, shift);  // (b,j) finite => non-empty range
                     outk = tk<Key>(best, shift);
                 } else {
                     tail = true;
@@ -222,10 +222,9 @@ __global__ void __launch_bounds__(CR_THREADS)
     }
 }
 
-// rs == 1 specialisation (the hot one): identical cell logic, fewer registers
-// (pinned to 40 so that 6 CTAs of 256 threads fit an SM alongside their smem).
+// rs == 1 specialisation (the hot one): identical cell logic, fewer registers.
 template <typename Key>
-__global__ void __launch_bounds__(CR_THREADS, 6)
+__global__ void __launch_bounds__(CR_THREADS)
     column_refine_fine_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int shift,
                          int32_t S, int32_t nblk, int32_t w1max, int64_t spd) {
     extern __shared__ int32_t csm[];
@@ -308,7 +307,7 @@ __global__ void __launch_bounds__(CR_THREADS, 6)
                         const Key key = tpack<Key>(v, k, shift);
                         best = key < best ? key : best;
                     }
-                    outv = best == ~(Key)0 ? inf : tval<Key>(best, shift);
+                    outv = tval<Key>(best, shift);  // (b,j) finite => non-empty range
                     outk = tk<Key>(best, shift);
                 } else {
                     tail = true;
@@ -329,6 +328,10 @@ __global__ void __launch_bounds__(CR_THREADS, 6)
                 const int32_t tkh = min(tj, __shfl_sync(0xffffffffu, kmc, src));
                 const int64_t trow = __shfl_sync(0xffffffffu, ci, src);
                 const int32_t *Ut = Ur + trow * uw1;
+                if (tkl > tkh) {  // empty candidate range (j beyond kmax_c + wl): INF
+                    if (lane == src) sR[r * CR_THREADS] = inf;
+                    continue;
+                }
                 Key best = ~(Key)0;
                 for (int32_t k = tkl + lane; k <= tkh; k += 32) {
                     int32_t v = inf;
@@ -337,9 +340,9 @@ __global__ void __launch_bounds__(CR_THREADS, 6)
                     best = key < best ? key : best;
                 }
                 best = twarp_min(best);
-                if (lane == src) {  // an empty candidate range means INF
-                    sR[r * CR_THREADS] = best == ~(Key)0 ? inf : tval<Key>(best, shift);
-                    sT[r * CR_THREADS] = best == ~(Key)0 ? 0 : tk<Key>(best, shift);
+                if (lane == src) {
+                    sR[r * CR_THREADS] = tval<Key>(best, shift);
+                    sT[r * CR_THREADS] = tk<Key>(best, shift);
                 }
             }
         }
