@@ -267,7 +267,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     size_t o_out = take((size_t)(1 + 2 * std::max<int64_t>(kmin, 1)) * 4);
     size_t o_sub = take((size_t)std::max<int64_t>(kmin, 1));
     // int32 tables of every combine node
-    const int skel_stride = std::max(1, env_int("LCSG_SKELETON_STRIDE", 16));
+    const int skel_stride = std::max(1, env_int("LCSG_SKELETON_STRIDE", 64));
     const int thread_max_w1 = env_int("LCSG_THREAD_MAX_W1", 65);
     const int skel_thread_max = env_int("LCSG_SKEL_THREAD_MAX_W1", 257);
     const int skel_warp_max = env_int("LCSG_SKEL_WARP_MAX_W1", 4097);
@@ -275,7 +275,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     const bool tiled = env_int("LCSG_REFINE_PASSES", 0) == 0;
     // block size (local rows) of each column-refinement stage, power of two
     int col_block = 1;
-    while (col_block * 2 <= std::min(64, std::max(2, env_int("LCSG_COL_BLOCK", 16)))) col_block *= 2;
+    while (col_block * 2 <= std::min(64, std::max(2, env_int("LCSG_COL_BLOCK", 8)))) col_block *= 2;
     size_t o_tab = off;
     int64_t tab_elems = 0;
     int32_t ncomb = 0;
