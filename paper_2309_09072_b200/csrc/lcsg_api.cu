@@ -268,7 +268,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     size_t o_sub = take((size_t)std::max<int64_t>(kmin, 1));
     // int32 tables of every combine node
     const int skel_stride = std::max(1, env_int("LCSG_SKELETON_STRIDE", 64));
-    const int thread_max_w1 = env_int("LCSG_THREAD_MAX_W1", 65);
+    const int thread_max_w1 = env_int("LCSG_THREAD_MAX_W1", 33);
     const int skel_thread_max = env_int("LCSG_SKEL_THREAD_MAX_W1", 257);
     const int skel_warp_max = env_int("LCSG_SKEL_WARP_MAX_W1", 4097);
     // refinement mode: tiled (default) or one launch per pass ("LCSG_REFINE_PASSES=1")

@@ -72,6 +72,7 @@ __device__ __forceinline__ int32_t tcell(const TabAcc &L, int32_t x, int32_t k, 
 // search window then over-covers, which keeps the bound valid.  U and L are
 // always materialised slabs here (never leaves), so plain row pointers are used.
 constexpr int CR_THREADS = 256;
+constexpr int FW = 8;  // fast-path window of U[c,.] entries per refined cell
 
 template <typename Key>
 __global__ void __launch_bounds__(CR_THREADS)
@@ -222,9 +223,11 @@ __global__ void __launch_bounds__(CR_THREADS)
     }
 }
 
-// rs == 1 specialisation (the hot one): identical cell logic, fewer registers.
+// rs == 1 specialisation (the hot one): the cell's whole candidate window of
+// U[c,.] is loaded at once (fast path) so a refined cell costs two dependent
+// global-load levels instead of one per binary-search step.
 template <typename Key>
-__global__ void __launch_bounds__(CR_THREADS)
+__global__ void __launch_bounds__(CR_THREADS, 4)
     column_refine_fine_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int shift,
                          int32_t S, int32_t nblk, int32_t w1max, int64_t spd) {
     extern __shared__ int32_t csm[];
@@ -279,37 +282,84 @@ __global__ void __launch_bounds__(CR_THREADS)
             if (real && Ra < inf) {
                 const int32_t Ta = sT[a * CR_THREADS];
                 const int32_t Xa = __ldg(Ur + (i0 + a) * uw1 + Ta);
-                int32_t hi = min(Ta, kmc);
-                int32_t lo = min(max(0, Ta - dl), hi);
-                while (lo < hi) {  // first k with U[c,k] >= X(a,j)
-                    const int32_t md = (lo + hi) >> 1;
-                    if (__ldg(Uc + md) >= Xa) hi = md; else lo = md + 1;
-                }
-                kl = max(lo, j - wl);
                 if (Rb < inf) {
                     const int32_t Tb = sT[b * CR_THREADS];
                     const int32_t Xb = __ldg(Ur + min(i0 + b, i0 + rb) * uw1 + Tb);
-                    lo = min(Tb, kmc);
-                    hi = min(Tb + dl, kmc);
-                    while (lo < hi) {  // last k with U[c,k] <= X(b,j)
-                        const int32_t md = (lo + hi + 1) >> 1;
-                        if (__ldg(Uc + md) <= Xb) lo = md; else hi = md - 1;
-                    }
-                    int32_t kh = min(lo, j);
-                    if (kl > kh) {  // safety net: never taken when the bounds hold
-                        kl = max(0, j - wl);
-                        kh = min(j, kmc);
-                    }
+                    // both bounds lie in the window [Ta - dl, Tb + dl] of U[c,.]
+                    const int32_t k0 = max(0, Ta - dl);
+                    const int32_t kend = min(Tb + dl, kmc);
                     Key best = ~(Key)0;
-                    for (int32_t k = kl; k <= kh; ++k) {
-                        const int32_t x = __ldg(Uc + k);  // finite: k <= kmax_c
-                        const int32_t v = __ldg(Lr + (int64_t)(x - 1) * lw1 + (j - k));
-                        const Key key = tpack<Key>(v, k, shift);
-                        best = key < best ? key : best;
+                    if (kend - k0 < FW) {
+                        // fast path: load the whole window at once, resolve both
+                        // bounds with register compares, issue the gathers together
+                        int32_t Uw[FW];
+#pragma unroll
+                        for (int t = 0; t < FW; ++t)
+                            Uw[t] = k0 + t <= kend ? __ldg(Uc + k0 + t) : 0x7fffffff;
+                        int32_t tlo = FW, thi = -1;
+#pragma unroll
+                        for (int t = FW - 1; t >= 0; --t)
+                            if (Uw[t] >= Xa) tlo = t;  // first k with U[c,k] >= X(a,j)
+#pragma unroll
+                        for (int t = 0; t < FW; ++t)
+                            if (k0 + t <= kend && Uw[t] <= Xb) thi = t;  // last k with U[c,k] <= X(b,j)
+                        kl = max(k0 + tlo, j - wl);
+                        const int32_t kh = min(k0 + thi, j);
+                        if (kl <= kh) {
+#pragma unroll
+                            for (int t = 0; t < FW; ++t) {
+                                const int32_t k = k0 + t;
+                                if (k >= kl && k <= kh) {
+                                    const int32_t v = __ldg(Lr + (int64_t)(Uw[t] - 1) * lw1 + (j - k));
+                                    const Key key = tpack<Key>(v, k, shift);
+                                    best = key < best ? key : best;
+                                }
+                            }
+                        } else {  // safety net: never taken when the bounds hold
+                            kl = max(0, j - wl);
+                            for (int32_t k = kl; k <= min(j, kmc); ++k) {
+                                const int32_t v = __ldg(Lr + (int64_t)(__ldg(Uc + k) - 1) * lw1 + (j - k));
+                                const Key key = tpack<Key>(v, k, shift);
+                                best = key < best ? key : best;
+                            }
+                        }
+                    } else {
+                        int32_t hi = min(Ta, kmc);
+                        int32_t lo = min(max(0, Ta - dl), hi);
+                        while (lo < hi) {  // first k with U[c,k] >= X(a,j)
+                            const int32_t md = (lo + hi) >> 1;
+                            if (__ldg(Uc + md) >= Xa) hi = md; else lo = md + 1;
+                        }
+                        kl = max(lo, j - wl);
+                        lo = min(Tb, kmc);
+                        hi = kend;
+                        while (lo < hi) {  // last k with U[c,k] <= X(b,j)
+                            const int32_t md = (lo + hi + 1) >> 1;
+                            if (__ldg(Uc + md) <= Xb) lo = md; else hi = md - 1;
+                        }
+                        int32_t kh = min(lo, j);
+                        if (kl > kh) {  // safety net: never taken when the bounds hold
+                            kl = max(0, j - wl);
+                            kh = min(j, kmc);
+                        }
+                        for (int32_t k = kl; k <= kh; ++k) {
+                            const int32_t x = __ldg(Uc + k);  // finite: k <= kmax_c
+                            const int32_t v = __ldg(Lr + (int64_t)(x - 1) * lw1 + (j - k));
+                            const Key key = tpack<Key>(v, k, shift);
+                            best = key < best ? key : best;
+                        }
                     }
                     outv = tval<Key>(best, shift);  // (b,j) finite => non-empty range
                     outk = tk<Key>(best, shift);
                 } else {
+                    // tail: lower bound only (scanned warp-cooperatively below)
+                    int32_t hi = min(Ta, kmc);
+                    int32_t lo = min(max(0, Ta - dl), hi);
+                    while (lo < hi) {  // first k with U[c,k] >= X(a,j)
+                        const int32_t md = (lo + hi) >> 1;
+                        if (__ldg(Uc + md) >= Xa) hi = md; else lo = md + 1;
+                    }
+                    kl = max(lo, j - wl);
                     tail = true;
                 }
             }
