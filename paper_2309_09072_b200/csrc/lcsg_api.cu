@@ -275,7 +275,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     const bool tiled = env_int("LCSG_REFINE_PASSES", 0) == 0;
     // block size (local rows) of each column-refinement stage, power of two
     int col_block = 1;
-    while (col_block * 2 <= std::min(64, std::max(2, env_int("LCSG_COL_BLOCK", 8)))) col_block *= 2;
+    while (col_block * 2 <= std::min(16, std::max(2, env_int("LCSG_COL_BLOCK", 8)))) col_block *= 2;
     size_t o_tab = off;
     int64_t tab_elems = 0;
     int32_t ncomb = 0;

@@ -86,6 +86,7 @@ __device__ __forceinline__ int32_t tcell(const TabAcc &L, int32_t x, int32_t k, 
 // materialised slabs here (never leaves), so plain row pointers are used.
 constexpr int CR_THREADS = 256;
 constexpr int FW = 8;  // batched window of U[c,.] entries in the general case
+constexpr int CR_QCAP = 32 * 8;  // queued cells per warp and pass: 32 lanes x S/2 (S <= 16)
 
 template <typename Key, bool kStaged>
 __global__ void __launch_bounds__(CR_THREADS, 4)
@@ -138,150 +139,192 @@ __global__ void __launch_bounds__(CR_THREADS, 4)
             sX[r * CR_THREADS] = r >= rb ? rbx : 0;
         }
     }
+    // per-warp queues of the cells that leave the cheap path (general and
+    // tail), so that they run with all lanes busy instead of diverging
+    __shared__ uint16_t s_gq[CR_THREADS / 32][CR_QCAP];
+    __shared__ uint16_t s_tq[CR_THREADS / 32][CR_QCAP];
+    const int wid = threadIdx.x >> 5;
+    const int warp_t0 = threadIdx.x & ~31;
+    // column / block of another lane of this warp (for queued cells)
+    auto lane_ctx = [&](int l, int32_t &jj, int64_t &ii0, int32_t &rbb) {
+        const int64_t sl = gt - lane + l - di * spd;
+        const int32_t bk = (int32_t)(sl / w1max);
+        jj = (int32_t)(sl - (int64_t)bk * w1max);
+        ii0 = (int64_t)bk * S * rs;
+        rbb = (int32_t)min((int64_t)S, (n1 - 1 - ii0 + rs - 1) / rs);
+    };
 #pragma unroll 1
     for (int dl = S >> 1; dl >= 1; dl >>= 1) {
         const int32_t dist = dl * rs;  // actual row distance to both bounding rows (upper bound)
+        int qn = 0, tn = 0;            // warp-uniform queue lengths
 #pragma unroll 1
         for (int r = dl; r < S; r += 2 * dl) {
             const int a = r - dl, b = r + dl;  // b <= S; rows >= rb mirror the bottom row
             const bool real = active && r < rb;
-            const int64_t ci = i0 + (int64_t)r * rs;
-            const int32_t *Uc = Ur + ci * uw1;
-            const int32_t kmc = real ? __ldg(Uk + ci) : -1;
             const int32_t Ra = sR[a * CR_THREADS], Rb = sR[b * CR_THREADS];
-            bool tail = false;
-            int32_t kl = 0, outv = inf, outk = 0, outx = 0;
-            if (real && Ra < inf) {
-                const int32_t Ta = sT[a * CR_THREADS], Xa = sX[a * CR_THREADS];
-                if (Rb < inf) {
-                    const int32_t Tb = sT[b * CR_THREADS], Xb = sX[b * CR_THREADS];
-                    bool done = false;
-                    if (Xa == Xb) {  // pinned crossing column
-                        const int32_t lo = max(Ta - dist, Tb), hi = min(min(Ta, Tb + dist), kmc);
-                        int32_t k = lo;
-                        if (lo < hi)
-                            while (k < hi && __ldg(Uc + k) != Xa) ++k;
-                        if (k <= hi && (lo == hi || __ldg(Uc + k) == Xa)) {
-                            outk = k;
-                            outx = Xa;
-                            outv = k == Ta ? Ra
-                                 : (k == Tb ? Rb
-                                            : __ldg(Lr + (int64_t)(Xa - 1) * lw1 + (j - k)));
-                            done = true;
-                        }
-                    }
-                    if (!done) {
-                        const int32_t k0 = max(0, Ta - dist);
-                        const int32_t kend = min(Tb + dist, kmc);
-                        Key best = ~(Key)0;
-                        int32_t kh = -1;
-                        if (kend - k0 < FW) {
-                            // window path: load [k0, kend] at once, resolve both bounds
-                            // with register compares, issue the gathers together
-                            int32_t Uw[FW];
-#pragma unroll
-                            for (int t = 0; t < FW; ++t)
-                                Uw[t] = k0 + t <= kend ? __ldg(Uc + k0 + t) : 0x7fffffff;
-                            int32_t tlo = FW, thi = -1;
-#pragma unroll
-                            for (int t = FW - 1; t >= 0; --t)
-                                if (Uw[t] >= Xa) tlo = t;  // first k with U[c,k] >= X(a,j)
-#pragma unroll
-                            for (int t = 0; t < FW; ++t)
-                                if (k0 + t <= kend && Uw[t] <= Xb) thi = t;  // last k with U[c,k] <= X(b,j)
-                            kl = max(k0 + tlo, j - wl);
-                            kh = min(k0 + thi, j);
-                            if (kl <= kh) {
-#pragma unroll
-                                for (int t = 0; t < FW; ++t) {
-                                    const int32_t k = k0 + t;
-                                    if (k >= kl && k <= kh) {
-                                        const int32_t v = __ldg(Lr + (int64_t)(Uw[t] - 1) * lw1 + (j - k));
-                                        const Key key = tpack<Key>(v, k, shift);
-                                        best = key < best ? key : best;
-                                    }
-                                }
-                            }
-                        } else {
-                            int32_t hi = min(Ta, kmc);
-                            int32_t lo = min(k0, hi);
-                            while (lo < hi) {  // first k with U[c,k] >= X(a,j)
-                                const int32_t md = (lo + hi) >> 1;
-                                if (__ldg(Uc + md) >= Xa) hi = md; else lo = md + 1;
-                            }
-                            kl = max(lo, j - wl);
-                            lo = min(Tb, kmc);
-                            hi = kend;
-                            while (lo < hi) {  // last k with U[c,k] <= X(b,j)
-                                const int32_t md = (lo + hi + 1) >> 1;
-                                if (__ldg(Uc + md) <= Xb) lo = md; else hi = md - 1;
-                            }
-                            kh = min(lo, j);
-                            for (int32_t k = kl; k <= kh; ++k) {
-                                const int32_t v = __ldg(Lr + (int64_t)(__ldg(Uc + k) - 1) * lw1 + (j - k));
-                                const Key key = tpack<Key>(v, k, shift);
-                                best = key < best ? key : best;
-                            }
-                        }
-                        if (kl > kh) {  // safety net: never taken when the bounds hold
-                            for (int32_t k = max(0, j - wl); k <= min(j, kmc); ++k) {
-                                const int32_t v = __ldg(Lr + (int64_t)(__ldg(Uc + k) - 1) * lw1 + (j - k));
-                                const Key key = tpack<Key>(v, k, shift);
-                                best = key < best ? key : best;
-                            }
-                        }
-                        outv = tval<Key>(best, shift);  // (b,j) finite => non-empty range
-                        outk = tk<Key>(best, shift);
-                        outx = __ldg(Uc + outk);
-                    }
+            int kind = 0;  // 0 done, 1 general, 2 tail
+            if (real) {
+                if (Ra >= inf) {
+                    sR[r * CR_THREADS] = inf;
+                } else if (Rb >= inf) {
+                    kind = 2;
                 } else {
-                    // tail: lower bound only (scanned warp-cooperatively below)
-                    int32_t hi = min(Ta, kmc);
-                    int32_t lo = min(max(0, Ta - dist), hi);
-                    while (lo < hi) {  // first k with U[c,k] >= X(a,j)
-                        const int32_t md = (lo + hi) >> 1;
-                        if (__ldg(Uc + md) >= Xa) hi = md; else lo = md + 1;
+                    const int32_t Ta = sT[a * CR_THREADS], Xa = sX[a * CR_THREADS];
+                    const int32_t Tb = sT[b * CR_THREADS], Xb = sX[b * CR_THREADS];
+                    kind = 1;
+                    if (Xa == Xb) {  // pinned crossing column: k* = index of X in U[c,.]
+                        const int32_t lo = max(Ta - dist, Tb), hi = min(Ta, Tb + dist);
+                        const int32_t *Uc = Ur + (i0 + (int64_t)r * rs) * uw1;
+                        int32_t k = lo;
+                        bool ok = lo == hi;
+                        for (; !ok && k <= hi; ++k)
+                            if (__ldg(Uc + k) == Xa) { ok = true; break; }
+                        if (ok) {
+                            sR[r * CR_THREADS] = k == Ta ? Ra
+                                               : (k == Tb ? Rb
+                                                          : __ldg(Lr + (int64_t)(Xa - 1) * lw1 + (j - k)));
+                            sT[r * CR_THREADS] = k;
+                            sX[r * CR_THREADS] = Xa;
+                            kind = 0;
+                        }
                     }
-                    kl = max(lo, j - wl);
-                    tail = true;
                 }
             }
-            if (!tail) {
-                sR[r * CR_THREADS] = outv;
-                sT[r * CR_THREADS] = outk;
-                sX[r * CR_THREADS] = outx;
-            }
-            // tail cells (finite above, INF below: no upper bound): the whole
-            // warp scans each one's range [kl, min(j, kmax_c)] in turn
-            unsigned mask = __ballot_sync(0xffffffffu, tail);
-            while (mask) {
-                const int src = __ffs(mask) - 1;
-                mask &= mask - 1;
-                const int32_t tj = __shfl_sync(0xffffffffu, j, src);
-                const int32_t tkl = __shfl_sync(0xffffffffu, kl, src);
-                const int32_t tkh = min(tj, __shfl_sync(0xffffffffu, kmc, src));
-                const int64_t trow = __shfl_sync(0xffffffffu, ci, src);
-                const int32_t *Ut = Ur + trow * uw1;
-                if (tkl > tkh) {  // empty candidate range (j beyond kmax_c + wl): INF
-                    if (lane == src) sR[r * CR_THREADS] = inf;
-                    continue;
+            const unsigned gm = __ballot_sync(0xffffffffu, kind == 1);
+            const unsigned tm = __ballot_sync(0xffffffffu, kind == 2);
+            const unsigned lt = (1u << lane) - 1;
+            if (kind == 1 && qn + __popc(gm & lt) < CR_QCAP)
+                s_gq[wid][qn + __popc(gm & lt)] = (uint16_t)((lane << 8) | r);
+            if (kind == 2 && tn + __popc(tm & lt) < CR_QCAP)
+                s_tq[wid][tn + __popc(tm & lt)] = (uint16_t)((lane << 8) | r);
+            qn += __popc(gm);
+            tn += __popc(tm);
+        }
+        qn = min(qn, CR_QCAP);
+        tn = min(tn, CR_QCAP);
+        __syncwarp();
+        // ---- general cells: first-wins minimum over the bounded k-range ----
+        for (int q = lane; q < qn; q += 32) {
+            const int e = s_gq[wid][q];
+            const int l = e >> 8, r = e & 0xff;
+            int32_t jj, rbb;
+            int64_t ii0;
+            lane_ctx(l, jj, ii0, rbb);
+            int32_t *gR = csm + warp_t0 + l, *gT = gR + (S + 1) * CR_THREADS, *gX = gT + (S + 1) * CR_THREADS;
+            const int a = r - dl, b = r + dl;
+            const int64_t ci = ii0 + (int64_t)r * rs;
+            const int32_t *Uc = Ur + ci * uw1;
+            const int32_t kmc = __ldg(Uk + ci);
+            const int32_t Ta = gT[a * CR_THREADS], Xa = gX[a * CR_THREADS];
+            const int32_t Tb = gT[b * CR_THREADS], Xb = gX[b * CR_THREADS];
+            const int32_t k0 = max(0, Ta - dist);
+            const int32_t kend = min(Tb + dist, kmc);
+            Key best = ~(Key)0;
+            int32_t kl, kh;
+            if (kend - k0 < FW) {
+                // window path: load [k0, kend] at once, resolve both bounds with
+                // register compares, issue the gathers together
+                int32_t Uw[FW];
+#pragma unroll
+                for (int t = 0; t < FW; ++t)
+                    Uw[t] = k0 + t <= kend ? __ldg(Uc + k0 + t) : 0x7fffffff;
+                int32_t tlo = FW, thi = -1;
+#pragma unroll
+                for (int t = FW - 1; t >= 0; --t)
+                    if (Uw[t] >= Xa) tlo = t;  // first k with U[c,k] >= X(a,j)
+#pragma unroll
+                for (int t = 0; t < FW; ++t)
+                    if (k0 + t <= kend && Uw[t] <= Xb) thi = t;  // last k with U[c,k] <= X(b,j)
+                kl = max(k0 + tlo, jj - wl);
+                kh = min(k0 + thi, jj);
+                if (kl <= kh) {
+#pragma unroll
+                    for (int t = 0; t < FW; ++t) {
+                        const int32_t k = k0 + t;
+                        if (k >= kl && k <= kh) {
+                            const int32_t v = __ldg(Lr + (int64_t)(Uw[t] - 1) * lw1 + (jj - k));
+                            const Key key = tpack<Key>(v, k, shift);
+                            best = key < best ? key : best;
+                        }
+                    }
                 }
+            } else {
+                int32_t hi = min(Ta, kmc);
+                int32_t lo = min(k0, hi);
+                while (lo < hi) {  // first k with U[c,k] >= X(a,j)
+                    const int32_t md = (lo + hi) >> 1;
+                    if (__ldg(Uc + md) >= Xa) hi = md; else lo = md + 1;
+                }
+                kl = max(lo, jj - wl);
+                lo = min(Tb, kmc);
+                hi = kend;
+                while (lo < hi) {  // last k with U[c,k] <= X(b,j)
+                    const int32_t md = (lo + hi + 1) >> 1;
+                    if (__ldg(Uc + md) <= Xb) lo = md; else hi = md - 1;
+                }
+                kh = min(lo, jj);
+                for (int32_t k = kl; k <= kh; ++k) {
+                    const int32_t v = __ldg(Lr + (int64_t)(__ldg(Uc + k) - 1) * lw1 + (jj - k));
+                    const Key key = tpack<Key>(v, k, shift);
+                    best = key < best ? key : best;
+                }
+            }
+            if (kl > kh) {  // safety net: never taken when the bounds hold
+                for (int32_t k = max(0, jj - wl); k <= min(jj, kmc); ++k) {
+                    const int32_t v = __ldg(Lr + (int64_t)(__ldg(Uc + k) - 1) * lw1 + (jj - k));
+                    const Key key = tpack<Key>(v, k, shift);
+                    best = key < best ? key : best;
+                }
+            }
+            const int32_t bk = tk<Key>(best, shift);  // (b,j) finite => non-empty range
+            gR[r * CR_THREADS] = tval<Key>(best, shift);
+            gT[r * CR_THREADS] = bk;
+            gX[r * CR_THREADS] = __ldg(Uc + bk);
+        }
+        __syncwarp();
+        // ---- tail cells (finite above, INF below: no upper bound): the whole
+        // warp scans each one's range [lower bound, min(j, kmax_c)] in turn
+        for (int q = 0; q < tn; ++q) {
+            const int e = s_tq[wid][q];
+            const int l = e >> 8, r = e & 0xff;
+            int32_t jj, rbb;
+            int64_t ii0;
+            lane_ctx(l, jj, ii0, rbb);
+            int32_t *gR = csm + warp_t0 + l, *gT = gR + (S + 1) * CR_THREADS, *gX = gT + (S + 1) * CR_THREADS;
+            const int a = r - dl;
+            const int64_t ci = ii0 + (int64_t)r * rs;
+            const int32_t *Uc = Ur + ci * uw1;
+            const int32_t kmc = __ldg(Uk + ci);
+            const int32_t Ta = gT[a * CR_THREADS], Xa = gX[a * CR_THREADS];
+            int32_t hi = min(Ta, kmc);
+            int32_t lo = min(max(0, Ta - dist), hi);
+            while (lo < hi) {  // first k with U[c,k] >= X(a,j)
+                const int32_t md = (lo + hi) >> 1;
+                if (__ldg(Uc + md) >= Xa) hi = md; else lo = md + 1;
+            }
+            const int32_t tkl = max(lo, jj - wl), tkh = min(jj, kmc);
+            int32_t outv = inf, outk = 0, outx = 0;
+            if (tkl <= tkh) {
                 Key best = ~(Key)0;
                 for (int32_t k = tkl + lane; k <= tkh; k += 32) {
                     int32_t v = inf;
-                    if (tj - k <= wl) v = __ldg(Lr + (int64_t)(__ldg(Ut + k) - 1) * lw1 + (tj - k));
+                    if (jj - k <= wl) v = __ldg(Lr + (int64_t)(__ldg(Uc + k) - 1) * lw1 + (jj - k));
                     const Key key = tpack<Key>(v, k, shift);
                     best = key < best ? key : best;
                 }
                 best = twarp_min(best);
-                if (lane == src) {
-                    const int32_t bk = tk<Key>(best, shift);
-                    sR[r * CR_THREADS] = tval<Key>(best, shift);
-                    sT[r * CR_THREADS] = bk;
-                    sX[r * CR_THREADS] = __ldg(Ut + bk);
-                }
+                outv = tval<Key>(best, shift);
+                outk = tk<Key>(best, shift);
+                if (outv < inf) outx = __ldg(Uc + outk);
             }
+            if (lane == 0) {
+                gR[r * CR_THREADS] = outv;
+                gT[r * CR_THREADS] = outk;
+                gX[r * CR_THREADS] = outx;
+            }
+            __syncwarp();
         }
+        __syncwarp();
     }
     // write the interior cells (staged: reach of INF cells too, since later
     // stages read these rows as bounds) and report each row's finite frontier
@@ -386,7 +429,7 @@ __global__ void __launch_bounds__(32 * FN_WARPS)
 int launch_block_refine(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
                         int32_t S, int32_t rs, int32_t maxw1, cudaStream_t s) {
     if (ndesc <= 0) return 0;
-    if (S < 2 || S > 64 || rs < 1) return (int)cudaErrorInvalidValue;
+    if (S < 2 || S > 16 || rs < 1) return (int)cudaErrorInvalidValue;  // queue capacity
     const int64_t n1 = (int64_t)c.n + 1;
     const int32_t nblk = (int32_t)((n1 - 1 + (int64_t)S * rs - 1) / ((int64_t)S * rs));
     if (nblk <= 0) return 0;
