@@ -59,44 +59,29 @@ __device__ __forceinline__ int32_t tcell(const TabAcc &L, int32_t x, int32_t k, 
     return tab_get(L, (int64_t)x - 1, j - k);
 }
 
-// One lane = one column j of one row block: local rows 0 and S of the block
-// (actual rows i0 and i0 + S*rs, or the last row) are already known; the S-1
-// interior rows (actual i0 + r*rs) are derived in divide-and-conquer order
-// (delta = S/2 ... 1).  The column's (reach, trace, crossing column X) values
-// live in a per-thread slice of shared memory (no cross-thread sharing, no
-// barriers); the cell body is a single non-unrolled copy (a fully unrolled
-// variant thrashed the instruction cache: 76% `no_instructions` stalls).
-//
-// Per cell c with bounding rows a < c < b (distance dist = delta*rs):
-//   * (a,j) INF               -> (c,j) INF
-//   * X(a,j) == X(b,j) = X    -> X(c,j) = X (sandwich), so the first-wins k* is
-//     the index of X in U[c,.], which lies in [Ta-dist, Ta] n [Tb, Tb+dist]
-//     (interleave); if k* equals Ta or Tb the reach value is the neighbour's
-//     (same L cell), else one gather.  This "pinned" case covers 70-86% of
-//     the cells on random 26-letter inputs.
-//   * otherwise               -> first-wins minimum over k in
-//     [first k: U[c,k] >= X(a,j), last k: U[c,k] <= X(b,j)]; the window of
-//     U[c,.] is loaded in one batch when it has <= FW entries.
-//   * (b,j) INF (tail)        -> no upper bound: the warp scans
-//     [lower bound, min(j, kmax_c)] cooperatively.
-// Neighbouring lanes hold neighbouring columns, so U and L reads of a warp hit
-// few lines and the final writes are coalesced.  A short last block treats
-// the local rows beyond the table as copies of its bottom row; the interleave
-// windows then over-cover, which keeps every bound valid.  U and L are always
-// materialised slabs here (never leaves), so plain row pointers are used.
+// One lane = one column j of one row block [i0, i0+S]: the block's two
+// skeleton cells of column j are loaded, then the S-1 interior cells are
+// derived in divide-and-conquer order (delta = S/2 ... 1).  The column's
+// (reach, trace) values live in a per-thread slice of shared memory (no
+// cross-thread sharing, no barriers); the cell body is a single, non-unrolled
+// copy of code (a fully unrolled variant thrashed the instruction cache: 76%
+// of stall samples were `no_instructions`).  Neighbouring lanes hold
+// neighbouring columns, so U and L reads of a warp hit few lines and the
+// final writes are coalesced.  A short last block (rb < S rows) treats the
+// local rows >= rb as copies of its bottom skeleton row; the interleave
+// search window then over-covers, which keeps the bound valid.  U and L are
+// always materialised slabs here (never leaves), so plain row pointers are used.
 constexpr int CR_THREADS = 256;
-constexpr int FW = 8;  // batched window of U[c,.] entries in the general case
-constexpr int CR_QCAP = 32 * 8;  // queued cells per warp and pass: 32 lanes x S/2 (S <= 16)
 
-template <typename Key, bool kStaged>
-__global__ void __launch_bounds__(CR_THREADS, 4)
+template <typename Key>
+__global__ void __launch_bounds__(CR_THREADS)
     column_refine_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int shift,
-                         int32_t S, int32_t rs_arg, int32_t nblk, int32_t w1max, int64_t spd) {
-    const int32_t rs = kStaged ? rs_arg : 1;
+                         int32_t S, int32_t rs, int32_t nblk, int32_t w1max, int64_t spd) {
+    // local row r of block blk is the actual row i0 + r*rs (rs = row step of
+    // this refinement stage); rows 0 and S of the block are already known
     extern __shared__ int32_t csm[];
     int32_t *sR = csm + threadIdx.x;  // sR[r * CR_THREADS]
     int32_t *sT = csm + (S + 1) * CR_THREADS + threadIdx.x;
-    int32_t *sX = csm + 2 * (S + 1) * CR_THREADS + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const int64_t gt = blockIdx.x * (int64_t)CR_THREADS + threadIdx.x;
     const int64_t di = gt / spd;  // warp-uniform: spd % 32 == 0
@@ -121,223 +106,257 @@ __global__ void __launch_bounds__(CR_THREADS, 4)
     const int32_t w1 = d.w1;
 
     {
-        int32_t r0v = inf, r0t = 0, r0x = 0, rbv = inf, rbt = 0, rbx = 0;
+        int32_t r0v = inf, r0t = 0, rbv = inf, rbt = 0;
         if (active && rb >= 2) {
             r0v = __ldg(d.out_reach + i0 * w1 + j);
             r0t = __ldg(d.out_trace + i0 * w1 + j);
             rbv = __ldg(d.out_reach + ibot * w1 + j);
             rbt = __ldg(d.out_trace + ibot * w1 + j);
-            if (r0v < inf) r0x = __ldg(Ur + i0 * uw1 + r0t);
-            if (rbv < inf) rbx = __ldg(Ur + ibot * uw1 + rbt);
         }
         sR[0] = r0v;
         sT[0] = r0t;
-        sX[0] = r0x;
         for (int r = 1; r <= S; ++r) {
             sR[r * CR_THREADS] = r >= rb ? rbv : inf;
             sT[r * CR_THREADS] = r >= rb ? rbt : 0;
-            sX[r * CR_THREADS] = r >= rb ? rbx : 0;
         }
     }
-    // per-warp queues of the cells that leave the cheap path (general and
-    // tail), so that they run with all lanes busy instead of diverging
-    __shared__ uint16_t s_gq[CR_THREADS / 32][CR_QCAP];
-    __shared__ uint16_t s_tq[CR_THREADS / 32][CR_QCAP];
-    const int wid = threadIdx.x >> 5;
-    const int warp_t0 = threadIdx.x & ~31;
-    // column / block of another lane of this warp (for queued cells)
-    auto lane_ctx = [&](int l, int32_t &jj, int64_t &ii0, int32_t &rbb) {
-        const int64_t sl = gt - lane + l - di * spd;
-        const int32_t bk = (int32_t)(sl / w1max);
-        jj = (int32_t)(sl - (int64_t)bk * w1max);
-        ii0 = (int64_t)bk * S * rs;
-        rbb = (int32_t)min((int64_t)S, (n1 - 1 - ii0 + rs - 1) / rs);
-    };
 #pragma unroll 1
     for (int dl = S >> 1; dl >= 1; dl >>= 1) {
-        const int32_t dist = dl * rs;  // actual row distance to both bounding rows (upper bound)
-        int qn = 0, tn = 0;            // warp-uniform queue lengths
+        const int32_t dist = dl * rs;  // actual row distance to both bounding rows
 #pragma unroll 1
         for (int r = dl; r < S; r += 2 * dl) {
             const int a = r - dl, b = r + dl;  // b <= S; rows >= rb mirror the bottom row
             const bool real = active && r < rb;
-            const int32_t Ra = sR[a * CR_THREADS], Rb = sR[b * CR_THREADS];
-            int kind = 0;  // 0 done, 1 general, 2 tail
-            if (real) {
-                if (Ra >= inf) {
-                    sR[r * CR_THREADS] = inf;
-                } else if (Rb >= inf) {
-                    kind = 2;
-                } else {
-                    const int32_t Ta = sT[a * CR_THREADS], Xa = sX[a * CR_THREADS];
-                    const int32_t Tb = sT[b * CR_THREADS], Xb = sX[b * CR_THREADS];
-                    kind = 1;
-                    if (Xa == Xb) {  // pinned crossing column: k* = index of X in U[c,.]
-                        const int32_t lo = max(Ta - dist, Tb), hi = min(Ta, Tb + dist);
-                        const int32_t *Uc = Ur + (i0 + (int64_t)r * rs) * uw1;
-                        int32_t k = lo;
-                        bool ok = lo == hi;
-                        for (; !ok && k <= hi; ++k)
-                            if (__ldg(Uc + k) == Xa) { ok = true; break; }
-                        if (ok) {
-                            sR[r * CR_THREADS] = k == Ta ? Ra
-                                               : (k == Tb ? Rb
-                                                          : __ldg(Lr + (int64_t)(Xa - 1) * lw1 + (j - k)));
-                            sT[r * CR_THREADS] = k;
-                            sX[r * CR_THREADS] = Xa;
-                            kind = 0;
-                        }
-                    }
-                }
-            }
-            const unsigned gm = __ballot_sync(0xffffffffu, kind == 1);
-            const unsigned tm = __ballot_sync(0xffffffffu, kind == 2);
-            const unsigned lt = (1u << lane) - 1;
-            if (kind == 1 && qn + __popc(gm & lt) < CR_QCAP)
-                s_gq[wid][qn + __popc(gm & lt)] = (uint16_t)((lane << 8) | r);
-            if (kind == 2 && tn + __popc(tm & lt) < CR_QCAP)
-                s_tq[wid][tn + __popc(tm & lt)] = (uint16_t)((lane << 8) | r);
-            qn += __popc(gm);
-            tn += __popc(tm);
-        }
-        qn = min(qn, CR_QCAP);
-        tn = min(tn, CR_QCAP);
-        __syncwarp();
-        // ---- general cells: first-wins minimum over the bounded k-range ----
-        for (int q = lane; q < qn; q += 32) {
-            const int e = s_gq[wid][q];
-            const int l = e >> 8, r = e & 0xff;
-            int32_t jj, rbb;
-            int64_t ii0;
-            lane_ctx(l, jj, ii0, rbb);
-            int32_t *gR = csm + warp_t0 + l, *gT = gR + (S + 1) * CR_THREADS, *gX = gT + (S + 1) * CR_THREADS;
-            const int a = r - dl, b = r + dl;
-            const int64_t ci = ii0 + (int64_t)r * rs;
+            const int64_t ci = i0 + (int64_t)r * rs;
+            const int64_t ai = i0 + (int64_t)a * rs;
+            const int64_t bi = b < rb ? i0 + (int64_t)b * rs : ibot;
             const int32_t *Uc = Ur + ci * uw1;
-            const int32_t kmc = __ldg(Uk + ci);
-            const int32_t Ta = gT[a * CR_THREADS], Xa = gX[a * CR_THREADS];
-            const int32_t Tb = gT[b * CR_THREADS], Xb = gX[b * CR_THREADS];
-            const int32_t k0 = max(0, Ta - dist);
-            const int32_t kend = min(Tb + dist, kmc);
-            Key best = ~(Key)0;
-            int32_t kl, kh;
-            if (kend - k0 < FW) {
-                // window path: load [k0, kend] at once, resolve both bounds with
-                // register compares, issue the gathers together
-                int32_t Uw[FW];
-#pragma unroll
-                for (int t = 0; t < FW; ++t)
-                    Uw[t] = k0 + t <= kend ? __ldg(Uc + k0 + t) : 0x7fffffff;
-                int32_t tlo = FW, thi = -1;
-#pragma unroll
-                for (int t = FW - 1; t >= 0; --t)
-                    if (Uw[t] >= Xa) tlo = t;  // first k with U[c,k] >= X(a,j)
-#pragma unroll
-                for (int t = 0; t < FW; ++t)
-                    if (k0 + t <= kend && Uw[t] <= Xb) thi = t;  // last k with U[c,k] <= X(b,j)
-                kl = max(k0 + tlo, jj - wl);
-                kh = min(k0 + thi, jj);
-                if (kl <= kh) {
-#pragma unroll
-                    for (int t = 0; t < FW; ++t) {
-                        const int32_t k = k0 + t;
-                        if (k >= kl && k <= kh) {
-                            const int32_t v = __ldg(Lr + (int64_t)(Uw[t] - 1) * lw1 + (jj - k));
-                            const Key key = tpack<Key>(v, k, shift);
-                            best = key < best ? key : best;
-                        }
-                    }
-                }
-            } else {
+            const int32_t kmc = real ? __ldg(Uk + ci) : -1;
+            const int32_t Ra = sR[a * CR_THREADS], Rb = sR[b * CR_THREADS];
+            bool tail = false;
+            int32_t kl = 0, outv = inf, outk = 0;
+            if (real && Ra < inf) {
+                const int32_t Ta = sT[a * CR_THREADS];
+                const int32_t Xa = __ldg(Ur + ai * uw1 + Ta);
                 int32_t hi = min(Ta, kmc);
-                int32_t lo = min(k0, hi);
+                int32_t lo = min(max(0, Ta - dist), hi);
                 while (lo < hi) {  // first k with U[c,k] >= X(a,j)
                     const int32_t md = (lo + hi) >> 1;
                     if (__ldg(Uc + md) >= Xa) hi = md; else lo = md + 1;
                 }
-                kl = max(lo, jj - wl);
-                lo = min(Tb, kmc);
-                hi = kend;
-                while (lo < hi) {  // last k with U[c,k] <= X(b,j)
-                    const int32_t md = (lo + hi + 1) >> 1;
-                    if (__ldg(Uc + md) <= Xb) lo = md; else hi = md - 1;
-                }
-                kh = min(lo, jj);
-                for (int32_t k = kl; k <= kh; ++k) {
-                    const int32_t v = __ldg(Lr + (int64_t)(__ldg(Uc + k) - 1) * lw1 + (jj - k));
-                    const Key key = tpack<Key>(v, k, shift);
-                    best = key < best ? key : best;
+                kl = max(lo, j - wl);
+                if (Rb < inf) {
+                    const int32_t Tb = sT[b * CR_THREADS];
+                    const int32_t Xb = __ldg(Ur + bi * uw1 + Tb);
+                    lo = min(Tb, kmc);
+                    hi = min(Tb + dist, kmc);
+                    while (lo < hi) {  // last k with U[c,k] <= X(b,j)
+                        const int32_t md = (lo + hi + 1) >> 1;
+                        if (__ldg(Uc + md) <= Xb) lo = md; else hi = md - 1;
+                    }
+                    int32_t kh = min(lo, j);
+                    if (kl > kh) {  // safety net: never taken when the bounds hold
+                        kl = max(0, j - wl);
+                        kh = min(j, kmc);
+                    }
+                    Key best = ~(Key)0;
+                    for (int32_t k = kl; k <= kh; ++k) {
+                        const int32_t x = __ldg(Uc + k);  // finite: k <= kmax_c
+                        const int32_t v = __ldg(Lr + (int64_t)(x - 1) * lw1 + (j - k));
+                        const Key key = tpack<Key>(v, k, shift);
+                        best = key < best ? key : best;
+                    }
+                    outv = tval<Key>(best, shift);  // (b,j) finite => non-empty range
+                    outk = tk<Key>(best, shift);
+                } else {
+                    tail = true;
                 }
             }
-            if (kl > kh) {  // safety net: never taken when the bounds hold
-                for (int32_t k = max(0, jj - wl); k <= min(jj, kmc); ++k) {
-                    const int32_t v = __ldg(Lr + (int64_t)(__ldg(Uc + k) - 1) * lw1 + (jj - k));
-                    const Key key = tpack<Key>(v, k, shift);
-                    best = key < best ? key : best;
-                }
+            if (!tail) {
+                sR[r * CR_THREADS] = outv;
+                sT[r * CR_THREADS] = outk;
             }
-            const int32_t bk = tk<Key>(best, shift);  // (b,j) finite => non-empty range
-            gR[r * CR_THREADS] = tval<Key>(best, shift);
-            gT[r * CR_THREADS] = bk;
-            gX[r * CR_THREADS] = __ldg(Uc + bk);
-        }
-        __syncwarp();
-        // ---- tail cells (finite above, INF below: no upper bound): the whole
-        // warp scans each one's range [lower bound, min(j, kmax_c)] in turn
-        for (int q = 0; q < tn; ++q) {
-            const int e = s_tq[wid][q];
-            const int l = e >> 8, r = e & 0xff;
-            int32_t jj, rbb;
-            int64_t ii0;
-            lane_ctx(l, jj, ii0, rbb);
-            int32_t *gR = csm + warp_t0 + l, *gT = gR + (S + 1) * CR_THREADS, *gX = gT + (S + 1) * CR_THREADS;
-            const int a = r - dl;
-            const int64_t ci = ii0 + (int64_t)r * rs;
-            const int32_t *Uc = Ur + ci * uw1;
-            const int32_t kmc = __ldg(Uk + ci);
-            const int32_t Ta = gT[a * CR_THREADS], Xa = gX[a * CR_THREADS];
-            int32_t hi = min(Ta, kmc);
-            int32_t lo = min(max(0, Ta - dist), hi);
-            while (lo < hi) {  // first k with U[c,k] >= X(a,j)
-                const int32_t md = (lo + hi) >> 1;
-                if (__ldg(Uc + md) >= Xa) hi = md; else lo = md + 1;
-            }
-            const int32_t tkl = max(lo, jj - wl), tkh = min(jj, kmc);
-            int32_t outv = inf, outk = 0, outx = 0;
-            if (tkl <= tkh) {
+            // tail cells (finite above, INF below: no upper bound): the whole
+            // warp scans each one's range [kl, min(j, kmax_c)] in turn
+            unsigned mask = __ballot_sync(0xffffffffu, tail);
+            while (mask) {
+                const int src = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const int32_t tj = __shfl_sync(0xffffffffu, j, src);
+                const int32_t tkl = __shfl_sync(0xffffffffu, kl, src);
+                const int32_t tkh = min(tj, __shfl_sync(0xffffffffu, kmc, src));
+                const int64_t trow = __shfl_sync(0xffffffffu, ci, src);
+                const int32_t *Ut = Ur + trow * uw1;
                 Key best = ~(Key)0;
                 for (int32_t k = tkl + lane; k <= tkh; k += 32) {
                     int32_t v = inf;
-                    if (jj - k <= wl) v = __ldg(Lr + (int64_t)(__ldg(Uc + k) - 1) * lw1 + (jj - k));
+                    if (tj - k <= wl) v = __ldg(Lr + (int64_t)(__ldg(Ut + k) - 1) * lw1 + (tj - k));
                     const Key key = tpack<Key>(v, k, shift);
                     best = key < best ? key : best;
                 }
                 best = twarp_min(best);
-                outv = tval<Key>(best, shift);
-                outk = tk<Key>(best, shift);
-                if (outv < inf) outx = __ldg(Uc + outk);
+                if (lane == src) {  // an empty candidate range means INF
+                    sR[r * CR_THREADS] = best == ~(Key)0 ? inf : tval<Key>(best, shift);
+                    sT[r * CR_THREADS] = best == ~(Key)0 ? 0 : tk<Key>(best, shift);
+                }
             }
-            if (lane == 0) {
-                gR[r * CR_THREADS] = outv;
-                gT[r * CR_THREADS] = outk;
-                gX[r * CR_THREADS] = outx;
-            }
-            __syncwarp();
         }
-        __syncwarp();
     }
-    // write the interior cells (staged: reach of INF cells too, since later
-    // stages read these rows as bounds) and report each row's finite frontier
+    // write every interior cell's reach (INF included: later stages read these
+    // rows as bounds) and the finite cells' traces; report each row's frontier
 #pragma unroll 1
     for (int r = 1; r < S; ++r) {
         const int32_t v = sR[r * CR_THREADS];
         const bool real = active && r < rb;
         const bool fin = real && v < inf;
         const int64_t row = i0 + (int64_t)r * rs;
-        if (kStaged ? real : fin) {
+        if (real) {
             const int64_t off = row * w1 + j;
             d.out_reach[off] = v;
             if (fin) d.out_trace[off] = sT[r * CR_THREADS];
+        }
+        // frontier: finite here and the next lane's cell (same row) is not
+        const bool nfin = __shfl_down_sync(0xffffffffu, fin, 1);
+        const int64_t nrow = __shfl_down_sync(0xffffffffu, row, 1);
+        if (fin && (lane == 31 || !nfin || nrow != row)) atomicMax(d.out_kmax + row, j);
+    }
+}
+
+// rs == 1 specialisation (the hot one): identical cell logic, fewer registers.
+template <typename Key>
+__global__ void __launch_bounds__(CR_THREADS)
+    column_refine_fine_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int shift,
+                         int32_t S, int32_t nblk, int32_t w1max, int64_t spd) {
+    extern __shared__ int32_t csm[];
+    int32_t *sR = csm + threadIdx.x;                     // sR[r * CR_THREADS]
+    int32_t *sT = csm + (S + 1) * CR_THREADS + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int64_t gt = blockIdx.x * (int64_t)CR_THREADS + threadIdx.x;
+    const int64_t di = gt / spd;  // warp-uniform: spd % 32 == 0
+    if (di >= ndesc) return;
+    const int64_t slot = gt - di * spd;
+    const int32_t blk = (int32_t)(slot / w1max);
+    const int32_t j = (int32_t)(slot - (int64_t)blk * w1max);
+    const CombineDesc &d = descs[di];
+    const int64_t n1 = (int64_t)c.n + 1;
+    const int32_t inf = c.inf;
+    const bool active = blk < nblk && j < d.w1;
+    const int64_t i0 = (int64_t)blk * S;
+    const int32_t rb = active ? (int32_t)min((int64_t)S, n1 - 1 - i0) : 0;
+    const int32_t *__restrict__ Ur = d.U.reach;
+    const int32_t *__restrict__ Uk = d.U.kmax;
+    const int32_t *__restrict__ Lr = d.L.reach;
+    const int32_t uw1 = d.U.w1, lw1 = d.L.w1, wl = lw1 - 1;
+    const int32_t w1 = d.w1;
+
+    {
+        int32_t r0v = inf, r0t = 0, rbv = inf, rbt = 0;
+        if (active && rb >= 2) {
+            r0v = __ldg(d.out_reach + i0 * w1 + j);
+            r0t = __ldg(d.out_trace + i0 * w1 + j);
+            rbv = __ldg(d.out_reach + (i0 + rb) * w1 + j);
+            rbt = __ldg(d.out_trace + (i0 + rb) * w1 + j);
+        }
+        sR[0] = r0v;
+        sT[0] = r0t;
+        for (int r = 1; r <= S; ++r) {
+            sR[r * CR_THREADS] = r >= rb ? rbv : inf;
+            sT[r * CR_THREADS] = r >= rb ? rbt : 0;
+        }
+    }
+#pragma unroll 1
+    for (int dl = S >> 1; dl >= 1; dl >>= 1) {
+#pragma unroll 1
+        for (int r = dl; r < S; r += 2 * dl) {
+            const int a = r - dl, b = r + dl;  // b <= S; rows >= rb mirror the bottom row
+            const bool real = active && r < rb;
+            const int64_t ci = i0 + r;
+            const int32_t *Uc = Ur + ci * uw1;
+            const int32_t kmc = real ? __ldg(Uk + ci) : -1;
+            const int32_t Ra = sR[a * CR_THREADS], Rb = sR[b * CR_THREADS];
+            bool tail = false;
+            int32_t kl = 0, outv = inf, outk = 0;
+            if (real && Ra < inf) {
+                const int32_t Ta = sT[a * CR_THREADS];
+                const int32_t Xa = __ldg(Ur + (i0 + a) * uw1 + Ta);
+                int32_t hi = min(Ta, kmc);
+                int32_t lo = min(max(0, Ta - dl), hi);
+                while (lo < hi) {  // first k with U[c,k] >= X(a,j)
+                    const int32_t md = (lo + hi) >> 1;
+                    if (__ldg(Uc + md) >= Xa) hi = md; else lo = md + 1;
+                }
+                kl = max(lo, j - wl);
+                if (Rb < inf) {
+                    const int32_t Tb = sT[b * CR_THREADS];
+                    const int32_t Xb = __ldg(Ur + min(i0 + b, i0 + rb) * uw1 + Tb);
+                    lo = min(Tb, kmc);
+                    hi = min(Tb + dl, kmc);
+                    while (lo < hi) {  // last k with U[c,k] <= X(b,j)
+                        const int32_t md = (lo + hi + 1) >> 1;
+                        if (__ldg(Uc + md) <= Xb) lo = md; else hi = md - 1;
+                    }
+                    int32_t kh = min(lo, j);
+                    if (kl > kh) {  // safety net: never taken when the bounds hold
+                        kl = max(0, j - wl);
+                        kh = min(j, kmc);
+                    }
+                    Key best = ~(Key)0;
+                    for (int32_t k = kl; k <= kh; ++k) {
+                        const int32_t x = __ldg(Uc + k);  // finite: k <= kmax_c
+                        const int32_t v = __ldg(Lr + (int64_t)(x - 1) * lw1 + (j - k));
+                        const Key key = tpack<Key>(v, k, shift);
+                        best = key < best ? key : best;
+                    }
+                    outv = tval<Key>(best, shift);  // (b,j) finite => non-empty range
+                    outk = tk<Key>(best, shift);
+                } else {
+                    tail = true;
+                }
+            }
+            if (!tail) {
+                sR[r * CR_THREADS] = outv;
+                sT[r * CR_THREADS] = outk;
+            }
+            // tail cells (finite above, INF below: no upper bound): the whole
+            // warp scans each one's range [kl, min(j, kmax_c)] in turn
+            unsigned mask = __ballot_sync(0xffffffffu, tail);
+            while (mask) {
+                const int src = __ffs(mask) - 1;
+                mask &= mask - 1;
+                const int32_t tj = __shfl_sync(0xffffffffu, j, src);
+                const int32_t tkl = __shfl_sync(0xffffffffu, kl, src);
+                const int32_t tkh = min(tj, __shfl_sync(0xffffffffu, kmc, src));
+                const int64_t trow = __shfl_sync(0xffffffffu, ci, src);
+                const int32_t *Ut = Ur + trow * uw1;
+                if (tkl > tkh) {  // empty candidate range (j beyond kmax_c + wl): INF
+                    if (lane == src) sR[r * CR_THREADS] = inf;
+                    continue;
+                }
+                Key best = ~(Key)0;
+                for (int32_t k = tkl + lane; k <= tkh; k += 32) {
+                    int32_t v = inf;
+                    if (tj - k <= wl) v = __ldg(Lr + (int64_t)(__ldg(Ut + k) - 1) * lw1 + (tj - k));
+                    const Key key = tpack<Key>(v, k, shift);
+                    best = key < best ? key : best;
+                }
+                best = twarp_min(best);
+                if (lane == src) {
+                    sR[r * CR_THREADS] = tval<Key>(best, shift);
+                    sT[r * CR_THREADS] = tk<Key>(best, shift);
+                }
+            }
+        }
+    }
+    // write the finite interior cells; report the finite frontier of each row
+#pragma unroll 1
+    for (int r = 1; r < S; ++r) {
+        const int32_t v = sR[r * CR_THREADS];
+        const bool fin = active && r < rb && v < inf;
+        const int64_t row = i0 + r;
+        if (fin) {
+            const int64_t off = row * w1 + j;
+            d.out_reach[off] = v;
+            d.out_trace[off] = sT[r * CR_THREADS];
         }
         // frontier: finite here and the next lane's cell (same row) is not
         const bool nfin = __shfl_down_sync(0xffffffffu, fin, 1);
@@ -429,31 +448,35 @@ __global__ void __launch_bounds__(32 * FN_WARPS)
 int launch_block_refine(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
                         int32_t S, int32_t rs, int32_t maxw1, cudaStream_t s) {
     if (ndesc <= 0) return 0;
-    if (S < 2 || S > 16 || rs < 1) return (int)cudaErrorInvalidValue;  // queue capacity
+    if (S < 2 || S > 64 || rs < 1) return (int)cudaErrorInvalidValue;
     const int64_t n1 = (int64_t)c.n + 1;
     const int32_t nblk = (int32_t)((n1 - 1 + (int64_t)S * rs - 1) / ((int64_t)S * rs));
     if (nblk <= 0) return 0;
     const int64_t spd = ((int64_t)nblk * maxw1 + 31) / 32 * 32;
     const unsigned blocks = (unsigned)((spd * ndesc + CR_THREADS - 1) / CR_THREADS);
-    const size_t smem = (size_t)3 * (S + 1) * CR_THREADS * 4;
+    const size_t smem = (size_t)2 * (S + 1) * CR_THREADS * 4;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(column_refine_kernel<uint32_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(column_refine_kernel<uint32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(column_refine_kernel<uint64_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        cudaFuncSetAttribute(column_refine_kernel<uint64_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(column_refine_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
+        cudaFuncSetAttribute(column_refine_kernel<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
+        cudaFuncSetAttribute(column_refine_fine_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
+        cudaFuncSetAttribute(column_refine_fine_kernel<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
         attr = true;
     }
-    // rs == 1 is the last stage: INF cells are left to finalize_rows_kernel
-#define LCSG_COLREF(K, ST)                                                                     \
-    column_refine_kernel<K, ST><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift, S, rs, \
-                                                                 nblk, maxw1, spd)
-    if (key64) {
-        if (rs == 1) LCSG_COLREF(uint64_t, false); else LCSG_COLREF(uint64_t, true);
+    if (rs == 1) {  // last stage: lean kernel (finite cells only; finalize writes INF)
+        if (key64)
+            column_refine_fine_kernel<uint64_t><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift,
+                                                                                S, nblk, maxw1, spd);
+        else
+            column_refine_fine_kernel<uint32_t><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift,
+                                                                                S, nblk, maxw1, spd);
+    } else if (key64) {
+        column_refine_kernel<uint64_t><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift, S,
+                                                                       rs, nblk, maxw1, spd);
     } else {
-        if (rs == 1) LCSG_COLREF(uint32_t, false); else LCSG_COLREF(uint32_t, true);
+        column_refine_kernel<uint32_t><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift, S,
+                                                                       rs, nblk, maxw1, spd);
     }
-#undef LCSG_COLREF
     LCSG_LAUNCH_CHECK();
     return 0;
 }
