@@ -124,6 +124,22 @@ int lcsg_combine_level(const int32_t *upper_reach, int32_t wu1, const int32_t *u
 int lcsg_base_case_row(const uint8_t *cols_dev, int64_t n, uint8_t sym, int32_t *out_dev,
                        void *stream);
 
+/* ---- multi-GPU building blocks -------------------------- */
+/* Rows [i_lo, i_hi) of one combine (_combine_tables, solver.py:91-110) with the
+ * fast exact kernels, on DEVICE tables of n1 rows: U/L reach (+kmax) in,
+ * reach/trace/kmax rows [i_lo, i_hi) out; *out_wstar (device int32, caller
+ * zero-initialises) is atomicMax'ed with the window's kmax.  Lets ranks shard
+ * an upper-level combine over start columns.  Asynchronous on `stream`. */
+int lcsg_combine_rows(const int32_t *upper_reach, int32_t wu1, const int32_t *upper_kmax,
+                      const int32_t *lower_reach, int32_t wl1, const int32_t *lower_kmax,
+                      int32_t lower_wstar, int32_t *out_reach, int32_t *out_trace,
+                      int32_t *out_kmax, int32_t *out_wstar, int32_t w1, int32_t inf, int64_t n1,
+                      int64_t i_lo, int64_t i_hi, void *stream);
+/* The recovery walk (solver.py:180-207) of a handle's slab from start column
+ * i_start (1-based) for weight j: writes the slab's m_slab+1 cross-vertex
+ * columns to HOST memory (a band sub-tree's share of the full-grid path). */
+int lcsg_recover_from(lcsg_handle h, int32_t i_start, int32_t j, int32_t *cols_out);
+
 /* ---- instrumentation ----------------------------------------------------- */
 /* Number of kernels the library launched on this handle (for bench
  * gpu_launches); time (ms, CUDA events on the handle stream) spent in the

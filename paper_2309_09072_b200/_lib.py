@@ -73,6 +73,9 @@ SIGNATURES = {
     "lcsg_combine_level": (ctypes.c_int, [_vp, _i32, _vp, _vp, _i32, _i32, _vp, _vp, _i32,
                                           ctypes.c_int, _i32, _i64, _i64, _i64, _vp]),
     "lcsg_base_case_row": (ctypes.c_int, [_vp, _i64, ctypes.c_uint8, _vp, _vp]),
+    "lcsg_combine_rows": (ctypes.c_int, [_vp, _i32, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp,
+                                         _vp, _i32, _i32, _i64, _i64, _i64, _vp]),
+    "lcsg_recover_from": (ctypes.c_int, [_vp, _i32, _i32, _vp]),
     "lcsg_stats": (ctypes.c_int, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_double),
                                   ctypes.POINTER(ctypes.c_double),
                                   ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64),

@@ -442,7 +442,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     for (int32_t id = 0; id < nn; ++id) {
         const NodeH &nd = t->nodes[id];
         WalkNode &w = hw[id];
-        w.top_row = nd.top_row;
+        w.top_row = nd.top_row - t->top_row + 1;  // relative: cols index = top_row - 1
         w.bottom_row = nd.bottom_row;
         w.upper = nd.upper;
         w.lower = nd.lower;
@@ -542,13 +542,13 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
 
 bool full_grid(const lcsg_tree_s *t) { return t->top_row == 1 && t->bottom_row == t->m_grid + 1; }
 
-// recovery walk for weight j (j < 0: the LCS length, read on the device)
-int run_walk(lcsg_tree_s *t, int32_t j) {
+// recovery walk for weight j from start column i_start (j < 0: the largest
+// weight from i_start, read on the device)
+int run_walk(lcsg_tree_s *t, int32_t j, int32_t i_start = 1) {
     const cudaStream_t s = t->stream;
     const Ctx c = t->ctx();
     const TabDev rt = t->tab(t->root);
-    CKL(launch_walk_root(t->d_walk, t->root, c, rt, j, (int32_t)t->m_slab, t->d_wi, t->d_wj,
-                         t->d_path, s));
+    CKL(launch_walk_root(t->d_walk, t->root, c, rt, j, i_start, t->d_wi, t->d_wj, t->d_path, s));
     ++t->launches;
     const bool retrace = !t->with_trace;
     for (auto &dr : t->depth_ranges) {
@@ -556,7 +556,7 @@ int run_walk(lcsg_tree_s *t, int32_t j) {
                               t->d_path, retrace, t->walk_shift, t->walk_key64, s));
         ++t->launches;
     }
-    CKL(launch_walk_final(c, rt, j, (int32_t)t->m_slab, t->d_wj + t->root, t->d_path, s));
+    CKL(launch_walk_final(c, rt, i_start, (int32_t)t->m_slab, t->d_wj + t->root, t->d_path, s));
     ++t->launches;
     return LCSG_OK;
 }
@@ -945,6 +945,101 @@ int lcsg_stats(lcsg_handle h, int64_t *launches, double *combine_ms, double *lea
     if (total_ms) *total_ms = c;
     if (h2d_bytes) *h2d_bytes = h->h2d_bytes;
     if (d2h_bytes) *d2h_bytes = h->d2h_bytes;
+    return LCSG_OK;
+}
+
+int lcsg_recover_from(lcsg_handle h, int32_t i_start, int32_t j, int32_t *cols_out) {
+    if (!h) return fail(LCSG_EINVAL, "null handle");
+    if (i_start < 1 || (int64_t)i_start > h->n + 1) return fail(LCSG_EINVAL, "start column out of range");
+    if (j < 0) return fail(LCSG_EINVAL, "negative weight");
+    DeviceGuard g(h->device);
+    const NodeH &r = h->nodes[h->root];
+    const int64_t n1 = h->n + 1;
+    int32_t km = 0;
+    if (r.upper < 0) {
+        int32_t *p = nullptr;
+        int rc = leaf_device(h, h->root, &p);
+        if (rc) return rc;
+        CK(cudaMemcpyAsync(&km, p + n1 * r.w1 + (i_start - 1), 4, cudaMemcpyDeviceToHost, h->stream));
+    } else {
+        CK(cudaMemcpyAsync(&km, h->d_tables + r.kmax_off + (i_start - 1), 4, cudaMemcpyDeviceToHost,
+                           h->stream));
+    }
+    CK(cudaStreamSynchronize(h->stream));
+    if (j > km)
+        return fail(LCSG_ERANGE, "no path of weight " + std::to_string(j) + " from column " +
+                                     std::to_string(i_start) + " (max " + std::to_string(km) + ")");
+    int rc = run_walk(h, j, i_start);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(cols_out, h->d_path, (size_t)(h->m_slab + 1) * 4, cudaMemcpyDeviceToHost,
+                       h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    return LCSG_OK;
+}
+
+int lcsg_combine_rows(const int32_t *upper_reach, int32_t wu1, const int32_t *upper_kmax,
+                      const int32_t *lower_reach, int32_t wl1, const int32_t *lower_kmax,
+                      int32_t lower_wstar, int32_t *out_reach, int32_t *out_trace,
+                      int32_t *out_kmax, int32_t *out_wstar, int32_t w1, int32_t inf, int64_t n1,
+                      int64_t i_lo, int64_t i_hi, void *stream) {
+    if (i_lo < 0 || i_hi > n1 || i_lo > i_hi) return fail(LCSG_EINVAL, "bad row range");
+    if (!out_trace || !out_kmax || !out_wstar) return fail(LCSG_EINVAL, "null output buffer");
+    const int64_t rows = i_hi - i_lo;
+    if (rows == 0) return LCSG_OK;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    int rc = prepare_device(dev);
+    if (rc) return rc;
+    cudaStream_t s = (cudaStream_t)stream;
+    struct Scratch {
+        CombineDesc d;
+        int32_t wstar_l;
+    };
+    Scratch *sc = nullptr;
+    CK(cudaMallocAsync((void **)&sc, sizeof(Scratch), s));
+    Scratch hs;
+    std::memset(&hs, 0, sizeof(hs));
+    // the row window [i_lo, i_hi) is addressed as a table of `rows` rows; L
+    // keeps absolute rows (x = U[i,k] indexes it directly)
+    hs.d.U = TabDev{upper_reach + i_lo * wu1, upper_kmax + i_lo, nullptr, wu1, -1};
+    hs.d.L = TabDev{lower_reach, lower_kmax, &sc->wstar_l, wl1, -1};
+    hs.d.out_reach = out_reach + i_lo * w1;
+    hs.d.out_trace = out_trace + i_lo * w1;
+    hs.d.out_kmax = out_kmax + i_lo;
+    hs.d.out_wstar = out_wstar;
+    hs.d.w1 = w1;
+    hs.wstar_l = lower_wstar;
+    CK(cudaMemcpyAsync(sc, &hs, sizeof(hs), cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(out_kmax + i_lo, 0xFF, (size_t)rows * 4, s));
+    Ctx c;
+    c.rows = nullptr;
+    c.nx = nullptr;
+    c.n = (int32_t)(rows - 1);
+    c.inf = inf;
+    const int shift = bits_for(wu1 - 1);
+    const bool key64 = bits_for(inf) + shift > 32;
+    const int thread_max_w1 = env_int("LCSG_THREAD_MAX_W1", 33);
+    int S = 1;
+    while (S * 2 <= std::max(1, env_int("LCSG_SKELETON_STRIDE", 64))) S *= 2;
+    int col_block = 1;
+    while (col_block * 2 <= std::min(16, std::max(2, env_int("LCSG_COL_BLOCK", 8)))) col_block *= 2;
+    if (w1 <= thread_max_w1 || S == 1 || rows < 3) {
+        CKL(launch_combine(w1 <= 65 ? 0 : 1, &sc->d, 1, c, shift, key64, s));
+    } else {
+        if (w1 <= env_int("LCSG_SKEL_THREAD_MAX_W1", 257))
+            CKL(launch_combine(0, &sc->d, 1, c, shift, key64, s, S));
+        else if (w1 <= env_int("LCSG_SKEL_WARP_MAX_W1", 4097))
+            CKL(launch_combine(1, &sc->d, 1, c, shift, key64, s, S));
+        else
+            CKL(launch_skeleton(&sc->d, 1, c, shift, key64, S, s));
+        for (int32_t rem = S; rem > 1;) {
+            const int32_t B = std::min<int32_t>(col_block, rem);
+            CKL(launch_block_refine(&sc->d, 1, c, shift, key64, B, rem / B, w1, s));
+            rem /= B;
+        }
+        CKL(launch_finalize_rows(&sc->d, 1, c, S, s, w1));
+    }
+    CK(cudaFreeAsync(sc, s));
     return LCSG_OK;
 }
 

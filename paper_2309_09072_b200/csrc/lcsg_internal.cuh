@@ -111,8 +111,9 @@ int launch_walk_level(const WalkNode *nodes, const int32_t *ids, int32_t count, 
                       int32_t *wi, int32_t *wj, int32_t *cols_out, bool retrace, int key_shift,
                       bool key64, cudaStream_t s);
 int launch_walk_root(const WalkNode *nodes, int32_t root, Ctx c, TabDev root_tab, int32_t j,
-                     int32_t m, int32_t *wi, int32_t *wj, int32_t *cols_out, cudaStream_t s);
-int launch_walk_final(Ctx c, TabDev root_tab, int32_t j, int32_t m, const int32_t *wj_root,
+                     int32_t i_start, int32_t *wi, int32_t *wj, int32_t *cols_out,
+                     cudaStream_t s);
+int launch_walk_final(Ctx c, TabDev root_tab, int32_t i_start, int32_t m, const int32_t *wj_root,
                       int32_t *cols_out, cudaStream_t s);
 int launch_assemble(const uint8_t *rows, int32_t m, const uint8_t *cols, int32_t n,
                     const int32_t *path, int32_t *out_len, int32_t *row_pos, int32_t *col_pos,

@@ -475,34 +475,36 @@ int launch_walk_level(const WalkNode *nodes, const int32_t *ids, int32_t count, 
 
 // Root of the walk: j < 0 means "the LCS length" = kmax[0] of the root
 // (solver.py:160-162), read on the device so no host round trip is needed.
+// (i_start = 1 for lcs(); other start columns walk a band sub-tree for the
+// multi-GPU schedule; WalkNode.top_row is relative to the slab's first row.)
 __global__ void walk_root_kernel(const WalkNode *nodes, int32_t root, Ctx c, TabDev root_tab,
-                                 int32_t j, int32_t *wi, int32_t *wj, int32_t *cols_out) {
+                                 int32_t j, int32_t i_start, int32_t *wi, int32_t *wj,
+                                 int32_t *cols_out) {
     const TabAcc R = resolve(root_tab, c);
-    const int32_t jj = j >= 0 ? j : tab_kmax(R, 0, c.inf);
-    wi[root] = 1;
+    const int32_t jj = j >= 0 ? j : tab_kmax(R, i_start - 1, c.inf);
+    wi[root] = i_start;
     wj[root] = jj;
-    if (nodes[root].is_leaf) cols_out[nodes[root].top_row - 1] = 1;
+    if (nodes[root].is_leaf) cols_out[nodes[root].top_row - 1] = i_start;
 }
 
 int launch_walk_root(const WalkNode *nodes, int32_t root, Ctx c, TabDev root_tab, int32_t j,
-                     int32_t m, int32_t *wi, int32_t *wj, int32_t *cols_out, cudaStream_t s) {
-    (void)m;
-    walk_root_kernel<<<1, 1, 0, s>>>(nodes, root, c, root_tab, j, wi, wj, cols_out);
+                     int32_t i_start, int32_t *wi, int32_t *wj, int32_t *cols_out,
+                     cudaStream_t s) {
+    walk_root_kernel<<<1, 1, 0, s>>>(nodes, root, c, root_tab, j, i_start, wi, wj, cols_out);
     LCSG_LAUNCH_CHECK();
     return 0;
 }
 
-// cols[m] = table.reach[0, j] (solver.py:206)
-__global__ void walk_final_kernel(Ctx c, TabDev root_tab, int32_t m, const int32_t *wj_root,
-                                  int32_t *cols_out) {
+// cols[m] = table.reach[i_start-1, j] (solver.py:206)
+__global__ void walk_final_kernel(Ctx c, TabDev root_tab, int32_t m, int32_t i_start,
+                                  const int32_t *wj_root, int32_t *cols_out) {
     const TabAcc R = resolve(root_tab, c);
-    cols_out[m] = tab_get(R, 0, *wj_root);
+    cols_out[m] = tab_get(R, i_start - 1, *wj_root);
 }
 
-int launch_walk_final(Ctx c, TabDev root_tab, int32_t j, int32_t m, const int32_t *wj_root,
+int launch_walk_final(Ctx c, TabDev root_tab, int32_t i_start, int32_t m, const int32_t *wj_root,
                       int32_t *cols_out, cudaStream_t s) {
-    (void)j;
-    walk_final_kernel<<<1, 1, 0, s>>>(c, root_tab, m, wj_root, cols_out);
+    walk_final_kernel<<<1, 1, 0, s>>>(c, root_tab, m, i_start, wj_root, cols_out);
     LCSG_LAUNCH_CHECK();
     return 0;
 }

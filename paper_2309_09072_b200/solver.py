@@ -209,7 +209,7 @@ def recover_cross_vertices(g: GridModel, table: CostTable, j: int) -> np.ndarray
     return cols
 
 
-def assemble_lcs(g: GridModel, path_cols: np.ndarray) -> LcsResult:
+def assemble_lcs(g: GridModel, path_cols: np.ndarray, *, device=None) -> LcsResult:
     """Read the subsequence off a cross-vertex path (reference
     solver.py:210-234): mark + scan + compact kernel on the device."""
     m, n = g.m, g.n
@@ -223,7 +223,7 @@ def assemble_lcs(g: GridModel, path_cols: np.ndarray) -> LcsResult:
     cp = np.empty(k, dtype=np.int32)
     rows = np.frombuffer(g.row_seq, dtype=np.uint8)
     cols = np.frombuffer(g.col_seq, dtype=np.uint8)
-    rc = _lib.load().lcsg_assemble(_ptr(rows), m, _ptr(cols), n, _ptr(path), 0,
+    rc = _lib.load().lcsg_assemble(_ptr(rows), m, _ptr(cols), n, _ptr(path), _device(device),
                                    ctypes.byref(length), _ptr(sub), _ptr(rp), _ptr(cp))
     _lib.check(rc, "assemble_lcs")
     L = int(length.value)
