@@ -24,9 +24,11 @@ cpu_baseline: the real reference (oracle/_ref, Cython backend) timed on this
 
 --impl reference runs the reference's own CPU path (oracle/_ref, all host
 threads) on the same config's bounded sample; rank 0 only.
-N > 1 (torchrun): each rank solves its own instance (seed + rank) of the same
-config on its own GPU -- weak scaling; the split-tree multi-GPU schedule is
-described in DESIGN.md and exercised by tests/test_distributed.py.
+N > 1 (torchrun): ONE solve of the config split across the ranks (strong
+scaling): each rank builds the reference tree's band subtrees, the upper
+combines are sharded over start columns with NCCL broadcasts of finished row
+ranges (paper_2309_09072_b200/distributed.py); --replicas runs
+an independent instance per GPU instead (weak scaling).
 """
 
 from __future__ import annotations
@@ -61,6 +63,8 @@ def parse():
     p.add_argument("--seed", type=int, default=0)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--replicas", action="store_true",
+                   help="N > 1: independent instance per GPU (weak) instead of one sharded solve")
     p.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU baseline work")
     return p.parse_args()
 
@@ -324,6 +328,66 @@ def run_ours(args, rank, world, dist):
     print(json.dumps(line), flush=True)
 
 
+def run_sharded(args, rank, world, dist):
+    """N > 1: ONE solve of the config split across the ranks (strong scaling):
+    band subtrees per rank, upper combines sharded over start columns with
+    NCCL broadcasts of finished row ranges (paper_2309_09072_b200.distributed)."""
+    import torch
+
+    from paper_2309_09072_b200 import distributed as D
+
+    local = int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count()
+    dev = torch.device("cuda", local)
+    a, b = workloads.generate(args.config, args.seed)
+    rows, cols = (b, a) if len(a) > len(b) else (a, b)
+    m, n = len(rows), len(cols)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=dev)
+    r = None
+    for _ in range(args.warmup):
+        r = D.lcs_sharded(a, b, device=local)
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r = D.lcs_sharded(a, b, device=local)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1))
+    t_ms = statistics.mean(times)
+    tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_ms = float(tt.item())
+    _, bands, upper = D.build_plan(m, world)
+    # kernels per solve on the busiest rank: its band build (~levels x 4) +
+    # every upper combine (skeleton, 2 refinement stages, finalize)
+    launches = args.steps * (4 * max(1, (m // max(1, len(bands))).bit_length()) + 4 * len(upper))
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": m * n / (t_ms / 1e3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic",
+        "config": {"workload": workloads.CONFIGS[args.config]["name"], "m": m, "n": n,
+                   "seed": args.seed, "lcs_length": r.length,
+                   "l2": "flushed (256 MiB) between steps",
+                   "parallelism": f"{len(bands)} band subtrees + {len(upper)} upper combines "
+                                  f"sharded over start columns across {world} GPUs (NCCL)"},
+        "roofline": None,
+        "e2e": {"value": m * n / (t_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": m + n,
+                "d2h_bytes_per_step": 4 * (m + 1)},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -336,11 +400,15 @@ def main():
         import torch
         import torch.distributed as tdist
 
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
-        tdist.init_process_group("nccl")
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")) % torch.cuda.device_count())
+        # LCSG_DIST_BACKEND=gloo lets several ranks share one GPU for testing
+        tdist.init_process_group(os.environ.get("LCSG_DIST_BACKEND", "nccl"))
         dist = tdist
     try:
-        run_ours(args, rank, world, dist)
+        if world > 1 and not args.replicas:
+            run_sharded(args, rank, world, dist)
+        else:
+            run_ours(args, rank, world, dist)
     finally:
         if dist is not None:
             dist.destroy_process_group()
