@@ -12,7 +12,8 @@ depth-first on one CPU (solver.py:113-119); here P ranks split it:
   columns i: all ranks hold the full U and L tables, rank r computes rows
   [lo_r, hi_r) (contiguous ranges balanced by the per-row work proxy
   kmax_U[i] + 1) with ``lcsg_combine_rows``, then each owner broadcasts its
-  row range so every rank ends with the full output table;
+  reach/kmax row range so every rank ends with the full output table (traces
+  stay with their owner: the walk needs one cell per upper node);
 * **recovery** -- the walk over the upper nodes (solver.py:180-207) runs on
   every rank from the gathered tables and yields each band's (start column,
   weight); each band owner walks its own subtree (``lcsg_recover_from``) and
@@ -241,11 +242,14 @@ def solve_sharded(rows: bytes, cols: bytes, dist, group=None, backend=None, with
         lo, hi = spans[rank]
         backend.combine_rows(U, L, out, lo, hi, inf)
         backend.synchronize()
+        # reach/kmax row ranges go to every rank (the next level reads them as
+        # U and L); traces stay with their row owner (the walk fetches one cell)
         for r, (a, b) in enumerate(spans):
-            for key in ("reach", "trace", "kmax"):
+            for key in ("reach", "kmax"):
                 _bcast(dist, group, out[key][a:b], r)
         _allreduce_max(dist, group, out["wstar_dev"])
         out["wstar"] = int(out["wstar_dev"].item())
+        out["spans"] = spans
         nd.table = out
     return root, bands, upper
 
@@ -262,7 +266,10 @@ def recover_sharded(root: Node, bands: List[Node], m: int, dist, group=None, bac
         if nd.band >= 0:
             start[nd.band] = (i, jj)
             return
-        k = int(nd.table["trace"][i - 1, jj].item())
+        owner = next(r for r, (a, b) in enumerate(nd.table["spans"]) if a <= i - 1 < b)
+        kt = nd.table["trace"][i - 1, jj].reshape(1).clone()
+        _bcast(dist, group, kt, owner)
+        k = int(kt.item())
         x = int(nd.upper.table["reach"][i - 1, k].item())
         walk(nd.upper, i, k)
         walk(nd.lower, x, jj - k)

@@ -117,7 +117,8 @@ def _cpu_worker(rank, world, port, seed, count):
             t = O.OracleTree(rows, cols)
             ref = t.node(t.root)
             np.testing.assert_array_equal(root.table["reach"].numpy(), ref.reach)
-            np.testing.assert_array_equal(root.table["trace"].numpy(), ref.trace)
+            lo, hi = root.table["spans"][rank]  # traces stay with their row owner
+            np.testing.assert_array_equal(root.table["trace"].numpy()[lo:hi], ref.trace[lo:hi])
             np.testing.assert_array_equal(root.table["kmax"].numpy(), ref.kmax)
             assert root.table["wstar"] == ref.wstar
     finally:
@@ -162,7 +163,8 @@ def _gpu_worker(rank, world, port, seed, count):
         root, bands, upper = D.solve_sharded(rows, cols, dist, None, be)
         tab = L.build_cost_table(L.GridModel(rows, cols), 1, len(rows) + 1)
         np.testing.assert_array_equal(root.table["reach"].cpu().numpy(), tab.reach)
-        np.testing.assert_array_equal(root.table["trace"].cpu().numpy(), tab.trace)
+        lo, hi = root.table["spans"][rank]
+        np.testing.assert_array_equal(root.table["trace"].cpu().numpy()[lo:hi], tab.trace[lo:hi])
         be.free()
         del rng
     finally:
