@@ -398,7 +398,8 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             L.shift = bits_for(maxk);
             L.key64 = vbits + L.shift > 32;
             if (kind < 2) {
-                L.kind = kind;
+                // narrow thread-per-row tables: shared-memory staged row writes
+                L.kind = (kind == 0 && maxw1 <= 33 && env_int("LCSG_STAGED_ROWS", 1)) ? 9 : kind;
                 t->plan.push_back(L);
                 continue;
             }
@@ -520,6 +521,8 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
         const CombineDesc *dd = t->d_descs + L.desc_off;
         if (L.kind <= 1)
             BCKL(launch_combine(L.kind, dd, L.count, c, L.shift, L.key64, s));
+        else if (L.kind == 9)
+            BCKL(launch_combine_staged(dd, L.count, c, L.shift, L.key64, s));
         else if (L.kind == 3)
             BCKL(launch_skeleton(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s));
         else if (L.kind == 5 || L.kind == 6)

@@ -93,6 +93,10 @@ int launch_base_case_row(const uint8_t *cols, int32_t n, uint8_t sym, int32_t *o
 // restricts the launch to the skeleton rows 0, S, 2S, ..., n
 int launch_combine(int kind, const CombineDesc *descs, int32_t ndesc, Ctx c, int key_shift,
                    bool key64, cudaStream_t s, int32_t stride = 1);
+// thread-per-row bisection for tables of width <= 33 with coalesced
+// (shared-memory staged) row writes
+int launch_combine_staged(const CombineDesc *descs, int32_t ndesc, Ctx c, int key_shift,
+                          bool key64, cudaStream_t s);
 // skeleton rows 0, S, 2S, ..., n by exact Alg. 1 (one CTA per row)
 int launch_skeleton(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
                     int32_t stride, cudaStream_t s);

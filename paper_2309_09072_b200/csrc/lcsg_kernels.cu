@@ -291,6 +291,99 @@ __global__ void __launch_bounds__(256) combine_thread_kernel(const CombineDesc *
     if ((threadIdx.x & 31) == 0 && wmax >= 0) atomicMax(d.out_wstar, wmax);
 }
 
+// Same exact bisection for narrow tables (w1 <= TS_W), all rows (stride 1):
+// each thread's row goes to a shared-memory slot first, then every warp writes
+// its 32 consecutive rows as ONE contiguous block.  Writing rows directly
+// (lane-strided stores) made ncu count ~3x the compulsory DRAM traffic on
+// these levels (partially written sectors).
+constexpr int TS_W = 33;       // max table width staged
+constexpr int TS_SLOT = 33;    // odd slot pitch: conflict-free per-lane writes
+constexpr int TS_THREADS = 128;
+
+template <typename Key>
+__global__ void __launch_bounds__(TS_THREADS)
+    combine_thread_staged_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c,
+                                 int shift, int64_t rows_pad) {
+    __shared__ int32_t s_reach[TS_THREADS * TS_SLOT];
+    __shared__ uint16_t s_trace[TS_THREADS * TS_SLOT];
+    const int lane = threadIdx.x & 31;
+    const int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t di = gid / rows_pad;  // warp-uniform: rows_pad % 32 == 0
+    if (di >= ndesc) return;
+    const int64_t i = gid - di * rows_pad;
+    const int64_t n1 = (int64_t)c.n + 1;
+    const CombineDesc &d = descs[di];
+    const int32_t inf = c.inf;
+    const int32_t w1 = d.w1, w = w1 - 1;
+    int32_t *sr = s_reach + threadIdx.x * TS_SLOT;
+    uint16_t *st = s_trace + threadIdx.x * TS_SLOT;
+    int32_t kfin = -1;
+    if (i < n1) {
+        const TabAcc U = resolve(d.U, c), L = resolve(d.L, c);
+        const int32_t wl = L.w1 - 1;
+        const int32_t kmaxU = tab_kmax(U, i, inf);
+        const int32_t colhi = min(w, kmaxU + *d.L.wstar);
+        uint64_t stk[STACK];
+        int sp = 0;
+        int32_t left = 0, right = colhi, top = 0, bottom = kmaxU;
+        for (;;) {
+            while (right >= left) {
+                const int32_t mid = (left + right + 1) >> 1;
+                Key best = ~(Key)0;
+                for (int32_t k = top; k <= bottom; ++k) {
+                    const int32_t x = tab_get(U, i, k);
+                    const Key key = pack<Key>(cell(L, x, k, mid, inf, wl), k, shift);
+                    best = key < best ? key : best;
+                }
+                const int32_t bv = key_val<Key>(best, shift), bk = key_k<Key>(best, shift);
+                sr[mid] = bv;
+                st[mid] = (uint16_t)bk;
+                if (bv != inf) {
+                    kfin = max(kfin, mid);
+                    if (mid + 1 <= right && sp < STACK)
+                        stk[sp++] = ((uint64_t)(uint16_t)(mid + 1) << 48) |
+                                    ((uint64_t)(uint16_t)right << 32) |
+                                    ((uint64_t)(uint16_t)bk << 16) | (uint64_t)(uint16_t)bottom;
+                    right = mid - 1;
+                    bottom = bk;
+                } else {
+                    for (int32_t q = mid + 1; q <= right; ++q) {
+                        sr[q] = inf;
+                        st[q] = (uint16_t)top;
+                    }
+                    right = mid - 1;
+                }
+            }
+            if (sp == 0) break;
+            const uint64_t e = stk[--sp];
+            left = (int32_t)(uint16_t)(e >> 48);
+            right = (int32_t)(uint16_t)(e >> 32);
+            top = (int32_t)(uint16_t)(e >> 16);
+            bottom = (int32_t)(uint16_t)e;
+        }
+        for (int32_t q = colhi + 1; q <= w; ++q) {
+            sr[q] = inf;
+            st[q] = 0;
+        }
+        d.out_kmax[i] = kfin;
+    }
+    __syncwarp();
+    // coalesced copy-out of the warp's consecutive rows
+    const int64_t i0 = i - lane;
+    const int32_t nrow = (int32_t)min((int64_t)32, max((int64_t)0, n1 - i0));
+    const int32_t total = nrow * w1;
+    const int wb = threadIdx.x - lane;
+    int32_t *gr = d.out_reach + i0 * w1;
+    int32_t *gt = d.out_trace ? d.out_trace + i0 * w1 : nullptr;
+    for (int32_t f = lane; f < total; f += 32) {
+        const int32_t rr = f / w1, cc = f - rr * w1;
+        gr[f] = s_reach[(wb + rr) * TS_SLOT + cc];
+        if (gt) gt[f] = s_trace[(wb + rr) * TS_SLOT + cc];
+    }
+    const int32_t wmax = __reduce_max_sync(0xffffffffu, kfin);
+    if (lane == 0 && wmax >= 0) atomicMax(d.out_wstar, wmax);
+}
+
 // Warp-per-row exact bisection: the warp evaluates one Alg. 1 node at a time,
 // lanes striding over its row range [top..bottom] and reducing packed keys
 // with a warp min (REDUX.MIN for 32-bit keys).  The DFS stack is warp-uniform
@@ -371,6 +464,20 @@ __global__ void __launch_bounds__(32 * WARP_KERNEL_WARPS)
         d.out_kmax[i] = kfin;
         atomicMax(d.out_wstar, kfin);
     }
+}
+
+int launch_combine_staged(const CombineDesc *descs, int32_t ndesc, Ctx c, int key_shift,
+                          bool key64, cudaStream_t s) {
+    if (ndesc <= 0) return 0;
+    const int64_t n1 = (int64_t)c.n + 1;
+    const int64_t rows_pad = (n1 + 31) / 32 * 32;
+    const unsigned blocks = (unsigned)((rows_pad * ndesc + TS_THREADS - 1) / TS_THREADS);
+    if (key64)
+        combine_thread_staged_kernel<uint64_t><<<blocks, TS_THREADS, 0, s>>>(descs, ndesc, c, key_shift, rows_pad);
+    else
+        combine_thread_staged_kernel<uint32_t><<<blocks, TS_THREADS, 0, s>>>(descs, ndesc, c, key_shift, rows_pad);
+    LCSG_LAUNCH_CHECK();
+    return 0;
 }
 
 int launch_combine(int kind, const CombineDesc *descs, int32_t ndesc, Ctx c, int key_shift,
