@@ -371,13 +371,17 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     for (auto &nd : t->nodes) maxh = std::max(maxh, nd.height);
     const int vbits = bits_for(t->inf);
     int32_t di = 0;
+    // node ids bucketed by height (ascending id order kept): O(nodes) planning
+    std::vector<std::vector<int32_t>> by_height(maxh + 1);
+    for (int32_t id = 0; id < nn; ++id)
+        if (t->nodes[id].upper >= 0) by_height[t->nodes[id].height].push_back(id);
     for (int32_t h = 1; h <= maxh; ++h) {
         for (int kind = 0; kind < 3; ++kind) {
             int32_t start = di;
             int32_t maxk = 0, maxw1 = 0;
-            for (int32_t id = 0; id < nn; ++id) {
+            for (const int32_t id : by_height[h]) {
                 const NodeH &nd = t->nodes[id];
-                if (nd.height != h || nd.kind != kind) continue;
+                if (nd.kind != kind) continue;
                 CombineDesc &d = hd[di++];
                 d.U = t->tab(nd.upper);
                 d.L = t->tab(nd.lower);
@@ -399,7 +403,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             L.key64 = vbits + L.shift > 32;
             if (kind < 2) {
                 // narrow thread-per-row tables: shared-memory staged row writes
-                L.kind = (kind == 0 && maxw1 <= 33 && env_int("LCSG_STAGED_ROWS", 1)) ? 9 : kind;
+                L.kind = (kind == 0 && maxw1 <= 33 && env_int("LCSG_STAGED_ROWS", 0)) ? 9 : kind;
                 t->plan.push_back(L);
                 continue;
             }
@@ -460,10 +464,12 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     t->walk_shift = bits_for(maxku);
     t->walk_key64 = vbits + t->walk_shift > 32;
     int32_t wpos = 0;
+    std::vector<std::vector<int32_t>> by_depth(maxd + 1);
+    for (int32_t id = 0; id < nn; ++id)
+        if (t->nodes[id].upper >= 0) by_depth[t->nodes[id].depth].push_back(id);
     for (int32_t dd = 0; dd <= maxd; ++dd) {
         int32_t start = wpos;
-        for (int32_t id = 0; id < nn; ++id)
-            if (t->nodes[id].upper >= 0 && t->nodes[id].depth == dd) hids[wpos++] = id;
+        for (const int32_t id : by_depth[dd]) hids[wpos++] = id;
         if (wpos > start) t->depth_ranges.push_back({start, wpos - start});
     }
     int32_t li = 0;
