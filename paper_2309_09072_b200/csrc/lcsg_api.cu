@@ -302,13 +302,17 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     }
     // kmax rows of every combine, contiguous: initialised to -1 in one memset
     // (the tiled refinement folds per-tile maxima into it with atomicMax)
+    // (only the refined combines, kind 2, need it: they come first)
     const int64_t kmax_region = tab_elems;
-    for (auto &nd : t->nodes) {
-        if (nd.upper < 0) continue;
-        nd.kmax_off = tab_elems;
-        tab_elems += (n1 + 63) / 64 * 64;
-    }
-    const int64_t kmax_region_elems = tab_elems - kmax_region;
+    for (int pass = 0; pass < 2; ++pass)
+        for (auto &nd : t->nodes) {
+            if (nd.upper < 0 || (nd.kind == 2) != (pass == 0)) continue;
+            nd.kmax_off = tab_elems;
+            tab_elems += (n1 + 63) / 64 * 64;
+        }
+    int64_t kmax_region_elems = 0;
+    for (auto &nd : t->nodes)
+        if (nd.upper >= 0 && nd.kind == 2) kmax_region_elems += (n1 + 63) / 64 * 64;
     // low-memory mode: the refinement passes still need this level's traces
     // (they bound neighbouring rows); one scratch region reused level by level
     int64_t scratch_elems = 0;
