@@ -18,7 +18,7 @@ _ROOT = os.path.dirname(_PKG)
 LIB_DIR = os.path.join(_PKG, "lib")
 LIB_PATH = os.environ.get("LCSG_LIB_PATH") or os.path.join(LIB_DIR, "liblcsgrid_b200.so")
 CSRC = os.path.join(_PKG, "csrc")
-SOURCES = ["lcsg_api.cu", "lcsg_kernels.cu", "lcsg_refine.cu", "lcsg_tile.cu"]
+SOURCES = ["lcsg_api.cu", "lcsg_kernels.cu", "lcsg_refine.cu", "lcsg_tile.cu", "lcsg_narrow.cu"]
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
     "-Xcompiler", "-fPIC", "-shared",

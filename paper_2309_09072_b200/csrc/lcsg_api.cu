@@ -78,7 +78,9 @@ int prepare_device(int device) {
 }
 
 // Kernel choice per combine:
-//   kind 0: thread-per-row exact bisection        (w1 <= LCSG_THREAD_MAX_W1, default 65)
+//   kind 0: narrow tables (w1 <= LCSG_THREAD_MAX_W1, default 33): staged
+//           brute-force first-wins min (lcsg_narrow.cu; LCSG_NARROW=0 selects
+//           the thread-per-row exact bisection instead)
 //   kind 2: skeleton rows (exact bisection: thread / warp / CTA per row by
 //           width) + refinement passes             (wider)
 //   kind 1: warp-per-row exact bisection          (fallback: U rows too big for smem)
@@ -95,7 +97,9 @@ struct NodeH {
 };
 
 struct LaunchH {
-    int kind;  // 0 thread, 1 warp, 3 skeleton, 4 refine pass
+    // 0 thread, 1 warp, 3 skeleton CTA, 4 refine pass, 5/6 skeleton thread/warp,
+    // 7 column-refinement stage, 8 finalize, 9 staged thread, 10 narrow
+    int kind;
     int32_t desc_off, count;
     int shift;
     bool key64;
@@ -273,6 +277,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     const int skel_warp_max = env_int("LCSG_SKEL_WARP_MAX_W1", 4097);
     // refinement mode: tiled (default) or one launch per pass ("LCSG_REFINE_PASSES=1")
     const bool tiled = env_int("LCSG_REFINE_PASSES", 0) == 0;
+    const bool narrow_on = env_int("LCSG_NARROW", 1) != 0;
     // block size (local rows) of each column-refinement stage, power of two
     int col_block = 1;
     while (col_block * 2 <= std::min(16, std::max(2, env_int("LCSG_COL_BLOCK", 8)))) col_block *= 2;
@@ -382,7 +387,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     for (int32_t h = 1; h <= maxh; ++h) {
         for (int kind = 0; kind < 3; ++kind) {
             int32_t start = di;
-            int32_t maxk = 0, maxw1 = 0;
+            int32_t maxk = 0, maxw1 = 0, maxkl = 0;
             for (const int32_t id : by_height[h]) {
                 const NodeH &nd = t->nodes[id];
                 if (nd.kind != kind) continue;
@@ -397,6 +402,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
                 d.w1 = nd.w1;
                 d.node = id;
                 maxk = std::max(maxk, t->nodes[nd.upper].w1 - 1);
+                maxkl = std::max(maxkl, t->nodes[nd.lower].w1 - 1);
                 maxw1 = std::max(maxw1, nd.w1);
             }
             if (di == start) continue;
@@ -408,6 +414,11 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             if (kind < 2) {
                 // narrow thread-per-row tables: shared-memory staged row writes
                 L.kind = (kind == 0 && maxw1 <= 33 && env_int("LCSG_STAGED_ROWS", 0)) ? 9 : kind;
+                const int P = narrow_bucket(std::max(maxk, maxkl));
+                if (kind == 0 && P > 0 && narrow_on) {
+                    L.kind = 10;
+                    L.stride_or_delta = P;
+                }
                 t->plan.push_back(L);
                 continue;
             }
@@ -533,6 +544,8 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             BCKL(launch_combine(L.kind, dd, L.count, c, L.shift, L.key64, s));
         else if (L.kind == 9)
             BCKL(launch_combine_staged(dd, L.count, c, L.shift, L.key64, s));
+        else if (L.kind == 10)
+            BCKL(launch_narrow(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s));
         else if (L.kind == 3)
             BCKL(launch_skeleton(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s));
         else if (L.kind == 5 || L.kind == 6)
@@ -1036,7 +1049,10 @@ int lcsg_combine_rows(const int32_t *upper_reach, int32_t wu1, const int32_t *up
     while (S * 2 <= std::max(1, env_int("LCSG_SKELETON_STRIDE", 64))) S *= 2;
     int col_block = 1;
     while (col_block * 2 <= std::min(16, std::max(2, env_int("LCSG_COL_BLOCK", 8)))) col_block *= 2;
-    if (w1 <= thread_max_w1 || S == 1 || rows < 3) {
+    const int P = narrow_bucket(std::max(wu1, wl1) - 1);
+    if (w1 <= thread_max_w1 && P > 0 && env_int("LCSG_NARROW", 1) != 0) {
+        CKL(launch_narrow(&sc->d, 1, c, shift, key64, P, s));
+    } else if (w1 <= thread_max_w1 || S == 1 || rows < 3) {
         CKL(launch_combine(w1 <= 65 ? 0 : 1, &sc->d, 1, c, shift, key64, s));
     } else {
         if (w1 <= env_int("LCSG_SKEL_THREAD_MAX_W1", 257))

@@ -97,6 +97,11 @@ int launch_combine(int kind, const CombineDesc *descs, int32_t ndesc, Ctx c, int
 // (shared-memory staged) row writes
 int launch_combine_staged(const CombineDesc *descs, int32_t ndesc, Ctx c, int key_shift,
                           bool key64, cudaStream_t s);
+// narrow combines (every U and L weight <= P, P in 1,2,4,8,16; lcsg_narrow.cu):
+// staged brute-force first-wins minimum, all rows
+int narrow_bucket(int32_t max_weight);  // P, or -1 when too wide
+int launch_narrow(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
+                  int32_t P, cudaStream_t s);
 // skeleton rows 0, S, 2S, ..., n by exact Alg. 1 (one CTA per row)
 int launch_skeleton(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
                     int32_t stride, cudaStream_t s);
