@@ -19,16 +19,21 @@
 
 namespace lcsg {
 
-constexpr int NR_THREADS = 256;  // output rows per CTA (thread per row)
+constexpr int NR_THREADS = 256;
 
 template <int P>
 struct NarrowGeom {
     static constexpr int PITCH = (P + 1) | 1;  // odd pitch: per-row reads conflict-free
-    // dynamic shared memory: U block + L window (~R + 26 P rows at sigma = 26);
-    // after the fold the whole area holds the output staging 2 x R x (2P+1)
-    static constexpr int BYTES = P <= 2 ? 24 * 1024 : P == 4 ? 32 * 1024 : P == 8 ? 48 * 1024
-                                                                                 : 72 * 1024;
-    static_assert(2 * NR_THREADS * (2 * P + 1) * 4 <= BYTES, "output staging must fit");
+    // rows per thread: the per-CTA latency chain (descriptor -> U block -> L
+    // window -> fold -> store) is amortised over more rows when the fold is short
+    static constexpr int RPT = P <= 2 ? 4 : P == 4 ? 2 : 1;
+    static constexpr int ROWS = NR_THREADS * RPT;  // output rows per CTA
+    // dynamic shared memory: U block + L window (~ROWS + 26 P rows at sigma =
+    // 26); after the fold the whole area holds the output staging 2 x ROWS x w1
+    static constexpr int BYTES = P == 1 ? 32 * 1024 : P <= 4 ? 40 * 1024 : P == 8 ? 48 * 1024
+                                                                                : 72 * 1024;
+    static_assert(2 * ROWS * (2 * P + 1) * 4 <= BYTES, "output staging must fit");
+    static_assert((ROWS + 64) * PITCH * 4 <= BYTES, "U block + a minimal L window must fit");
 };
 
 template <typename Key>
@@ -44,10 +49,12 @@ __device__ __forceinline__ void stage_rows(int32_t *dst, const TabAcc &t, int64_
                                            int32_t nrows, int32_t inf) {
     const int tid = threadIdx.x;
     if (t.nx) {  // leaf: (r + 1, NX[sym][r]) (breakout.py:37-55)
+        const int32_t *nx = t.nx + row0;
+        const bool w2 = t.w1 > 1;
         for (int r = tid; r < nrows; r += NR_THREADS) {
             int32_t *d = dst + r * PT;
             d[0] = (int32_t)(row0 + r + 1);
-            if (PT > 1) d[1] = t.w1 > 1 ? __ldg(t.nx + row0 + r) : inf;
+            if (PT > 1) d[1] = w2 ? __ldg(nx + r) : inf;
 #pragma unroll
             for (int k = 2; k < PT; ++k) d[k] = inf;
         }
@@ -77,19 +84,20 @@ template <int P, typename Key>
 __global__ void __launch_bounds__(NR_THREADS)
     narrow_combine_kernel(const CombineDesc *__restrict__ descs, Ctx c, int shift, int32_t bpd,
                           int32_t lcap) {
-    constexpr int PT = NarrowGeom<P>::PITCH;
+    using G = NarrowGeom<P>;
+    constexpr int PT = G::PITCH, RPT = G::RPT, ROWS = G::ROWS;
     extern __shared__ int32_t nsm[];
-    int32_t *sU = nsm;                     // NR_THREADS x PT
-    int32_t *sL = nsm + NR_THREADS * PT;   // (lcap + 1) x PT; row lcap = all INF
+    int32_t *sU = nsm;               // ROWS x PT
+    int32_t *sL = nsm + ROWS * PT;   // (lcap + 1) x PT; row lcap = all INF
     __shared__ int32_t s_xmax, s_wstar;
-    const int64_t di = blockIdx.x / bpd;
-    const int64_t i0 = (int64_t)(blockIdx.x - di * bpd) * NR_THREADS;
+    const int32_t di = blockIdx.x / bpd;
+    const int64_t i0 = (int64_t)(blockIdx.x - di * bpd) * ROWS;
     const CombineDesc &d = descs[di];
     const int64_t n1 = (int64_t)c.n + 1;
-    const int nr = (int)min((int64_t)NR_THREADS, n1 - i0);
+    const int nr = (int)min((int64_t)ROWS, n1 - i0);
     const int32_t inf = c.inf;
     const TabAcc U = resolve(d.U, c), L = resolve(d.L, c);
-    const int32_t wu = U.w1 - 1, wl = L.w1 - 1;
+    const int32_t wl = L.w1 - 1;
     const int tid = threadIdx.x;
     if (tid == 0) {
         s_xmax = 0;
@@ -99,81 +107,97 @@ __global__ void __launch_bounds__(NR_THREADS)
     stage_rows<PT>(sU, U, i0, nr, inf);
     for (int idx = tid; idx < PT; idx += NR_THREADS) sL[lcap * PT + idx] = inf;
     __syncthreads();
-    // kmax_U of this row (finite prefix of the U row) and the reach of the block
-    int32_t ku = -1, xlast = 0;
-    if (tid < nr) {
+    // kmax_U of each row (finite prefix of the U row) and the reach of the block
+    int32_t ku[RPT];
+    int32_t xlast = 0;
 #pragma unroll
-        for (int k = 0; k <= P; ++k) {
-            const int32_t x = sU[tid * PT + k];
-            if (x < inf) {
-                ku = k;
-                xlast = x;
+    for (int q = 0; q < RPT; ++q) {
+        const int r = tid + q * NR_THREADS;
+        ku[q] = -1;
+        if (r < nr) {
+#pragma unroll
+            for (int k = 0; k <= P; ++k) {
+                const int32_t x = sU[r * PT + k];
+                if (x < inf) {
+                    ku[q] = k;
+                    xlast = max(xlast, x);
+                }
             }
         }
-        atomicMax(&s_xmax, xlast);
     }
+    xlast = __reduce_max_sync(0xffffffffu, xlast);
+    if ((tid & 31) == 0) atomicMax(&s_xmax, xlast);
     __syncthreads();
     // 2. the L rows every finite x of the block lands on: [base, base + nL)
     const int64_t base = (int64_t)sU[0] - 1;  // U[i0, 0] = smallest x of the block
     const int32_t nL = (int32_t)min((int64_t)s_xmax - base, (int64_t)lcap);
     stage_rows<PT>(sL, L, base, nL, inf);
     __syncthreads();
-    // 3. first-wins minimum over every candidate of the row, in registers
-    Key best[2 * P + 1];
+    // 3. first-wins minimum over every candidate of each row, in registers
+    Key best[RPT][2 * P + 1];
 #pragma unroll
-    for (int j = 0; j <= 2 * P; ++j) best[j] = ~(Key)0;
-    if (tid < nr) {
+    for (int q = 0; q < RPT; ++q) {
 #pragma unroll
-        for (int k = 0; k <= P; ++k) {
-            const int32_t x = sU[tid * PT + k];
-            const int64_t lr = x < inf ? (int64_t)x - 1 - base : lcap;
-            if (lr < nL || lr == lcap) {
-                const int32_t *row = sL + lr * PT;
+        for (int j = 0; j <= 2 * P; ++j) best[q][j] = ~(Key)0;
+        const int r = tid + q * NR_THREADS;
+        if (r < nr) {
 #pragma unroll
-                for (int e = 0; e <= P; ++e) {
-                    const Key key = npack<Key>(row[e], k, shift);
-                    best[k + e] = key < best[k + e] ? key : best[k + e];
-                }
-            } else {  // beyond the staged window (sparse matches): read L directly
+            for (int k = 0; k <= P; ++k) {
+                const int32_t x = sU[r * PT + k];
+                const int64_t lr = x < inf ? (int64_t)x - 1 - base : lcap;
+                if (lr < nL || lr == lcap) {
+                    const int32_t *row = sL + lr * PT;
 #pragma unroll
-                for (int e = 0; e <= P; ++e) {
-                    const int32_t v = e <= wl ? tab_get(L, (int64_t)x - 1, e) : inf;
-                    const Key key = npack<Key>(v, k, shift);
-                    best[k + e] = key < best[k + e] ? key : best[k + e];
+                    for (int e = 0; e <= P; ++e) {
+                        const Key key = npack<Key>(row[e], k, shift);
+                        best[q][k + e] = key < best[q][k + e] ? key : best[q][k + e];
+                    }
+                } else {  // beyond the staged window (sparse matches): read L directly
+#pragma unroll
+                    for (int e = 0; e <= P; ++e) {
+                        const int32_t v = e <= wl ? tab_get(L, (int64_t)x - 1, e) : inf;
+                        const Key key = npack<Key>(v, k, shift);
+                        best[q][k + e] = key < best[q][k + e] ? key : best[q][k + e];
+                    }
                 }
             }
         }
     }
     __syncthreads();  // sU and sL are reused as the output staging area below
     const int32_t w1 = d.w1, w = w1 - 1;
+    const int32_t wstar_l = *d.L.wstar;
     int32_t *sR = nsm;
-    int32_t *sT = nsm + NR_THREADS * w1;
-    int32_t kfin = -1;
-    if (tid < nr) {
-        int32_t *rr = sR + tid * w1;
-        int32_t *tr = sT + tid * w1;
+    int32_t *sT = nsm + ROWS * w1;
+    int32_t wmax = -1;
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+        const int r = tid + q * NR_THREADS;
+        if (r >= nr) continue;
+        int32_t *rr = sR + r * w1;
+        int32_t *tr = sT + r * w1;
+        int32_t kfin = -1;
 #pragma unroll
         for (int j = 0; j <= 2 * P; ++j) {
             if (j <= w) {
-                const int32_t v = (int32_t)(best[j] >> shift);
+                const int32_t v = (int32_t)(best[q][j] >> shift);
                 if (v < inf) kfin = j;
                 rr[j] = v < inf ? v : inf;
-                tr[j] = (int32_t)(best[j] & (((Key)1 << shift) - 1));
+                tr[j] = (int32_t)(best[q][j] & (((Key)1 << shift) - 1));
             }
         }
         // INF cells: Alg. 1's node `top` (replay of the bisection path over
         // the finite traces), 0 beyond colhi
-        const int32_t colhi = min(w, ku + *d.L.wstar);
-        for (int32_t q = kfin + 1; q <= w; ++q) {
+        const int32_t colhi = min(w, ku[q] + wstar_l);
+        for (int32_t qq = kfin + 1; qq <= w; ++qq) {
             int32_t t = 0;
-            if (q <= colhi) {
+            if (qq <= colhi) {
                 int32_t left = 0, right = colhi, top = 0;
                 for (;;) {
                     const int32_t mid = (left + right + 1) >> 1;
-                    if (mid <= kfin) {  // finite node: q lies to its right
+                    if (mid <= kfin) {  // finite node: qq lies to its right
                         top = tr[mid];
                         left = mid + 1;
-                    } else if (q >= mid) {
+                    } else if (qq >= mid) {
                         break;  // INF node: mid..right all get `top`
                     } else {
                         right = mid - 1;
@@ -181,11 +205,12 @@ __global__ void __launch_bounds__(NR_THREADS)
                 }
                 t = top;
             }
-            tr[q] = t;
+            tr[qq] = t;
         }
-        d.out_kmax[i0 + tid] = kfin;
+        d.out_kmax[i0 + r] = kfin;
+        wmax = max(wmax, kfin);
     }
-    const int32_t wmax = __reduce_max_sync(0xffffffffu, kfin);
+    wmax = __reduce_max_sync(0xffffffffu, wmax);
     if ((tid & 31) == 0 && wmax >= 0) atomicMax(&s_wstar, wmax);
     __syncthreads();
     // 4. the block's rows are one contiguous range of the output
@@ -207,9 +232,9 @@ static int launch_narrow_t(const CombineDesc *descs, int32_t ndesc, Ctx c, int s
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, BYTES);
     if (e != cudaSuccess) return (int)e;
     const int64_t n1 = (int64_t)c.n + 1;
-    const int32_t bpd = (int32_t)((n1 + NR_THREADS - 1) / NR_THREADS);
+    const int32_t bpd = (int32_t)((n1 + NarrowGeom<P>::ROWS - 1) / NarrowGeom<P>::ROWS);
     // L window rows: whatever the budget leaves after the U block
-    const int32_t lcap = (int32_t)(BYTES / 4 - NR_THREADS * PT) / PT - 1;
+    const int32_t lcap = (int32_t)(BYTES / 4 - NarrowGeom<P>::ROWS * PT) / PT - 1;
     const int64_t blocks = (int64_t)ndesc * bpd;
     if (blocks == 0) return 0;
     if (blocks >= ((int64_t)1 << 31)) return (int)cudaErrorInvalidConfiguration;
