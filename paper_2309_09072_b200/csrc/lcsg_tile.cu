@@ -223,6 +223,22 @@ __global__ void __launch_bounds__(CR_THREADS)
     }
 }
 
+// Per-warp scratch of the segmented cooperative scan (fine kernel).
+template <typename Key>
+struct CoopSlot {
+    int32_t start, kl, j, row;
+    Key key;
+};
+__device__ __forceinline__ void key_atomic_min(uint32_t *p, uint32_t v) { atomicMin(p, v); }
+__device__ __forceinline__ void key_atomic_min(uint64_t *p, uint64_t v) {
+    atomicMin((unsigned long long *)p, (unsigned long long)v);
+}
+template <typename Key>
+__device__ __forceinline__ CoopSlot<Key> *coop_slots() {
+    __shared__ CoopSlot<Key> slots[CR_THREADS];
+    return slots;
+}
+
 // rs == 1 specialisation (the hot one): identical cell logic, fewer registers.
 template <typename Key>
 __global__ void __launch_bounds__(CR_THREADS)
@@ -326,34 +342,48 @@ __global__ void __launch_bounds__(CR_THREADS)
                 sT[r * CR_THREADS] = outk;
             }
             // tail cells (finite above, INF below: no upper bound; range
-            // [kl, min(j, kmax_c)]) and long ranges: the whole warp scans each
-            // one in turn
-            const int32_t chi = tail ? min(j, kmc) : khl;
-            unsigned mask = __ballot_sync(0xffffffffu, tail || longr);
-            while (mask) {
-                const int src = __ffs(mask) - 1;
-                mask &= mask - 1;
-                const int32_t tj = __shfl_sync(0xffffffffu, j, src);
-                const int32_t tkl = __shfl_sync(0xffffffffu, kl, src);
-                const int32_t tkh = __shfl_sync(0xffffffffu, chi, src);
-                const int64_t trow = __shfl_sync(0xffffffffu, ci, src);
-                const int32_t *Ut = Ur + trow * uw1;
-                if (tkl > tkh) {  // empty candidate range (j beyond kmax_c + wl): INF
-                    if (lane == src) sR[r * CR_THREADS] = inf;
-                    continue;
+            // [kl, min(j, kmax_c)]) and long ranges: the candidates of all such
+            // cells of the warp are concatenated (prefix sum of the range
+            // lengths) and spread over the lanes; keys reduce per cell with a
+            // shared-memory atomicMin.  (One cell per warp pass left ~2/3 of
+            // the lanes idle and cost ~40% of the kernel's instructions.)
+            const bool coop = tail || longr;
+            if (__any_sync(0xffffffffu, coop)) {
+                const int32_t chi = tail ? min(j, kmc) : khl;
+                const int32_t len = coop ? max(0, chi - kl + 1) : 0;
+                int32_t incl = len;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += t;
                 }
-                Key best = ~(Key)0;
-                for (int32_t k = tkl + lane; k <= tkh; k += 32) {
+                const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
+                CoopSlot<Key> *ws = coop_slots<Key>() + (threadIdx.x >> 5) * 32;
+                ws[lane].start = incl - len;
+                ws[lane].kl = kl;
+                ws[lane].j = j;
+                ws[lane].row = (int32_t)ci;
+                ws[lane].key = ~(Key)0;
+                __syncwarp();
+                for (int32_t g = lane; g < total; g += 32) {
+                    int o = 0;  // owner: last lane whose range starts at or before g
+#pragma unroll
+                    for (int step = 16; step > 0; step >>= 1)
+                        if (ws[o + step].start <= g) o += step;
+                    const int32_t k = ws[o].kl + (g - ws[o].start), tj = ws[o].j;
                     int32_t v = inf;
-                    if (tj - k <= wl) v = __ldg(Lr + (int64_t)(__ldg(Ut + k) - 1) * lw1 + (tj - k));
-                    const Key key = tpack<Key>(v, k, shift);
-                    best = key < best ? key : best;
+                    if (tj - k <= wl)
+                        v = __ldg(Lr + (int64_t)(__ldg(Ur + (int64_t)ws[o].row * uw1 + k) - 1) * lw1 +
+                                  (tj - k));
+                    key_atomic_min(&ws[o].key, tpack<Key>(v, k, shift));
                 }
-                best = twarp_min(best);
-                if (lane == src) {
-                    sR[r * CR_THREADS] = tval<Key>(best, shift);
-                    sT[r * CR_THREADS] = tk<Key>(best, shift);
+                __syncwarp();
+                if (coop) {
+                    const Key best = ws[lane].key;  // empty range (j beyond kmax_c + wl): INF
+                    sR[r * CR_THREADS] = len > 0 ? tval<Key>(best, shift) : inf;
+                    sT[r * CR_THREADS] = len > 0 ? tk<Key>(best, shift) : 0;
                 }
+                __syncwarp();
             }
         }
     }
