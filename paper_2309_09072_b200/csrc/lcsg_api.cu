@@ -273,8 +273,8 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     // int32 tables of every combine node
     const int skel_stride = std::max(1, env_int("LCSG_SKELETON_STRIDE", 64));
     const int thread_max_w1 = env_int("LCSG_THREAD_MAX_W1", 33);
-    const int skel_thread_max = env_int("LCSG_SKEL_THREAD_MAX_W1", 257);
-    const int skel_warp_max = env_int("LCSG_SKEL_WARP_MAX_W1", 4097);
+    const int skel_thread_max = env_int("LCSG_SKEL_THREAD_MAX_W1", 65);
+    const int skel_warp_max = env_int("LCSG_SKEL_WARP_MAX_W1", 257);
     // refinement mode: tiled (default) or one launch per pass ("LCSG_REFINE_PASSES=1")
     const bool tiled = env_int("LCSG_REFINE_PASSES", 0) == 0;
     const bool narrow_on = env_int("LCSG_NARROW", 1) != 0;
@@ -1055,9 +1055,9 @@ int lcsg_combine_rows(const int32_t *upper_reach, int32_t wu1, const int32_t *up
     } else if (w1 <= thread_max_w1 || S == 1 || rows < 3) {
         CKL(launch_combine(w1 <= 65 ? 0 : 1, &sc->d, 1, c, shift, key64, s));
     } else {
-        if (w1 <= env_int("LCSG_SKEL_THREAD_MAX_W1", 257))
+        if (w1 <= env_int("LCSG_SKEL_THREAD_MAX_W1", 65))
             CKL(launch_combine(0, &sc->d, 1, c, shift, key64, s, S));
-        else if (w1 <= env_int("LCSG_SKEL_WARP_MAX_W1", 4097))
+        else if (w1 <= env_int("LCSG_SKEL_WARP_MAX_W1", 257))
             CKL(launch_combine(1, &sc->d, 1, c, shift, key64, s, S));
         else
             CKL(launch_skeleton(&sc->d, 1, c, shift, key64, S, s));

@@ -218,6 +218,7 @@ __device__ __forceinline__ int32_t cell(const TabAcc &L, int32_t x, int32_t k, i
 // Thread-per-row exact bisection (small tables): the reference's col_mins
 // (_kernel.pyx:28-60) as an iterative DFS with an explicit right-sibling stack.
 constexpr int STACK = 24;
+constexpr int CT_THREADS = 64;
 
 template <typename Key>
 __global__ void __launch_bounds__(256) combine_thread_kernel(const CombineDesc *__restrict__ descs,
@@ -388,7 +389,7 @@ __global__ void __launch_bounds__(TS_THREADS)
 // lanes striding over its row range [top..bottom] and reducing packed keys
 // with a warp min (REDUX.MIN for 32-bit keys).  The DFS stack is warp-uniform
 // and lives in shared memory.
-constexpr int WARP_KERNEL_WARPS = 8;
+constexpr int WARP_KERNEL_WARPS = 2;
 constexpr int WSTACK = 34;  // > log2(max colhi) + 1 for colhi < 2^32
 
 template <typename Key>
@@ -489,11 +490,13 @@ int launch_combine(int kind, const CombineDesc *descs, int32_t ndesc, Ctx c, int
     if (kind == 0) {
         const int64_t rows_pad = ((int64_t)nrows + 31) / 32 * 32;
         const int64_t threads = rows_pad * ndesc;
-        const unsigned blocks = (unsigned)((threads + 255) / 256);
+        // small CTAs: per-row DFS work is very uneven, and a CTA holds its
+        // slot until its slowest row is done
+        const unsigned blocks = (unsigned)((threads + CT_THREADS - 1) / CT_THREADS);
         if (key64)
-            combine_thread_kernel<uint64_t><<<blocks, 256, 0, s>>>(descs, ndesc, c, key_shift, rows_pad, stride, nrows);
+            combine_thread_kernel<uint64_t><<<blocks, CT_THREADS, 0, s>>>(descs, ndesc, c, key_shift, rows_pad, stride, nrows);
         else
-            combine_thread_kernel<uint32_t><<<blocks, 256, 0, s>>>(descs, ndesc, c, key_shift, rows_pad, stride, nrows);
+            combine_thread_kernel<uint32_t><<<blocks, CT_THREADS, 0, s>>>(descs, ndesc, c, key_shift, rows_pad, stride, nrows);
     } else {
         const int64_t warps = (int64_t)nrows * ndesc;
         const unsigned blocks = (unsigned)((warps + WARP_KERNEL_WARPS - 1) / WARP_KERNEL_WARPS);

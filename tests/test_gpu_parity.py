@@ -257,7 +257,7 @@ def test_dg_rows_by_definition(cfg):
         np.testing.assert_array_equal(R[i - 1], _dg_row_by_definition(rows, cols, i, R.shape[1]))
 
 
-@pytest.mark.parametrize("stride", [1, 2, 4, 16, 64])
+@pytest.mark.parametrize("stride", [1, 2, 4, 16, 64, 512])
 def test_skeleton_refine_strides(stride, monkeypatch):
     """The wide-table combine (skeleton rows by exact bisection + refinement
     passes bounded by neighbouring rows) is bit-exact -- reach, kmax, wstar
@@ -296,6 +296,9 @@ def test_skeleton_refine_strides(stride, monkeypatch):
     {"LCSG_SKELETON_STRIDE": "32", "LCSG_COL_BLOCK": "32"},  # one stage of 32 rows
     {"LCSG_REFINE_PASSES": "1"},                            # one launch per refinement pass
     {"LCSG_THREAD_MAX_W1": "3", "LCSG_SKEL_THREAD_MAX_W1": "3", "LCSG_SKEL_WARP_MAX_W1": "9"},
+    {"LCSG_SKEL_THREAD_MAX_W1": "1", "LCSG_SKEL_WARP_MAX_W1": "1"},  # CTA kernel for every skeleton row
+    {"LCSG_NARROW": "0"},                                   # bisection kernel for the narrow tables
+    {"LCSG_NARROW": "0", "LCSG_THREAD_MAX_W1": "65"},
 ])
 def test_refinement_variants(env, monkeypatch):
     """Every geometry / schedule of the wide-table combine is bit-exact."""
@@ -320,3 +323,26 @@ def test_refinement_variants(env, monkeypatch):
             np.testing.assert_array_equal(nodes[idx].trace, exp.trace, err_msg=f"{env} {idx}")
             np.testing.assert_array_equal(nodes[idx].kmax, exp.kmax)
             assert nodes[idx].wstar == exp.wstar
+
+
+def test_narrow_window_overflow():
+    """Sparse matches (256 symbols, long columns): the reach of a 16-row slab
+    runs far past the narrow kernel's staged L window, so its direct-read path
+    is exercised; every node stays bit-exact."""
+    rng = np.random.default_rng(4242)
+    for m, n in ((64, 6000), (40, 9000), (33, 3000)):
+        a = rng.integers(0, 256, m).astype(np.uint8).tobytes()
+        b = rng.integers(0, 256, n).astype(np.uint8).tobytes()
+        g = L.GridModel(a, b)
+        t = O.OracleTree(a, b)
+        nodes = gpu_tree_nodes(L.build_cost_table(g, 1, m + 1))
+        for idx in range(len(t)):
+            exp = t.node(idx)
+            if exp.upper < 0:
+                continue
+            np.testing.assert_array_equal(nodes[idx].reach, exp.reach, err_msg=f"{m}x{n} {idx}")
+            np.testing.assert_array_equal(nodes[idx].trace, exp.trace, err_msg=f"{m}x{n} {idx}")
+            np.testing.assert_array_equal(nodes[idx].kmax, exp.kmax)
+            assert nodes[idx].wstar == exp.wstar
+        r = L.lcs(a, b)
+        assert (r.length, r.subsequence, r.row_positions, r.col_positions) == O.lcs(a, b)
