@@ -27,9 +27,6 @@ namespace lcsg {
         if (e__ != cudaSuccess) return (int)e__;    \
     } while (0)
 
-constexpr int BT_THREADS = 256;
-constexpr int BT_MAXS = 64;
-constexpr int BT_TAILCAP = 512;
 constexpr int FN_WARPS = 4;
 
 template <typename Key>
@@ -239,6 +236,37 @@ __device__ __forceinline__ CoopSlot<Key> *coop_slots() {
     return slots;
 }
 
+// Interleave-window counts for the fine kernel: with U[c,.] strictly
+// increasing over finite k, the first k in [lo, hi] with U[c,k] >= Xa is
+// lo + #{k in [lo, hi) : U[c,k] < Xa}, and the last k in [lo2, hi2] with
+// U[c,k] <= Xb is lo2 + #{k in (lo2, hi2] : U[c,k] <= Xb}.
+template <int D>
+__device__ __forceinline__ void window_counts(const int32_t *Uc, int32_t lo, int32_t hi,
+                                              int32_t Xa, bool fb, int32_t lo2, int32_t hi2,
+                                              int32_t Xb, int32_t &c1, int32_t &c2) {
+    c1 = 0;
+    c2 = 0;
+#pragma unroll
+    for (int t = 0; t < D; ++t) {
+        const int32_t k1 = lo + t, k2 = lo2 + 1 + t;
+        const int32_t u1 = k1 < hi ? __ldg(Uc + k1) : INT_MAX;
+        const int32_t u2 = (fb && k2 <= hi2) ? __ldg(Uc + k2) : INT_MAX;
+        c1 += u1 < Xa;
+        c2 += u2 <= Xb;
+    }
+}
+__device__ __forceinline__ void window_counts_n(const int32_t *Uc, int32_t D, int32_t lo,
+                                                int32_t hi, int32_t Xa, bool fb, int32_t lo2,
+                                                int32_t hi2, int32_t Xb, int32_t &c1, int32_t &c2) {
+    c1 = 0;
+    c2 = 0;
+    for (int t = 0; t < D; ++t) {
+        const int32_t k1 = lo + t, k2 = lo2 + 1 + t;
+        if (k1 < hi) c1 += __ldg(Uc + k1) < Xa;
+        if (fb && k2 <= hi2) c2 += __ldg(Uc + k2) <= Xb;
+    }
+}
+
 // rs == 1 specialisation (the hot one): identical cell logic, fewer registers.
 template <typename Key>
 __global__ void __launch_bounds__(CR_THREADS)
@@ -294,25 +322,26 @@ __global__ void __launch_bounds__(CR_THREADS)
             bool tail = false, longr = false;
             int32_t kl = 0, khl = 0, outv = inf, outk = 0;
             if (real && Ra < inf) {
+                const bool fb = Rb < inf;
                 const int32_t Ta = sT[a * CR_THREADS];
+                const int32_t Tb = fb ? sT[b * CR_THREADS] : 0;
+                // both interleave windows hold <= dl+1 candidates: count them
+                // with independent loads (no dependent binary-search steps)
                 const int32_t Xa = __ldg(Ur + (i0 + a) * uw1 + Ta);
-                int32_t hi = min(Ta, kmc);
-                int32_t lo = min(max(0, Ta - dl), hi);
-                while (lo < hi) {  // first k with U[c,k] >= X(a,j)
-                    const int32_t md = (lo + hi) >> 1;
-                    if (__ldg(Uc + md) >= Xa) hi = md; else lo = md + 1;
+                const int32_t Xb = fb ? __ldg(Ur + min(i0 + b, i0 + rb) * uw1 + Tb) : 0;
+                const int32_t hi = min(Ta, kmc);
+                const int32_t lo = min(max(0, Ta - dl), hi);
+                const int32_t lo2 = min(Tb, kmc), hi2 = min(Tb + dl, kmc);
+                int32_t c1, c2;
+                switch (dl) {
+                    case 1: window_counts<1>(Uc, lo, hi, Xa, fb, lo2, hi2, Xb, c1, c2); break;
+                    case 2: window_counts<2>(Uc, lo, hi, Xa, fb, lo2, hi2, Xb, c1, c2); break;
+                    case 4: window_counts<4>(Uc, lo, hi, Xa, fb, lo2, hi2, Xb, c1, c2); break;
+                    default: window_counts_n(Uc, dl, lo, hi, Xa, fb, lo2, hi2, Xb, c1, c2); break;
                 }
-                kl = max(lo, j - wl);
-                if (Rb < inf) {
-                    const int32_t Tb = sT[b * CR_THREADS];
-                    const int32_t Xb = __ldg(Ur + min(i0 + b, i0 + rb) * uw1 + Tb);
-                    lo = min(Tb, kmc);
-                    hi = min(Tb + dl, kmc);
-                    while (lo < hi) {  // last k with U[c,k] <= X(b,j)
-                        const int32_t md = (lo + hi + 1) >> 1;
-                        if (__ldg(Uc + md) <= Xb) lo = md; else hi = md - 1;
-                    }
-                    int32_t kh = min(lo, j);
+                kl = max(lo + c1, j - wl);  // first k with U[c,k] >= X(a,j)
+                if (fb) {
+                    int32_t kh = min(lo2 + c2, j);  // last k with U[c,k] <= X(b,j)
                     if (kl > kh) {  // safety net: never taken when the bounds hold
                         kl = max(0, j - wl);
                         kh = min(j, kmc);
