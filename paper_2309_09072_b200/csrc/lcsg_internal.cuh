@@ -67,6 +67,25 @@ __device__ __forceinline__ int32_t tab_kmax(const TabAcc &t, int64_t r, int32_t 
     return __ldg(t.kmax + r);
 }
 
+// Division by a launch-constant divisor without a divide sequence: q = n / d
+// for 0 <= n < 2^31 as one 64-bit multiply and a shift (M = floor(2^(32+l)/d)
+// + 1, l = ceil(log2 d); exact because (M d - 2^(32+l)) n < 2^(32+l)).
+struct FastDiv {
+    uint64_t M;
+    int32_t d, l;
+};
+inline FastDiv make_fastdiv(int32_t d) {
+    FastDiv f;
+    f.d = d;
+    f.l = 0;
+    while ((1LL << f.l) < d) ++f.l;
+    f.M = (uint64_t)((((unsigned __int128)1) << (32 + f.l)) / (unsigned)d) + 1;
+    return f;
+}
+__device__ __forceinline__ int32_t fdiv(int32_t n, const FastDiv &f) {
+    return (int32_t)(((uint64_t)(uint32_t)n * f.M) >> (32 + f.l));
+}
+
 // Recovery walk node (solver.py:180-207).
 struct WalkNode {
     int32_t top_row, bottom_row;  // absolute 1-based vertex rows

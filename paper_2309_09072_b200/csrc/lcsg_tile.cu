@@ -15,6 +15,7 @@
 // Cells finite in row a but INF in row b (at most 2*delta per row and pass)
 // have no upper bound; they are queued and scanned warp-cooperatively over
 // [lower bound, min(j, kmax_c)].
+#include <algorithm>
 #include <climits>
 
 #include "lcsg_internal.cuh"
@@ -74,19 +75,18 @@ constexpr int CR_INLINE = 4;  // longer candidate ranges go to the warp-cooperat
 template <typename Key>
 __global__ void __launch_bounds__(CR_THREADS)
     column_refine_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int shift,
-                         int32_t S, int32_t rs, int32_t nblk, int32_t w1max, int64_t spd) {
+                         int32_t S, int32_t rs, int32_t nblk, FastDiv w1div) {
     // local row r of block blk is the actual row i0 + r*rs (rs = row step of
     // this refinement stage); rows 0 and S of the block are already known
     extern __shared__ int32_t csm[];
     int32_t *sR = csm + threadIdx.x;  // sR[r * CR_THREADS]
     int32_t *sT = csm + (S + 1) * CR_THREADS + threadIdx.x;
     const int lane = threadIdx.x & 31;
-    const int64_t gt = blockIdx.x * (int64_t)CR_THREADS + threadIdx.x;
-    const int64_t di = gt / spd;  // warp-uniform: spd % 32 == 0
+    const int32_t di = (int32_t)(blockIdx.z * 65535u + blockIdx.y);  // CTA-uniform
     if (di >= ndesc) return;
-    const int64_t slot = gt - di * spd;
-    const int32_t blk = (int32_t)(slot / w1max);
-    const int32_t j = (int32_t)(slot - (int64_t)blk * w1max);
+    const int32_t slot = (int32_t)(blockIdx.x * CR_THREADS + threadIdx.x);
+    const int32_t blk = fdiv(slot, w1div);
+    const int32_t j = slot - blk * w1div.d;
     const CombineDesc &d = descs[di];
     const int64_t n1 = (int64_t)c.n + 1;
     const int32_t inf = c.inf;
@@ -271,17 +271,16 @@ __device__ __forceinline__ void window_counts_n(const int32_t *Uc, int32_t D, in
 template <typename Key>
 __global__ void __launch_bounds__(CR_THREADS)
     column_refine_fine_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int shift,
-                         int32_t S, int32_t nblk, int32_t w1max, int64_t spd) {
+                         int32_t S, int32_t nblk, FastDiv w1div) {
     extern __shared__ int32_t csm[];
     int32_t *sR = csm + threadIdx.x;                     // sR[r * CR_THREADS]
     int32_t *sT = csm + (S + 1) * CR_THREADS + threadIdx.x;
     const int lane = threadIdx.x & 31;
-    const int64_t gt = blockIdx.x * (int64_t)CR_THREADS + threadIdx.x;
-    const int64_t di = gt / spd;  // warp-uniform: spd % 32 == 0
+    const int32_t di = (int32_t)(blockIdx.z * 65535u + blockIdx.y);  // CTA-uniform
     if (di >= ndesc) return;
-    const int64_t slot = gt - di * spd;
-    const int32_t blk = (int32_t)(slot / w1max);
-    const int32_t j = (int32_t)(slot - (int64_t)blk * w1max);
+    const int32_t slot = (int32_t)(blockIdx.x * CR_THREADS + threadIdx.x);
+    const int32_t blk = fdiv(slot, w1div);
+    const int32_t j = slot - blk * w1div.d;
     const CombineDesc &d = descs[di];
     const int64_t n1 = (int64_t)c.n + 1;
     const int32_t inf = c.inf;
@@ -521,8 +520,12 @@ int launch_block_refine(const CombineDesc *descs, int32_t ndesc, Ctx c, int shif
     const int64_t n1 = (int64_t)c.n + 1;
     const int32_t nblk = (int32_t)((n1 - 1 + (int64_t)S * rs - 1) / ((int64_t)S * rs));
     if (nblk <= 0) return 0;
-    const int64_t spd = ((int64_t)nblk * maxw1 + 31) / 32 * 32;
-    const unsigned blocks = (unsigned)((spd * ndesc + CR_THREADS - 1) / CR_THREADS);
+    // grid: x = column slots of one combine (blocks x maxw1), y/z = combine
+    const int64_t slots = (int64_t)nblk * maxw1;
+    if (slots >= ((int64_t)1 << 31)) return (int)cudaErrorInvalidValue;
+    const dim3 blocks((unsigned)((slots + CR_THREADS - 1) / CR_THREADS),
+                      (unsigned)std::min<int32_t>(ndesc, 65535), (unsigned)((ndesc + 65534) / 65535));
+    const FastDiv w1div = make_fastdiv(maxw1);
     const size_t smem = (size_t)2 * (S + 1) * CR_THREADS * 4;
     static bool attr = false;
     if (!attr) {
@@ -535,16 +538,16 @@ int launch_block_refine(const CombineDesc *descs, int32_t ndesc, Ctx c, int shif
     if (rs == 1) {  // last stage: lean kernel (finite cells only; finalize writes INF)
         if (key64)
             column_refine_fine_kernel<uint64_t><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift,
-                                                                                S, nblk, maxw1, spd);
+                                                                                S, nblk, w1div);
         else
             column_refine_fine_kernel<uint32_t><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift,
-                                                                                S, nblk, maxw1, spd);
+                                                                                S, nblk, w1div);
     } else if (key64) {
         column_refine_kernel<uint64_t><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift, S,
-                                                                       rs, nblk, maxw1, spd);
+                                                                       rs, nblk, w1div);
     } else {
         column_refine_kernel<uint32_t><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift, S,
-                                                                       rs, nblk, maxw1, spd);
+                                                                       rs, nblk, w1div);
     }
     LCSG_LAUNCH_CHECK();
     return 0;
