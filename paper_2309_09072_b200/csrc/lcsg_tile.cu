@@ -70,7 +70,7 @@ __device__ __forceinline__ int32_t tcell(const TabAcc &L, int32_t x, int32_t k, 
 // search window then over-covers, which keeps the bound valid.  U and L are
 // always materialised slabs here (never leaves), so plain row pointers are used.
 constexpr int CR_THREADS = 64;
-constexpr int CR_INLINE = 4;  // longer candidate ranges go to the warp-cooperative scan
+constexpr int CR_INLINE = 12;  // longer candidate ranges go to the warp-cooperative scan
 
 template <typename Key>
 __global__ void __launch_bounds__(CR_THREADS)
