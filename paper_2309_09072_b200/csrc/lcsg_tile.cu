@@ -488,7 +488,9 @@ __global__ void __launch_bounds__(32 * FN_WARPS)
     }
     kmax_warp = __reduce_max_sync(0xffffffffu, kmax_warp);
     __syncwarp();
-    // phase 2: fill the INF suffix of each row, coalesced
+    // phase 2: fill the INF suffix of each row, coalesced: reach INF over
+    // (K, w], trace 0 over (colhi, w], and each INF node's segment
+    // [mid_s, hi_s] (hi_0 = colhi, hi_s = mid_{s-1} - 1) with its `top`
     for (int rr = 0; rr < rpw; ++rr) {
         const bool ract = __shfl_sync(0xffffffffu, act, rr);
         if (!ract) continue;
@@ -498,16 +500,13 @@ __global__ void __launch_bounds__(32 * FN_WARPS)
         const int2 *sg = seg_all[wid][rr];
         int32_t *reach = d.out_reach + (r0 + rr) * d.w1;
         int32_t *trace = d.out_trace + (r0 + rr) * d.w1;
-        for (int32_t q = Kr + 1 + lane; q <= w; q += 32) {
-            int32_t tv = 0;
-            if (q <= ch) {
-                int s = 0;
-                while (s + 1 < ns && sg[s + 1].x > q) ++s;  // mids descend; segment s = [mid_s, prev-1]
-                while (s < ns && sg[s].x > q) ++s;
-                tv = s < ns ? sg[s].y : 0;
-            }
-            reach[q] = inf;
-            trace[q] = tv;
+        for (int32_t q = Kr + 1 + lane; q <= w; q += 32) reach[q] = inf;
+        for (int32_t q = max(ch, Kr) + 1 + lane; q <= w; q += 32) trace[q] = 0;
+        int32_t hi = ch;
+        for (int sgi = 0; sgi < ns; ++sgi) {
+            const int2 e = sg[sgi];
+            for (int32_t q = e.x + lane; q <= hi; q += 32) trace[q] = e.y;
+            hi = e.x - 1;
         }
     }
     if (lane == 0 && kmax_warp >= 0) atomicMax(d.out_wstar, kmax_warp);
