@@ -449,11 +449,10 @@ __global__ void __launch_bounds__(32 * FN_WARPS)
     __shared__ int nseg_all[FN_WARPS][32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t n1 = (int64_t)c.n + 1;
-    const int64_t rows_pd = (n1 + rpw - 1) / rpw * rpw;  // padded rows per desc
-    const int64_t gw = blockIdx.x * (int64_t)FN_WARPS + wid;
-    const int64_t di = (gw * rpw) / rows_pd;
-    if (di >= ndesc) return;  // warp-uniform
-    const int64_t r0 = gw * rpw - di * rows_pd;
+    const int32_t di = (int32_t)(blockIdx.z * 65535u + blockIdx.y);  // CTA-uniform
+    if (di >= ndesc) return;
+    const int64_t r0 = ((int64_t)blockIdx.x * FN_WARPS + wid) * rpw;
+    if (r0 >= n1) return;  // warp-uniform
     const CombineDesc &d = descs[di];
     const int32_t inf = c.inf;
     const TabAcc U = resolve(d.U, c);
@@ -461,7 +460,7 @@ __global__ void __launch_bounds__(32 * FN_WARPS)
     const int32_t wstarL = *d.L.wstar;
     // phase 1: lane = row
     const int64_t i = r0 + lane;
-    const bool act = lane < rpw && i < n1 - 1 && (i % S) != 0;
+    const bool act = lane < rpw && i < n1 - 1 && (i & (S - 1)) != 0;  // S: power of two
     int32_t K = -1, colhi = -1, kmax_warp = -1;
     if (act) {
         colhi = min(w, tab_kmax(U, i, inf) + wstarL);
@@ -557,9 +556,10 @@ int launch_finalize_rows(const CombineDesc *descs, int32_t ndesc, Ctx c, int32_t
     if (ndesc <= 0) return 0;
     const int64_t n1 = (int64_t)c.n + 1;
     const int rpw = maxw1 <= 512 ? 32 : (maxw1 <= 2048 ? 8 : (maxw1 <= 8192 ? 2 : 1));
-    const int64_t rows_pd = (n1 + rpw - 1) / rpw * rpw;
-    const int64_t warps = rows_pd / rpw * ndesc;
-    const unsigned blocks = (unsigned)((warps + FN_WARPS - 1) / FN_WARPS);
+    if (S & (S - 1)) return (int)cudaErrorInvalidValue;
+    const int64_t warps = (n1 + rpw - 1) / rpw;  // per combine
+    const dim3 blocks((unsigned)((warps + FN_WARPS - 1) / FN_WARPS),
+                      (unsigned)std::min<int32_t>(ndesc, 65535), (unsigned)((ndesc + 65534) / 65535));
     finalize_rows_kernel<<<blocks, 32 * FN_WARPS, 0, s>>>(descs, ndesc, c, S, rpw);
     LCSG_LAUNCH_CHECK();
     return 0;
