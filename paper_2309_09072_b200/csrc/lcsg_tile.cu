@@ -350,6 +350,11 @@ __global__ void __launch_bounds__(CR_THREADS)
                         // (a profile showed the per-lane loop at 7.8 active lanes)
                         longr = true;
                         khl = kh;
+                    } else if (kl == kh && Xa == Xb) {
+                        // pinned crossing: X(c,j) = X(a,j) = X(b,j) = U[c,kl]
+                        // is already known -- one gather, no U load
+                        outv = __ldg(Lr + (int64_t)(Xa - 1) * lw1 + (j - kl));
+                        outk = kl;
                     } else {
                         Key best = ~(Key)0;
                         for (int32_t k = kl; k <= kh; ++k) {
