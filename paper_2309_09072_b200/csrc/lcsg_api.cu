@@ -305,19 +305,13 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             tab_elems += n1 * nd.w1;
         }
     }
-    // kmax rows of every combine, contiguous: initialised to -1 in one memset
-    // (the tiled refinement folds per-tile maxima into it with atomicMax)
-    // (only the refined combines, kind 2, need it: they come first)
-    const int64_t kmax_region = tab_elems;
-    for (int pass = 0; pass < 2; ++pass)
-        for (auto &nd : t->nodes) {
-            if (nd.upper < 0 || (nd.kind == 2) != (pass == 0)) continue;
-            nd.kmax_off = tab_elems;
-            tab_elems += (n1 + 63) / 64 * 64;
-        }
-    int64_t kmax_region_elems = 0;
-    for (auto &nd : t->nodes)
-        if (nd.upper >= 0 && nd.kind == 2) kmax_region_elems += (n1 + 63) / 64 * 64;
+    // kmax rows of every combine (written by the kernel that finishes each row:
+    // narrow / skeleton / finalize -- no initialisation needed)
+    for (auto &nd : t->nodes) {
+        if (nd.upper < 0) continue;
+        nd.kmax_off = tab_elems;
+        tab_elems += (n1 + 63) / 64 * 64;
+    }
     // low-memory mode: the refinement passes still need this level's traces
     // (they bound neighbouring rows); one scratch region reused level by level
     int64_t scratch_elems = 0;
@@ -531,8 +525,6 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     t->h2d_bytes = (int64_t)meta.size() + (rows_dev ? 0 : t->m_slab) + (cols_dev ? 0 : n);
     // the pageable-host copy above is staged synchronously, so `meta` may die
     BCK(cudaMemsetAsync(t->d_node_wstar, 0, (size_t)nn * 4, s));
-    if (kmax_region_elems > 0)
-        BCK(cudaMemsetAsync(t->d_tables + kmax_region, 0xFF, (size_t)kmax_region_elems * 4, s));
     BCKL(launch_nx(t->d_cols, (int32_t)n, t->d_nx, t->d_sym_wstar, s));
     BCKL(launch_leaf_wstar(t->d_rows, t->d_leaf_nodes, t->d_leaf_rows, t->nleaves,
                            t->d_sym_wstar, t->d_node_wstar, s));
@@ -1036,7 +1028,6 @@ int lcsg_combine_rows(const int32_t *upper_reach, int32_t wu1, const int32_t *up
     hs.d.w1 = w1;
     hs.wstar_l = lower_wstar;
     CK(cudaMemcpyAsync(sc, &hs, sizeof(hs), cudaMemcpyHostToDevice, s));
-    CK(cudaMemsetAsync(out_kmax + i_lo, 0xFF, (size_t)rows * 4, s));
     Ctx c;
     c.rows = nullptr;
     c.nx = nullptr;

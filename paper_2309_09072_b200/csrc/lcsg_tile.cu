@@ -201,22 +201,16 @@ __global__ void __launch_bounds__(CR_THREADS)
         }
     }
     // write every interior cell's reach (INF included: later stages read these
-    // rows as bounds) and the finite cells' traces; report each row's frontier
+    // rows as bounds, finalize finds each row's finite prefix in them) and the
+    // finite cells' traces
 #pragma unroll 1
     for (int r = 1; r < S; ++r) {
         const int32_t v = sR[r * CR_THREADS];
-        const bool real = active && r < rb;
-        const bool fin = real && v < inf;
-        const int64_t row = i0 + (int64_t)r * rs;
-        if (real) {
-            const int64_t off = row * w1 + j;
+        if (active && r < rb) {
+            const int64_t off = (i0 + (int64_t)r * rs) * w1 + j;
             d.out_reach[off] = v;
-            if (fin) d.out_trace[off] = sT[r * CR_THREADS];
+            if (v < inf) d.out_trace[off] = sT[r * CR_THREADS];
         }
-        // frontier: finite here and the next lane's cell (same row) is not
-        const bool nfin = __shfl_down_sync(0xffffffffu, fin, 1);
-        const int64_t nrow = __shfl_down_sync(0xffffffffu, row, 1);
-        if (fin && (lane == 31 || !nfin || nrow != row)) atomicMax(d.out_kmax + row, j);
     }
 }
 
@@ -420,21 +414,16 @@ __global__ void __launch_bounds__(CR_THREADS)
             }
         }
     }
-    // write the finite interior cells; report the finite frontier of each row
+    // write every interior cell's reach (INF included: finalize finds each
+    // row's finite prefix in it) and the finite cells' traces
 #pragma unroll 1
     for (int r = 1; r < S; ++r) {
         const int32_t v = sR[r * CR_THREADS];
-        const bool fin = active && r < rb && v < inf;
-        const int64_t row = i0 + r;
-        if (fin) {
-            const int64_t off = row * w1 + j;
+        if (active && r < rb) {
+            const int64_t off = (i0 + r) * w1 + j;
             d.out_reach[off] = v;
-            d.out_trace[off] = sT[r * CR_THREADS];
+            if (v < inf) d.out_trace[off] = sT[r * CR_THREADS];
         }
-        // frontier: finite here and the next lane's cell (same row) is not
-        const bool nfin = __shfl_down_sync(0xffffffffu, fin, 1);
-        const int64_t nrow = __shfl_down_sync(0xffffffffu, row, 1);
-        if (fin && (lane == 31 || !nfin || nrow != row)) atomicMax(d.out_kmax + row, j);
     }
 }
 
@@ -469,13 +458,16 @@ __global__ void __launch_bounds__(32 * FN_WARPS)
     int32_t K = -1, colhi = -1, kmax_warp = -1;
     if (act) {
         colhi = min(w, tab_kmax(U, i, inf) + wstarL);
-        K = d.out_kmax[i];
+        const int32_t *reach = d.out_reach + i * d.w1;
         const int32_t *trace = d.out_trace + i * d.w1;
+        // the replay of Alg. 1's bisection over [0, colhi] IS a binary search
+        // for the end of the row's finite prefix: finite mids go right, INF
+        // mids are the INF nodes (their segments) and go left; K = left - 1
         int32_t left = 0, right = colhi, fm = -1;
         int ns = 0;
         while (right >= left) {
             const int32_t mid = (left + right + 1) >> 1;
-            if (mid <= K) {
+            if (__ldg(reach + mid) < inf) {
                 fm = mid;
                 left = mid + 1;
             } else {
@@ -483,6 +475,8 @@ __global__ void __launch_bounds__(32 * FN_WARPS)
                 right = mid - 1;
             }
         }
+        K = left - 1;
+        d.out_kmax[i] = K;
         for (int s = 0; s < ns; ++s) {  // resolve tops (independent loads)
             const int32_t f = seg_all[wid][lane][s].y;
             seg_all[wid][lane][s].y = f >= 0 ? __ldg(trace + f) : 0;
@@ -492,8 +486,8 @@ __global__ void __launch_bounds__(32 * FN_WARPS)
     }
     kmax_warp = __reduce_max_sync(0xffffffffu, kmax_warp);
     __syncwarp();
-    // phase 2: fill the INF suffix of each row, coalesced: reach INF over
-    // (K, w], trace 0 over (colhi, w], and each INF node's segment
+    // phase 2: fill the INF suffix traces of each row, coalesced (the reach
+    // cells are already written): 0 over (colhi, w], and each INF node's segment
     // [mid_s, hi_s] (hi_0 = colhi, hi_s = mid_{s-1} - 1) with its `top`
     for (int rr = 0; rr < rpw; ++rr) {
         const bool ract = __shfl_sync(0xffffffffu, act, rr);
@@ -502,9 +496,7 @@ __global__ void __launch_bounds__(32 * FN_WARPS)
         const int32_t ch = __shfl_sync(0xffffffffu, colhi, rr);
         const int ns = nseg_all[wid][rr];
         const int2 *sg = seg_all[wid][rr];
-        int32_t *reach = d.out_reach + (r0 + rr) * d.w1;
         int32_t *trace = d.out_trace + (r0 + rr) * d.w1;
-        for (int32_t q = Kr + 1 + lane; q <= w; q += 32) reach[q] = inf;
         for (int32_t q = max(ch, Kr) + 1 + lane; q <= w; q += 32) trace[q] = 0;
         int32_t hi = ch;
         for (int sgi = 0; sgi < ns; ++sgi) {

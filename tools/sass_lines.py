@@ -1,13 +1,22 @@
 """Per-source-line instruction and stall shares of one kernel: joins an ncu
 SASS source page (--page source --csv --print-source sass) with nvdisasm
 --print-line-info output of the same cubin function.
-Usage: python tools/sass_lines.py page.csv func_li.sass source.cu [N]"""
+Usage: python tools/sass_lines.py page.csv cubin_li.sass source.cu [N] [func-substring]
+(cubin_li.sass = nvdisasm --print-line-info -c of the whole cubin; the
+function is cut from its label to the next function label)"""
 import collections, csv, re, sys
 
 page, li, src_path = sys.argv[1:4]
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 30
+func = sys.argv[5] if len(sys.argv) > 5 else None
+lines = open(li).read().split("\n")
+if func:
+    labels = [i for i, l in enumerate(lines) if re.match(r"^_Z\w+:$", l)]
+    start = next(i for i in labels if func in lines[i])
+    end = next((i for i in labels if i > start), len(lines))
+    lines = lines[start:end]
 cur, off2line = None, {}
-for l in open(li):
+for l in lines:
     m = re.search(r'line (\d+)', l)
     if m:
         cur = int(m.group(1))
