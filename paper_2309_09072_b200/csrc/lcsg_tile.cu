@@ -465,6 +465,9 @@ __global__ void __launch_bounds__(32 * FN_WARPS)
         // mids are the INF nodes (their segments) and go left; K = left - 1
         int32_t left = 0, right = colhi, fm = -1;
         int ns = 0;
+        // common at the lower levels: the whole [0, colhi] is finite, every
+        // mid goes right and there is no INF node (fm is then unused)
+        if (__ldg(reach + colhi) < inf) left = colhi + 1;
         while (right >= left) {
             const int32_t mid = (left + right + 1) >> 1;
             if (__ldg(reach + mid) < inf) {
