@@ -72,6 +72,38 @@ __device__ __forceinline__ int32_t tcell(const TabAcc &L, int32_t x, int32_t k, 
 constexpr int CR_THREADS = 64;
 constexpr int CR_INLINE = 12;  // longer candidate ranges go to the warp-cooperative scan
 
+// Interleave-window counts (column kernels): with U[c,.] strictly
+// increasing over finite k, the first k in [lo, hi] with U[c,k] >= Xa is
+// lo + #{k in [lo, hi) : U[c,k] < Xa}, and the last k in [lo2, hi2] with
+// U[c,k] <= Xb is lo2 + #{k in (lo2, hi2] : U[c,k] <= Xb}.
+template <int D>
+__device__ __forceinline__ void window_counts(const int32_t *Uc, int32_t lo, int32_t hi,
+                                              int32_t Xa, bool fb, int32_t lo2, int32_t hi2,
+                                              int32_t Xb, int32_t &c1, int32_t &c2) {
+    c1 = 0;
+    c2 = 0;
+#pragma unroll
+    for (int t = 0; t < D; ++t) {
+        const int32_t k1 = lo + t, k2 = lo2 + 1 + t;
+        const int32_t u1 = k1 < hi ? __ldg(Uc + k1) : INT_MAX;
+        const int32_t u2 = (fb && k2 <= hi2) ? __ldg(Uc + k2) : INT_MAX;
+        c1 += u1 < Xa;
+        c2 += u2 <= Xb;
+    }
+}
+__device__ __forceinline__ void window_counts_n(const int32_t *Uc, int32_t D, int32_t lo,
+                                                int32_t hi, int32_t Xa, bool fb, int32_t lo2,
+                                                int32_t hi2, int32_t Xb, int32_t &c1, int32_t &c2) {
+    c1 = 0;
+    c2 = 0;
+    for (int t = 0; t < D; ++t) {
+        const int32_t k1 = lo + t, k2 = lo2 + 1 + t;
+        if (k1 < hi) c1 += __ldg(Uc + k1) < Xa;
+        if (fb && k2 <= hi2) c2 += __ldg(Uc + k2) <= Xb;
+    }
+}
+
+
 template <typename Key>
 __global__ void __launch_bounds__(CR_THREADS)
     column_refine_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int shift,
@@ -134,25 +166,40 @@ __global__ void __launch_bounds__(CR_THREADS)
             bool tail = false;
             int32_t kl = 0, outv = inf, outk = 0;
             if (real && Ra < inf) {
+                const bool fb = Rb < inf;
                 const int32_t Ta = sT[a * CR_THREADS];
+                const int32_t Tb = fb ? sT[b * CR_THREADS] : 0;
                 const int32_t Xa = __ldg(Ur + ai * uw1 + Ta);
-                int32_t hi = min(Ta, kmc);
-                int32_t lo = min(max(0, Ta - dist), hi);
-                while (lo < hi) {  // first k with U[c,k] >= X(a,j)
-                    const int32_t md = (lo + hi) >> 1;
-                    if (__ldg(Uc + md) >= Xa) hi = md; else lo = md + 1;
+                const int32_t Xb = fb ? __ldg(Ur + bi * uw1 + Tb) : 0;
+                const int32_t hi1 = min(Ta, kmc);
+                const int32_t lo1 = min(max(0, Ta - dist), hi1);
+                const int32_t lo2 = min(Tb, kmc), hi2 = min(Tb + dist, kmc);
+                int32_t lo, kh0;
+                if (dist <= 8) {  // short windows: independent counting loads
+                    int32_t c1, c2;
+                    window_counts<8>(Uc, lo1, hi1, Xa, fb, lo2, hi2, Xb, c1, c2);
+                    lo = lo1 + c1;
+                    kh0 = lo2 + c2;
+                } else {
+                    lo = lo1;
+                    int32_t hi = hi1;
+                    while (lo < hi) {  // first k with U[c,k] >= X(a,j)
+                        const int32_t md = (lo + hi) >> 1;
+                        if (__ldg(Uc + md) >= Xa) hi = md; else lo = md + 1;
+                    }
+                    kh0 = lo2;
+                    if (fb) {
+                        int32_t l2 = lo2, h2 = hi2;
+                        while (l2 < h2) {  // last k with U[c,k] <= X(b,j)
+                            const int32_t md = (l2 + h2 + 1) >> 1;
+                            if (__ldg(Uc + md) <= Xb) l2 = md; else h2 = md - 1;
+                        }
+                        kh0 = l2;
+                    }
                 }
                 kl = max(lo, j - wl);
-                if (Rb < inf) {
-                    const int32_t Tb = sT[b * CR_THREADS];
-                    const int32_t Xb = __ldg(Ur + bi * uw1 + Tb);
-                    lo = min(Tb, kmc);
-                    hi = min(Tb + dist, kmc);
-                    while (lo < hi) {  // last k with U[c,k] <= X(b,j)
-                        const int32_t md = (lo + hi + 1) >> 1;
-                        if (__ldg(Uc + md) <= Xb) lo = md; else hi = md - 1;
-                    }
-                    int32_t kh = min(lo, j);
+                if (fb) {
+                    int32_t kh = min(kh0, j);
                     if (kl > kh) {  // safety net: never taken when the bounds hold
                         kl = max(0, j - wl);
                         kh = min(j, kmc);
@@ -228,37 +275,6 @@ template <typename Key>
 __device__ __forceinline__ CoopSlot<Key> *coop_slots() {
     __shared__ CoopSlot<Key> slots[CR_THREADS];
     return slots;
-}
-
-// Interleave-window counts for the fine kernel: with U[c,.] strictly
-// increasing over finite k, the first k in [lo, hi] with U[c,k] >= Xa is
-// lo + #{k in [lo, hi) : U[c,k] < Xa}, and the last k in [lo2, hi2] with
-// U[c,k] <= Xb is lo2 + #{k in (lo2, hi2] : U[c,k] <= Xb}.
-template <int D>
-__device__ __forceinline__ void window_counts(const int32_t *Uc, int32_t lo, int32_t hi,
-                                              int32_t Xa, bool fb, int32_t lo2, int32_t hi2,
-                                              int32_t Xb, int32_t &c1, int32_t &c2) {
-    c1 = 0;
-    c2 = 0;
-#pragma unroll
-    for (int t = 0; t < D; ++t) {
-        const int32_t k1 = lo + t, k2 = lo2 + 1 + t;
-        const int32_t u1 = k1 < hi ? __ldg(Uc + k1) : INT_MAX;
-        const int32_t u2 = (fb && k2 <= hi2) ? __ldg(Uc + k2) : INT_MAX;
-        c1 += u1 < Xa;
-        c2 += u2 <= Xb;
-    }
-}
-__device__ __forceinline__ void window_counts_n(const int32_t *Uc, int32_t D, int32_t lo,
-                                                int32_t hi, int32_t Xa, bool fb, int32_t lo2,
-                                                int32_t hi2, int32_t Xb, int32_t &c1, int32_t &c2) {
-    c1 = 0;
-    c2 = 0;
-    for (int t = 0; t < D; ++t) {
-        const int32_t k1 = lo + t, k2 = lo2 + 1 + t;
-        if (k1 < hi) c1 += __ldg(Uc + k1) < Xa;
-        if (fb && k2 <= hi2) c2 += __ldg(Uc + k2) <= Xb;
-    }
 }
 
 // rs == 1 specialisation (the hot one): identical cell logic, fewer registers.
