@@ -78,7 +78,7 @@ int prepare_device(int device) {
 }
 
 // Kernel choice per combine:
-//   kind 0: narrow tables (w1 <= LCSG_THREAD_MAX_W1, default 33): staged
+//   kind 0: narrow tables (w1 <= LCSG_THREAD_MAX_W1, default 65): staged
 //           brute-force first-wins min (lcsg_narrow.cu; LCSG_NARROW=0 selects
 //           the thread-per-row exact bisection instead)
 //   kind 2: skeleton rows (exact bisection: thread / warp / CTA per row by
@@ -272,7 +272,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     size_t o_sub = take((size_t)std::max<int64_t>(kmin, 1));
     // int32 tables of every combine node
     const int skel_stride = std::max(1, env_int("LCSG_SKELETON_STRIDE", 64));
-    const int thread_max_w1 = env_int("LCSG_THREAD_MAX_W1", 33);
+    const int thread_max_w1 = env_int("LCSG_THREAD_MAX_W1", 65);
     const int skel_thread_max = env_int("LCSG_SKEL_THREAD_MAX_W1", 65);
     const int skel_warp_max = env_int("LCSG_SKEL_WARP_MAX_W1", 257);
     // refinement mode: tiled (default) or one launch per pass ("LCSG_REFINE_PASSES=1")
@@ -1035,7 +1035,7 @@ int lcsg_combine_rows(const int32_t *upper_reach, int32_t wu1, const int32_t *up
     c.inf = inf;
     const int shift = bits_for(wu1 - 1);
     const bool key64 = bits_for(inf) + shift > 32;
-    const int thread_max_w1 = env_int("LCSG_THREAD_MAX_W1", 33);
+    const int thread_max_w1 = env_int("LCSG_THREAD_MAX_W1", 65);
     int S = 1;
     while (S * 2 <= std::max(1, env_int("LCSG_SKELETON_STRIDE", 64))) S *= 2;
     int col_block = 1;

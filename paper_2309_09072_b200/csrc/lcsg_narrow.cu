@@ -1,5 +1,5 @@
-// lcsg_narrow.cu -- the narrow combines (tables <= 33 wide: the bottom five
-// levels of a power-of-two tree, ~1/4 of a cfg5 solve in the bisection form).
+// lcsg_narrow.cu -- the narrow combines (tables <= 65 wide: the bottom six
+// levels of a power-of-two tree).
 //
 // Reference: _combine_tables (solver.py:91-110) -> combine_level / col_mins
 // (_kernel.pyx:28-82).  For a finite output cell the reference's Alg. 1 value
@@ -10,7 +10,9 @@
 // window of L rows they reach (x-1 for every finite x = U[i,k]) in shared
 // memory, then each thread folds the (w_U+1) x (w_L+1) candidates of its row
 // into registers with compile-time indices -- one LDS, one IMAD (pack) and
-// one unsigned min per candidate, no stack, no divergence.  INF cells get the
+// one unsigned min per candidate, no stack, no divergence.  For the widest
+// bucket the L window is staged per chunk of split weights k (the window of
+// all k would not fit next to the U block).  INF cells get the
 // reference's bisection artefacts: trace = `top` of the Alg. 1 node covering
 // the column (replayed from the finite traces, O(log w)), and (INF, 0) beyond
 // colhi = min(w, kmax_U + wstar_L) (_kernel.pyx:79-82).  Rows leave through a
@@ -19,39 +21,45 @@
 
 namespace lcsg {
 
-constexpr int NR_THREADS = 256;
-
 template <int P>
 struct NarrowGeom {
     static constexpr int PITCH = (P + 1) | 1;  // odd pitch: per-row reads conflict-free
+    static constexpr int NT = P <= 16 ? 256 : 128;  // threads per CTA
     // rows per thread: the per-CTA latency chain (descriptor -> U block -> L
     // window -> fold -> store) is amortised over more rows when the fold is short
     static constexpr int RPT = P <= 2 ? 4 : P == 4 ? 2 : 1;
-    static constexpr int ROWS = NR_THREADS * RPT;  // output rows per CTA
-    // dynamic shared memory: U block + L window (~ROWS + 26 P rows at sigma =
-    // 26); after the fold the whole area holds the output staging 2 x ROWS x w1
+    static constexpr int ROWS = NT * RPT;  // output rows per CTA
+    // split weights k per staged L window
+    static constexpr int KC = P <= 16 ? P + 1 : 8;
+    static constexpr int NCH = (P + 1 + KC - 1) / KC;
+    // dynamic shared memory: U block + L window (~ROWS + 26 KC rows at sigma
+    // = 26); after the fold the whole area holds the output staging 2 x ROWS x w1
     static constexpr int BYTES = P == 1 ? 32 * 1024 : P <= 4 ? 40 * 1024 : P == 8 ? 48 * 1024
                                                                                 : 72 * 1024;
     static_assert(2 * ROWS * (2 * P + 1) * 4 <= BYTES, "output staging must fit");
     static_assert((ROWS + 64) * PITCH * 4 <= BYTES, "U block + a minimal L window must fit");
 };
 
-template <typename Key>
-__device__ __forceinline__ Key npack(int32_t v, int32_t k, int shift) {
-    return ((Key)(uint32_t)v << shift) | (Key)(uint32_t)k;
+// packed key (v << shift) | k; `mul` = 1 << shift, so the 32-bit pack is one
+// IMAD with the compile-time k as addend
+__device__ __forceinline__ uint32_t npack(uint32_t v, int32_t k, int shift, uint32_t mul) {
+    return v * mul + (uint32_t)k;
+}
+__device__ __forceinline__ uint64_t npack(uint64_t v, int32_t k, int shift, uint32_t) {
+    return (v << shift) | (uint64_t)(uint32_t)k;
 }
 
 // rows [row0, row0 + nrows) of a table into shared memory at pitch PT
 // (columns >= w1 are INF).  A block of slab rows is one contiguous range of
 // the table, copied flat when w1 == PT (every power-of-two tree level).
-template <int PT>
+template <int PT, int NT>
 __device__ __forceinline__ void stage_rows(int32_t *dst, const TabAcc &t, int64_t row0,
                                            int32_t nrows, int32_t inf) {
     const int tid = threadIdx.x;
     if (t.nx) {  // leaf: (r + 1, NX[sym][r]) (breakout.py:37-55)
         const int32_t *nx = t.nx + row0;
         const bool w2 = t.w1 > 1;
-        for (int r = tid; r < nrows; r += NR_THREADS) {
+        for (int r = tid; r < nrows; r += NT) {
             int32_t *d = dst + r * PT;
             d[0] = (int32_t)(row0 + r + 1);
             if (PT > 1) d[1] = w2 ? __ldg(nx + r) : inf;
@@ -62,34 +70,43 @@ __device__ __forceinline__ void stage_rows(int32_t *dst, const TabAcc &t, int64_
         const int32_t *src = t.reach + row0 * PT;
         const int tot = nrows * PT;
         int g = tid;
-        for (; g + 3 * NR_THREADS < tot; g += 4 * NR_THREADS) {
-            const int32_t a = __ldg(src + g), b = __ldg(src + g + NR_THREADS);
-            const int32_t c2 = __ldg(src + g + 2 * NR_THREADS), e = __ldg(src + g + 3 * NR_THREADS);
+        for (; g + 3 * NT < tot; g += 4 * NT) {
+            const int32_t a = __ldg(src + g), b = __ldg(src + g + NT);
+            const int32_t c2 = __ldg(src + g + 2 * NT), e = __ldg(src + g + 3 * NT);
             dst[g] = a;
-            dst[g + NR_THREADS] = b;
-            dst[g + 2 * NR_THREADS] = c2;
-            dst[g + 3 * NR_THREADS] = e;
+            dst[g + NT] = b;
+            dst[g + 2 * NT] = c2;
+            dst[g + 3 * NT] = e;
         }
-        for (; g < tot; g += NR_THREADS) dst[g] = __ldg(src + g);
+        for (; g < tot; g += NT) dst[g] = __ldg(src + g);
     } else {
-        for (int idx = tid; idx < nrows * PT; idx += NR_THREADS) {
+        for (int idx = tid; idx < nrows * PT; idx += NT) {
             const int r = idx / PT, k = idx - r * PT;
             dst[idx] = k < t.w1 ? __ldg(t.reach + (row0 + r) * t.w1 + k) : inf;
         }
     }
 }
 
+// out-of-line copy for the chunked (widest) bucket, whose k-chunk loop is
+// unrolled: one shared body instead of one inlined copy per chunk
+template <int PT, int NT>
+__device__ __noinline__ void stage_rows_call(int32_t *dst, const TabAcc &t, int64_t row0,
+                                             int32_t nrows, int32_t inf) {
+    stage_rows<PT, NT>(dst, t, row0, nrows, inf);
+}
+
 // P: bucket >= every U and L weight (w1 - 1) of the launch
 template <int P, typename Key>
-__global__ void __launch_bounds__(NR_THREADS)
+__global__ void __launch_bounds__(NarrowGeom<P>::NT)
     narrow_combine_kernel(const CombineDesc *__restrict__ descs, Ctx c, int shift, int32_t bpd,
                           int32_t lcap) {
     using G = NarrowGeom<P>;
-    constexpr int PT = G::PITCH, RPT = G::RPT, ROWS = G::ROWS;
+    constexpr int PT = G::PITCH, RPT = G::RPT, ROWS = G::ROWS, NT = G::NT, KC = G::KC,
+                  NCH = G::NCH;
     extern __shared__ int32_t nsm[];
     int32_t *sU = nsm;               // ROWS x PT
-    int32_t *sL = nsm + ROWS * PT;   // (lcap + 1) x PT; row lcap = all INF
-    __shared__ int32_t s_xmax, s_wstar;
+    int32_t *sL = nsm + ROWS * PT;   // lcap x PT
+    __shared__ int32_t s_xmax[NCH], s_wstar;
     const int32_t di = blockIdx.x / bpd;
     const int64_t i0 = (int64_t)(blockIdx.x - di * bpd) * ROWS;
     const CombineDesc &d = descs[di];
@@ -97,22 +114,22 @@ __global__ void __launch_bounds__(NR_THREADS)
     const int nr = (int)min((int64_t)ROWS, n1 - i0);
     const int32_t inf = c.inf;
     const TabAcc U = resolve(d.U, c), L = resolve(d.L, c);
-    const int32_t wl = L.w1 - 1;
     const int tid = threadIdx.x;
-    if (tid == 0) {
-        s_xmax = 0;
-        s_wstar = -1;
-    }
+    const uint32_t mul = 1u << (shift & 31);
+    if (tid < NCH) s_xmax[tid] = 0;
+    if (tid == 0) s_wstar = -1;
     // 1. U rows of the block (columns beyond w_U are INF: no candidate)
-    stage_rows<PT>(sU, U, i0, nr, inf);
-    for (int idx = tid; idx < PT; idx += NR_THREADS) sL[lcap * PT + idx] = inf;
+    stage_rows<PT, NT>(sU, U, i0, nr, inf);
     __syncthreads();
-    // kmax_U of each row (finite prefix of the U row) and the reach of the block
+    // kmax_U of each row (finite prefix of the U row) and, per chunk of split
+    // weights, the largest finite x of the block
     int32_t ku[RPT];
-    int32_t xlast = 0;
+    int32_t xlast[NCH];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) xlast[ch] = 0;
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
-        const int r = tid + q * NR_THREADS;
+        const int r = tid + q * NT;
         ku[q] = -1;
         if (r < nr) {
 #pragma unroll
@@ -120,47 +137,66 @@ __global__ void __launch_bounds__(NR_THREADS)
                 const int32_t x = sU[r * PT + k];
                 if (x < inf) {
                     ku[q] = k;
-                    xlast = max(xlast, x);
+                    xlast[k / KC] = max(xlast[k / KC], x);
                 }
             }
         }
     }
-    xlast = __reduce_max_sync(0xffffffffu, xlast);
-    if ((tid & 31) == 0) atomicMax(&s_xmax, xlast);
-    __syncthreads();
-    // 2. the L rows every finite x of the block lands on: [base, base + nL)
-    const int64_t base = (int64_t)sU[0] - 1;  // U[i0, 0] = smallest x of the block
-    const int32_t nL = (int32_t)min((int64_t)s_xmax - base, (int64_t)lcap);
-    stage_rows<PT>(sL, L, base, nL, inf);
-    __syncthreads();
-    // 3. first-wins minimum over every candidate of each row, in registers
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) {
+        const int32_t m = __reduce_max_sync(0xffffffffu, xlast[ch]);
+        if ((tid & 31) == 0 && m > 0) atomicMax(&s_xmax[ch], m);
+    }
+    // 2./3. per chunk: the L rows its finite x land on, [base, base + nL), then
+    // the first-wins minimum over the chunk's candidates, in registers
     Key best[RPT][2 * P + 1];
 #pragma unroll
-    for (int q = 0; q < RPT; ++q) {
+    for (int q = 0; q < RPT; ++q)
 #pragma unroll
         for (int j = 0; j <= 2 * P; ++j) best[q][j] = ~(Key)0;
-        const int r = tid + q * NR_THREADS;
-        if (r < nr) {
 #pragma unroll
-            for (int k = 0; k <= P; ++k) {
-                const int32_t x = sU[r * PT + k];
-                const int64_t lr = x < inf ? (int64_t)x - 1 - base : lcap;
-                if (lr < nL || lr == lcap) {
-                    const int32_t *row = sL + lr * PT;
+    for (int ch = 0; ch < NCH; ++ch) {
+        const int k0 = ch * KC;
+        __syncthreads();  // U block / xmax ready
+        // U[i0, k0] is the smallest x of the chunk (U rows nondecreasing in i);
+        // INF there means no finite candidate in this chunk or beyond
+        const int32_t x0 = sU[k0];
+        if (x0 >= inf) break;  // CTA-uniform
+        const int64_t base = (int64_t)x0 - 1;
+        const int64_t need = (int64_t)s_xmax[ch] - base;  // L rows of the chunk
+        // usually one window; sparse matches can need several (each candidate
+        // is folded in the window holding its L row; INF candidates are
+        // skipped -- INF cells take their trace from the replay below)
+        for (int64_t w0 = 0; w0 < need; w0 += lcap) {
+            const int32_t nL = (int32_t)min(need - w0, (int64_t)lcap);
+            if (w0 > 0) __syncthreads();  // previous window consumed
+            if (NCH > 1)
+                stage_rows_call<PT, NT>(sL, L, base + w0, nL, inf);
+            else
+                stage_rows<PT, NT>(sL, L, base + w0, nL, inf);
+            __syncthreads();
 #pragma unroll
-                    for (int e = 0; e <= P; ++e) {
-                        const Key key = npack<Key>(row[e], k, shift);
-                        best[q][k + e] = key < best[q][k + e] ? key : best[q][k + e];
-                    }
-                } else {  // beyond the staged window (sparse matches): read L directly
+            for (int q = 0; q < RPT; ++q) {
+                const int r = tid + q * NT;
+                if (r < nr) {
 #pragma unroll
-                    for (int e = 0; e <= P; ++e) {
-                        const int32_t v = e <= wl ? tab_get(L, (int64_t)x - 1, e) : inf;
-                        const Key key = npack<Key>(v, k, shift);
-                        best[q][k + e] = key < best[q][k + e] ? key : best[q][k + e];
+                    for (int kk = 0; kk < KC; ++kk) {
+                        const int k = ch * KC + kk;
+                        if (k > P) break;
+                        const int32_t x = sU[r * PT + k];
+                        const int64_t lr = (int64_t)x - 1 - base - w0;
+                        if (x < inf && lr >= 0 && lr < nL) {
+                            const int32_t *row = sL + lr * PT;
+#pragma unroll
+                            for (int e = 0; e <= P; ++e) {
+                                const Key key = npack((Key)(uint32_t)row[e], k, shift, mul);
+                                best[q][k + e] = key < best[q][k + e] ? key : best[q][k + e];
+                            }
+                        }
                     }
                 }
             }
+            __syncthreads();  // window consumed (next window / chunk / staging)
         }
     }
     __syncthreads();  // sU and sL are reused as the output staging area below
@@ -171,7 +207,7 @@ __global__ void __launch_bounds__(NR_THREADS)
     int32_t wmax = -1;
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
-        const int r = tid + q * NR_THREADS;
+        const int r = tid + q * NT;
         if (r >= nr) continue;
         int32_t *rr = sR + r * w1;
         int32_t *tr = sT + r * w1;
@@ -216,10 +252,10 @@ __global__ void __launch_bounds__(NR_THREADS)
     // 4. the block's rows are one contiguous range of the output
     int32_t *gr = d.out_reach + i0 * w1;
     const int tot = nr * w1;
-    for (int idx = tid; idx < tot; idx += NR_THREADS) gr[idx] = sR[idx];
+    for (int idx = tid; idx < tot; idx += NT) gr[idx] = sR[idx];
     if (d.out_trace) {
         int32_t *gt = d.out_trace + i0 * w1;
-        for (int idx = tid; idx < tot; idx += NR_THREADS) gt[idx] = sT[idx];
+        for (int idx = tid; idx < tot; idx += NT) gt[idx] = sT[idx];
     }
     if (tid == 0 && s_wstar >= 0) atomicMax(d.out_wstar, s_wstar);
 }
@@ -227,26 +263,27 @@ __global__ void __launch_bounds__(NR_THREADS)
 template <int P, typename Key>
 static int launch_narrow_t(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift,
                            cudaStream_t s) {
-    constexpr int PT = NarrowGeom<P>::PITCH, BYTES = NarrowGeom<P>::BYTES;
+    using G = NarrowGeom<P>;
+    constexpr int PT = G::PITCH, BYTES = G::BYTES;
     cudaError_t e = cudaFuncSetAttribute(narrow_combine_kernel<P, Key>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, BYTES);
     if (e != cudaSuccess) return (int)e;
     const int64_t n1 = (int64_t)c.n + 1;
-    const int32_t bpd = (int32_t)((n1 + NarrowGeom<P>::ROWS - 1) / NarrowGeom<P>::ROWS);
+    const int32_t bpd = (int32_t)((n1 + G::ROWS - 1) / G::ROWS);
     // L window rows: whatever the budget leaves after the U block
-    const int32_t lcap = (int32_t)(BYTES / 4 - NarrowGeom<P>::ROWS * PT) / PT - 1;
+    const int32_t lcap = (int32_t)(BYTES / 4 - G::ROWS * PT) / PT;
     const int64_t blocks = (int64_t)ndesc * bpd;
     if (blocks == 0) return 0;
     if (blocks >= ((int64_t)1 << 31)) return (int)cudaErrorInvalidConfiguration;
-    narrow_combine_kernel<P, Key><<<(unsigned)blocks, NR_THREADS, BYTES, s>>>(
-        descs, c, shift, bpd, lcap);
+    narrow_combine_kernel<P, Key><<<(unsigned)blocks, G::NT, BYTES, s>>>(descs, c, shift, bpd,
+                                                                         lcap);
     return (int)cudaGetLastError();
 }
 
 int narrow_bucket(int32_t max_weight) {
     int P = 1;
     while (P < max_weight) P *= 2;
-    return P <= 16 ? P : -1;
+    return P <= 32 ? P : -1;
 }
 
 int launch_narrow(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
@@ -261,6 +298,7 @@ int launch_narrow(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, boo
         NARROW_CASE(4)
         NARROW_CASE(8)
         NARROW_CASE(16)
+        NARROW_CASE(32)
         default:
             return (int)cudaErrorInvalidValue;
     }
