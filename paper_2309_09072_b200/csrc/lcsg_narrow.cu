@@ -67,18 +67,15 @@ __device__ __forceinline__ void stage_rows(int32_t *dst, const TabAcc &t, int64_
             for (int k = 2; k < PT; ++k) d[k] = inf;
         }
     } else if (t.w1 == PT) {
+        // contiguous: asynchronous global -> shared copies (LDGSTS), all in
+        // flight at once without staging registers
         const int32_t *src = t.reach + row0 * PT;
         const int tot = nrows * PT;
-        int g = tid;
-        for (; g + 3 * NT < tot; g += 4 * NT) {
-            const int32_t a = __ldg(src + g), b = __ldg(src + g + NT);
-            const int32_t c2 = __ldg(src + g + 2 * NT), e = __ldg(src + g + 3 * NT);
-            dst[g] = a;
-            dst[g + NT] = b;
-            dst[g + 2 * NT] = c2;
-            dst[g + 3 * NT] = e;
+        for (int g = tid; g < tot; g += NT) {
+            const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + g);
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(src + g));
         }
-        for (; g < tot; g += NT) dst[g] = __ldg(src + g);
+        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
     } else {
         for (int idx = tid; idx < nrows * PT; idx += NT) {
             const int r = idx / PT, k = idx - r * PT;
