@@ -49,6 +49,18 @@ __device__ __forceinline__ uint64_t npack(uint64_t v, int32_t k, int shift, uint
     return (v << shift) | (uint64_t)(uint32_t)k;
 }
 
+__device__ __forceinline__ void cp_async4(int32_t *dst, const int32_t *src) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(src));
+}
+__device__ __forceinline__ void cp_async16(int32_t *dst, const int32_t *src) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
 // rows [row0, row0 + nrows) of a table into shared memory at pitch PT
 // (columns >= w1 are INF).  A block of slab rows is one contiguous range of
 // the table, copied flat when w1 == PT (every power-of-two tree level).
@@ -62,20 +74,31 @@ __device__ __forceinline__ void stage_rows(int32_t *dst, const TabAcc &t, int64_
         for (int r = tid; r < nrows; r += NT) {
             int32_t *d = dst + r * PT;
             d[0] = (int32_t)(row0 + r + 1);
-            if (PT > 1) d[1] = w2 ? __ldg(nx + r) : inf;
+            if (PT > 1) {
+                if (w2) cp_async4(d + 1, nx + r);
+                else d[1] = inf;
+            }
 #pragma unroll
             for (int k = 2; k < PT; ++k) d[k] = inf;
         }
+        cp_async_wait_all();
     } else if (t.w1 == PT) {
         // contiguous: asynchronous global -> shared copies (LDGSTS), all in
-        // flight at once without staging registers
+        // flight at once without staging registers; 16-byte copies for the
+        // aligned body when source and destination are congruent mod 16
         const int32_t *src = t.reach + row0 * PT;
         const int tot = nrows * PT;
-        for (int g = tid; g < tot; g += NT) {
-            const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + g);
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(src + g));
+        if ((((uintptr_t)src ^ (uintptr_t)__cvta_generic_to_shared(dst)) & 15) == 0) {
+            const int h = min(tot, (int)(((16 - ((uintptr_t)src & 15)) & 15) >> 2));
+            const int nb = (tot - h) >> 2;
+            if (tid < h) cp_async4(dst + tid, src + tid);
+            for (int c2 = tid; c2 < nb; c2 += NT) cp_async16(dst + h + 4 * c2, src + h + 4 * c2);
+            const int t0 = h + 4 * nb;
+            if (t0 + tid < tot) cp_async4(dst + t0 + tid, src + t0 + tid);
+        } else {
+            for (int g = tid; g < tot; g += NT) cp_async4(dst + g, src + g);
         }
-        asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+        cp_async_wait_all();
     } else {
         for (int idx = tid; idx < nrows * PT; idx += NT) {
             const int r = idx / PT, k = idx - r * PT;
@@ -167,10 +190,14 @@ __global__ void __launch_bounds__(NarrowGeom<P>::NT)
         for (int64_t w0 = 0; w0 < need; w0 += lcap) {
             const int32_t nL = (int32_t)min(need - w0, (int64_t)lcap);
             if (w0 > 0) __syncthreads();  // previous window consumed
+            // shift the window by 0..3 ints so that it is congruent mod 16
+            // bytes with its source rows (16-byte async copies)
+            const int sh = L.nx ? 0 : (int)(((uintptr_t)(L.reach + (base + w0) * PT) >> 2) & 3);
+            int32_t *sLw = sL + sh;
             if (NCH > 1)
-                stage_rows_call<PT, NT>(sL, L, base + w0, nL, inf);
+                stage_rows_call<PT, NT>(sLw, L, base + w0, nL, inf);
             else
-                stage_rows<PT, NT>(sL, L, base + w0, nL, inf);
+                stage_rows<PT, NT>(sLw, L, base + w0, nL, inf);
             __syncthreads();
 #pragma unroll
             for (int q = 0; q < RPT; ++q) {
@@ -183,7 +210,7 @@ __global__ void __launch_bounds__(NarrowGeom<P>::NT)
                         const int32_t x = sU[r * PT + k];
                         const int64_t lr = (int64_t)x - 1 - base - w0;
                         if (x < inf && lr >= 0 && lr < nL) {
-                            const int32_t *row = sL + lr * PT;
+                            const int32_t *row = sLw + lr * PT;
 #pragma unroll
                             for (int e = 0; e <= P; ++e) {
                                 const Key key = npack((Key)(uint32_t)row[e], k, shift, mul);
@@ -268,7 +295,7 @@ static int launch_narrow_t(const CombineDesc *descs, int32_t ndesc, Ctx c, int s
     const int64_t n1 = (int64_t)c.n + 1;
     const int32_t bpd = (int32_t)((n1 + G::ROWS - 1) / G::ROWS);
     // L window rows: whatever the budget leaves after the U block
-    const int32_t lcap = (int32_t)(BYTES / 4 - G::ROWS * PT) / PT;
+    const int32_t lcap = (int32_t)(BYTES / 4 - G::ROWS * PT - 3) / PT;  // 3: window shift
     const int64_t blocks = (int64_t)ndesc * bpd;
     if (blocks == 0) return 0;
     if (blocks >= ((int64_t)1 << 31)) return (int)cudaErrorInvalidConfiguration;
