@@ -107,6 +107,22 @@ __device__ __forceinline__ void stage_rows(int32_t *dst, const TabAcc &t, int64_
     }
 }
 
+// shared -> global copy of a contiguous block: 16-byte vectors when the
+// destination is 16-byte aligned (the staging area always is)
+template <int NT>
+__device__ __forceinline__ void copy_out(int32_t *g, const int32_t *sm, int tot) {
+    const int tid = threadIdx.x;
+    if (((uintptr_t)g & 15) == 0) {
+        const int n4 = tot >> 2;
+        for (int v = tid; v < n4; v += NT)
+            reinterpret_cast<int4 *>(g)[v] = reinterpret_cast<const int4 *>(sm)[v];
+        const int t0 = n4 << 2;
+        if (t0 + tid < tot) g[t0 + tid] = sm[t0 + tid];
+    } else {
+        for (int idx = tid; idx < tot; idx += NT) g[idx] = sm[idx];
+    }
+}
+
 // out-of-line copy for the chunked (widest) bucket, whose k-chunk loop is
 // unrolled: one shared body instead of one inlined copy per chunk
 template <int PT, int NT>
@@ -274,13 +290,9 @@ __global__ void __launch_bounds__(NarrowGeom<P>::NT)
     if ((tid & 31) == 0 && wmax >= 0) atomicMax(&s_wstar, wmax);
     __syncthreads();
     // 4. the block's rows are one contiguous range of the output
-    int32_t *gr = d.out_reach + i0 * w1;
     const int tot = nr * w1;
-    for (int idx = tid; idx < tot; idx += NT) gr[idx] = sR[idx];
-    if (d.out_trace) {
-        int32_t *gt = d.out_trace + i0 * w1;
-        for (int idx = tid; idx < tot; idx += NT) gt[idx] = sT[idx];
-    }
+    copy_out<NT>(d.out_reach + i0 * w1, sR, tot);
+    if (d.out_trace) copy_out<NT>(d.out_trace + i0 * w1, sT, tot);
     if (tid == 0 && s_wstar >= 0) atomicMax(d.out_wstar, s_wstar);
 }
 
