@@ -90,6 +90,8 @@ int env_int(const char *name, int def) {
     return v && *v ? atoi(v) : def;
 }
 
+int default_skeleton_stride(int64_t n1) { return n1 <= 8193 ? 32 : 64; }
+
 struct NodeH {
     int32_t top_row, bottom_row, w1, upper, lower, height, depth, leaf_row;
     int64_t reach_off = -1, trace_off = -1, kmax_off = -1;  // int32 element offsets
@@ -271,7 +273,10 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     size_t o_out = take((size_t)(1 + 2 * std::max<int64_t>(kmin, 1)) * 4);
     size_t o_sub = take((size_t)std::max<int64_t>(kmin, 1));
     // int32 tables of every combine node
-    const int skel_stride = std::max(1, env_int("LCSG_SKELETON_STRIDE", 64));
+    // skeleton stride: 32 rows for small column counts (the extra skeleton
+    // rows are cheaper than the latency of a coarser refinement stage), 64
+    // above (measured on cfg2/cfg3 vs cfg4/cfg5)
+    const int skel_stride = std::max(1, env_int("LCSG_SKELETON_STRIDE", default_skeleton_stride(n + 1)));
     const int thread_max_w1 = env_int("LCSG_THREAD_MAX_W1", 65);
     const int skel_thread_max = env_int("LCSG_SKEL_THREAD_MAX_W1", 65);
     const int skel_warp_max = env_int("LCSG_SKEL_WARP_MAX_W1", 257);
@@ -1037,7 +1042,7 @@ int lcsg_combine_rows(const int32_t *upper_reach, int32_t wu1, const int32_t *up
     const bool key64 = bits_for(inf) + shift > 32;
     const int thread_max_w1 = env_int("LCSG_THREAD_MAX_W1", 65);
     int S = 1;
-    while (S * 2 <= std::max(1, env_int("LCSG_SKELETON_STRIDE", 64))) S *= 2;
+    while (S * 2 <= std::max(1, env_int("LCSG_SKELETON_STRIDE", default_skeleton_stride(n1)))) S *= 2;
     int col_block = 1;
     while (col_block * 2 <= std::min(16, std::max(2, env_int("LCSG_COL_BLOCK", 8)))) col_block *= 2;
     const int P = narrow_bucket(std::max(wu1, wl1) - 1);
