@@ -269,3 +269,30 @@ def lcs(
     return LcsResult(length=L, subsequence=sub[:L].tobytes(),
                      row_positions=tuple(int(v) for v in pa[:L]),
                      col_positions=tuple(int(v) for v in pb[:L]))
+
+
+def lcs_many(
+    pairs,
+    *,
+    threads: int = 1,
+    backend=None,
+    low_memory: bool = False,
+    device=None,
+    concurrency: int = 8,
+) -> list:
+    """``[lcs(a, b) for a, b in pairs]`` with independent solves overlapped
+    on the GPU (many small pairs, e.g. the planted
+    queries of cfg4).  Each solve runs on its own CUDA stream from one of
+    ``concurrency`` host worker threads (the C-ABI call releases the GIL), so
+    small latency-bound solves share the device instead of queueing behind
+    each other.  Results are identical to the sequential calls, in order."""
+    _backend.resolve(backend)
+    items = list(pairs)
+    if concurrency <= 1 or len(items) <= 1:
+        return [lcs(a, b, threads=threads, low_memory=low_memory, device=device) for a, b in items]
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=min(concurrency, len(items))) as ex:
+        futs = [ex.submit(lcs, a, b, threads=threads, low_memory=low_memory, device=device)
+                for a, b in items]
+        return [f.result() for f in futs]

@@ -347,3 +347,17 @@ def test_narrow_window_overflow():
             assert nodes[idx].wstar == exp.wstar
         r = L.lcs(a, b)
         assert (r.length, r.subsequence, r.row_positions, r.col_positions) == O.lcs(a, b)
+
+
+def test_lcs_many_matches_sequential():
+    """Overlapped independent solves (lcs_many) return exactly the sequential
+    results, in order, for mixed sizes, alphabets and empty inputs."""
+    rng = np.random.default_rng(99)
+    pairs = [workloads.random_pair(rng, int(rng.integers(1, 300)), int(rng.integers(1, 400)),
+                                   int(rng.choice([2, 4, 26]))) for _ in range(40)]
+    pairs += [(b"", b"abc"), (b"gatttatgcagg", b"tcaggatt"), workloads.generate(1)]
+    got = L.lcs_many(pairs, concurrency=8)
+    assert got == [L.lcs(a, b) for a, b in pairs]
+    for (a, b), r in zip(pairs[:10], got[:10]):
+        assert (r.length, r.subsequence, r.row_positions, r.col_positions) == O.lcs(a, b)
+    assert L.lcs_many(pairs[:5], concurrency=1, low_memory=True) == got[:5]
