@@ -242,6 +242,11 @@ __global__ void __launch_bounds__(NarrowGeom<P>::NT)
     __syncthreads();  // sU and sL are reused as the output staging area below
     const int32_t w1 = d.w1, w = w1 - 1;
     const int32_t wstar_l = *d.L.wstar;
+    // descriptor fields in registers (stores below must not force re-loads)
+    int32_t *__restrict__ const out_kmax = d.out_kmax;
+    int32_t *__restrict__ const out_reach = d.out_reach;
+    int32_t *__restrict__ const out_trace = d.out_trace;
+    int32_t *const out_wstar = d.out_wstar;
     int32_t *sR = nsm;
     int32_t *sT = nsm + ROWS * w1;
     int32_t wmax = -1;
@@ -283,7 +288,7 @@ __global__ void __launch_bounds__(NarrowGeom<P>::NT)
             }
             tr[qq] = t;
         }
-        d.out_kmax[i0 + r] = kfin;
+        out_kmax[i0 + r] = kfin;
         wmax = max(wmax, kfin);
     }
     wmax = __reduce_max_sync(0xffffffffu, wmax);
@@ -291,9 +296,9 @@ __global__ void __launch_bounds__(NarrowGeom<P>::NT)
     __syncthreads();
     // 4. the block's rows are one contiguous range of the output
     const int tot = nr * w1;
-    copy_out<NT>(d.out_reach + i0 * w1, sR, tot);
-    if (d.out_trace) copy_out<NT>(d.out_trace + i0 * w1, sT, tot);
-    if (tid == 0 && s_wstar >= 0) atomicMax(d.out_wstar, s_wstar);
+    copy_out<NT>(out_reach + i0 * w1, sR, tot);
+    if (out_trace) copy_out<NT>(out_trace + i0 * w1, sT, tot);
+    if (tid == 0 && s_wstar >= 0) atomicMax(out_wstar, s_wstar);
 }
 
 template <int P, typename Key>

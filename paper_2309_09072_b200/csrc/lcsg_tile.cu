@@ -134,14 +134,18 @@ __global__ void __launch_bounds__(CR_THREADS)
     const int32_t *__restrict__ Lr = d.L.reach;
     const int32_t uw1 = d.U.w1, lw1 = d.L.w1, wl = lw1 - 1;
     const int32_t w1 = d.w1;
+    // output pointers in registers: stores through them must not force
+    // re-loads of the descriptor (which lives in global memory)
+    int32_t *__restrict__ const out_reach = d.out_reach;
+    int32_t *__restrict__ const out_trace = d.out_trace;
 
     {
         int32_t r0v = inf, r0t = 0, rbv = inf, rbt = 0;
         if (active && rb >= 2) {
-            r0v = __ldg(d.out_reach + i0 * w1 + j);
-            r0t = __ldg(d.out_trace + i0 * w1 + j);
-            rbv = __ldg(d.out_reach + ibot * w1 + j);
-            rbt = __ldg(d.out_trace + ibot * w1 + j);
+            r0v = __ldg(out_reach + i0 * w1 + j);
+            r0t = __ldg(out_trace + i0 * w1 + j);
+            rbv = __ldg(out_reach + ibot * w1 + j);
+            rbt = __ldg(out_trace + ibot * w1 + j);
         }
         sR[0] = r0v;
         sT[0] = r0t;
@@ -255,8 +259,8 @@ __global__ void __launch_bounds__(CR_THREADS)
         const int32_t v = sR[r * CR_THREADS];
         if (active && r < rb) {
             const int64_t off = (i0 + (int64_t)r * rs) * w1 + j;
-            d.out_reach[off] = v;
-            if (v < inf) d.out_trace[off] = sT[r * CR_THREADS];
+            out_reach[off] = v;
+            if (v < inf) out_trace[off] = sT[r * CR_THREADS];
         }
     }
 }
@@ -302,14 +306,18 @@ __global__ void __launch_bounds__(CR_THREADS)
     const int32_t *__restrict__ Lr = d.L.reach;
     const int32_t uw1 = d.U.w1, lw1 = d.L.w1, wl = lw1 - 1;
     const int32_t w1 = d.w1;
+    // output pointers in registers: stores through them must not force
+    // re-loads of the descriptor (which lives in global memory)
+    int32_t *__restrict__ const out_reach = d.out_reach;
+    int32_t *__restrict__ const out_trace = d.out_trace;
 
     {
         int32_t r0v = inf, r0t = 0, rbv = inf, rbt = 0;
         if (active && rb >= 2) {
-            r0v = __ldg(d.out_reach + i0 * w1 + j);
-            r0t = __ldg(d.out_trace + i0 * w1 + j);
-            rbv = __ldg(d.out_reach + (i0 + rb) * w1 + j);
-            rbt = __ldg(d.out_trace + (i0 + rb) * w1 + j);
+            r0v = __ldg(out_reach + i0 * w1 + j);
+            r0t = __ldg(out_trace + i0 * w1 + j);
+            rbv = __ldg(out_reach + (i0 + rb) * w1 + j);
+            rbt = __ldg(out_trace + (i0 + rb) * w1 + j);
         }
         sR[0] = r0v;
         sT[0] = r0t;
@@ -437,8 +445,8 @@ __global__ void __launch_bounds__(CR_THREADS)
         const int32_t v = sR[r * CR_THREADS];
         if (active && r < rb) {
             const int64_t off = (i0 + r) * w1 + j;
-            d.out_reach[off] = v;
-            if (v < inf) d.out_trace[off] = sT[r * CR_THREADS];
+            out_reach[off] = v;
+            if (v < inf) out_trace[off] = sT[r * CR_THREADS];
         }
     }
 }
@@ -468,14 +476,18 @@ __global__ void __launch_bounds__(32 * FN_WARPS)
     const TabAcc U = resolve(d.U, c);
     const int32_t w = d.w1 - 1;
     const int32_t wstarL = *d.L.wstar;
+    int32_t *__restrict__ const out_reach = d.out_reach;
+    int32_t *__restrict__ const out_trace = d.out_trace;
+    int32_t *__restrict__ const out_kmax = d.out_kmax;
+    const int32_t w1 = d.w1;
     // phase 1: lane = row
     const int64_t i = r0 + lane;
     const bool act = lane < rpw && i < n1 - 1 && (i & (S - 1)) != 0;  // S: power of two
     int32_t K = -1, colhi = -1, kmax_warp = -1;
     if (act) {
         colhi = min(w, tab_kmax(U, i, inf) + wstarL);
-        const int32_t *reach = d.out_reach + i * d.w1;
-        const int32_t *trace = d.out_trace + i * d.w1;
+        const int32_t *reach = out_reach + i * w1;
+        const int32_t *trace = out_trace + i * w1;
         // the replay of Alg. 1's bisection over [0, colhi] IS a binary search
         // for the end of the row's finite prefix: finite mids go right, INF
         // mids are the INF nodes (their segments) and go left; K = left - 1
@@ -495,7 +507,7 @@ __global__ void __launch_bounds__(32 * FN_WARPS)
             }
         }
         K = left - 1;
-        d.out_kmax[i] = K;
+        out_kmax[i] = K;
         for (int s = 0; s < ns; ++s) {  // resolve tops (independent loads)
             const int32_t f = seg_all[wid][lane][s].y;
             seg_all[wid][lane][s].y = f >= 0 ? __ldg(trace + f) : 0;
@@ -515,7 +527,7 @@ __global__ void __launch_bounds__(32 * FN_WARPS)
         const int32_t ch = __shfl_sync(0xffffffffu, colhi, rr);
         const int ns = nseg_all[wid][rr];
         const int2 *sg = seg_all[wid][rr];
-        int32_t *trace = d.out_trace + (r0 + rr) * d.w1;
+        int32_t *trace = out_trace + (r0 + rr) * w1;
         for (int32_t q = max(ch, Kr) + 1 + lane; q <= w; q += 32) trace[q] = 0;
         int32_t hi = ch;
         for (int sgi = 0; sgi < ns; ++sgi) {
