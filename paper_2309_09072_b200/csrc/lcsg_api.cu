@@ -417,6 +417,8 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
                 if (kind == 0 && P > 0 && narrow_on) {
                     L.kind = 10;
                     L.stride_or_delta = P;
+                    // height 1: both children are leaves
+                    if (h == 1 && env_int("LCSG_LEAFPAIR", 1)) L.kind = 11;
                 }
                 t->plan.push_back(L);
                 continue;
@@ -543,6 +545,8 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             BCKL(launch_combine_staged(dd, L.count, c, L.shift, L.key64, s));
         else if (L.kind == 10)
             BCKL(launch_narrow(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s));
+        else if (L.kind == 11)
+            BCKL(launch_narrow_leafpair(dd, L.count, c, L.shift, L.key64, s));
         else if (L.kind == 3)
             BCKL(launch_skeleton(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s));
         else if (L.kind == 5 || L.kind == 6)

@@ -119,6 +119,9 @@ int launch_combine_staged(const CombineDesc *descs, int32_t ndesc, Ctx c, int ke
 // narrow combines (every U and L weight <= P, P in 1,2,4,8,16; lcsg_narrow.cu):
 // staged brute-force first-wins minimum, all rows
 int narrow_bucket(int32_t max_weight);  // P, or -1 when too wide
+// height-1 combines (both children leaves): direct NX reads, no staging
+int launch_narrow_leafpair(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
+                           cudaStream_t s);
 int launch_narrow(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
                   int32_t P, cudaStream_t s);
 // skeleton rows 0, S, 2S, ..., n by exact Alg. 1 (one CTA per row)

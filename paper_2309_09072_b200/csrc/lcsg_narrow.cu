@@ -301,6 +301,109 @@ __global__ void __launch_bounds__(NarrowGeom<P>::NT)
     if (tid == 0 && s_wstar >= 0) atomicMax(out_wstar, s_wstar);
 }
 
+// Height-1 combines (two leaf children, rows of 3 cells): the fold needs only
+// NX_a[i], NX_b[i] and NX_b[NX_a[i] - 1] (breakout.py:37-55 leaf rows), all in
+// L2 (26 symbols x (n+1) ints), so nothing is staged on the way in; rows
+// still leave through the shared-memory transpose.  Same first-wins values,
+// traces and INF replay as narrow_combine_kernel<1>.
+constexpr int LP_NT = 256, LP_RPT = 4, LP_ROWS = LP_NT * LP_RPT;
+
+template <typename Key>
+__global__ void __launch_bounds__(LP_NT)
+    narrow_leafpair_kernel(const CombineDesc *__restrict__ descs, Ctx c, int shift, int32_t bpd) {
+    __shared__ int32_t sR[LP_ROWS * 3], sT[LP_ROWS * 3];
+    __shared__ int32_t s_wstar;
+    const int32_t di = blockIdx.x / bpd;
+    const int64_t i0 = (int64_t)(blockIdx.x - di * bpd) * LP_ROWS;
+    const CombineDesc &d = descs[di];
+    const int64_t n1 = (int64_t)c.n + 1;
+    const int nr = (int)min((int64_t)LP_ROWS, n1 - i0);
+    const int32_t inf = c.inf;
+    const TabAcc U = resolve(d.U, c), L = resolve(d.L, c);  // both leaves
+    const int32_t w1 = d.w1, w = w1 - 1;
+    const int32_t wstar_l = *d.L.wstar;
+    int32_t *__restrict__ const out_kmax = d.out_kmax;
+    int32_t *__restrict__ const out_reach = d.out_reach;
+    int32_t *__restrict__ const out_trace = d.out_trace;
+    const uint32_t mul = 1u << (shift & 31);
+    const int tid = threadIdx.x;
+    if (tid == 0) s_wstar = -1;
+    int32_t wmax = -1;
+#pragma unroll
+    for (int q = 0; q < LP_RPT; ++q) {
+        const int r = tid + q * LP_NT;
+        if (r >= nr) continue;
+        const int64_t i = i0 + r;
+        // U row (i+1, NX_a[i]); L row x-1: (x, NX_b[x-1])
+        const int32_t xa = U.w1 > 1 ? __ldg(U.nx + i) : inf;
+        const int32_t nb = L.w1 > 1 ? __ldg(L.nx + i) : inf;
+        const int32_t nb2 = (xa < inf && L.w1 > 1) ? __ldg(L.nx + (xa - 1)) : inf;
+        // candidates (k, e): j = k + e; first-wins min of packed keys
+        Key best[3];
+        best[0] = npack((Key)(uint32_t)(i + 1), 0, shift, mul);  // (0,0): L[i][0] = i+1
+        const Key k01 = npack((Key)(uint32_t)nb, 0, shift, mul);           // (0,1): L[i][1]
+        const Key k10 = npack((Key)(uint32_t)(xa < inf ? xa : inf), 1, shift, mul);  // (1,0)
+        best[1] = k01 < k10 ? k01 : k10;
+        best[2] = npack((Key)(uint32_t)nb2, 1, shift, mul);              // (1,1)
+        const int32_t ku = xa < inf ? 1 : 0;
+        int32_t kfin = -1;
+        int32_t *rr = sR + r * w1;
+        int32_t *tr = sT + r * w1;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            if (j <= w) {
+                const int32_t v = (int32_t)(best[j] >> shift);
+                if (v < inf) kfin = j;
+                rr[j] = v < inf ? v : inf;
+                tr[j] = (int32_t)(best[j] & (((Key)1 << shift) - 1));
+            }
+        }
+        const int32_t colhi = min(w, ku + wstar_l);
+        for (int32_t qq = kfin + 1; qq <= w; ++qq) {  // Alg. 1 replay for INF cells
+            int32_t t = 0;
+            if (qq <= colhi) {
+                int32_t left = 0, right = colhi, top = 0;
+                for (;;) {
+                    const int32_t mid = (left + right + 1) >> 1;
+                    if (mid <= kfin) {
+                        top = tr[mid];
+                        left = mid + 1;
+                    } else if (qq >= mid) {
+                        break;
+                    } else {
+                        right = mid - 1;
+                    }
+                }
+                t = top;
+            }
+            tr[qq] = t;
+        }
+        out_kmax[i] = kfin;
+        wmax = max(wmax, kfin);
+    }
+    wmax = __reduce_max_sync(0xffffffffu, wmax);
+    if ((tid & 31) == 0 && wmax >= 0) atomicMax(&s_wstar, wmax);
+    __syncthreads();
+    const int tot = nr * w1;
+    copy_out<LP_NT>(out_reach + i0 * w1, sR, tot);
+    if (out_trace) copy_out<LP_NT>(out_trace + i0 * w1, sT, tot);
+    if (tid == 0 && s_wstar >= 0) atomicMax(d.out_wstar, s_wstar);
+}
+
+int launch_narrow_leafpair(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
+                           cudaStream_t s) {
+    const int64_t n1 = (int64_t)c.n + 1;
+    const int32_t bpd = (int32_t)((n1 + LP_ROWS - 1) / LP_ROWS);
+    const int64_t blocks = (int64_t)ndesc * bpd;
+    if (blocks == 0) return 0;
+    if (blocks >= ((int64_t)1 << 31)) return (int)cudaErrorInvalidConfiguration;
+    if (key64)
+        narrow_leafpair_kernel<uint64_t><<<(unsigned)blocks, LP_NT, 0, s>>>(descs, c, shift, bpd);
+    else
+        narrow_leafpair_kernel<uint32_t><<<(unsigned)blocks, LP_NT, 0, s>>>(descs, c, shift, bpd);
+    return (int)cudaGetLastError();
+}
+
 template <int P, typename Key>
 static int launch_narrow_t(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift,
                            cudaStream_t s) {

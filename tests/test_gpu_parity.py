@@ -299,6 +299,7 @@ def test_skeleton_refine_strides(stride, monkeypatch):
     {"LCSG_SKEL_THREAD_MAX_W1": "1", "LCSG_SKEL_WARP_MAX_W1": "1"},  # CTA kernel for every skeleton row
     {"LCSG_NARROW": "0"},                                   # bisection kernel for the narrow tables
     {"LCSG_THREAD_MAX_W1": "33"},                           # 65-wide tables through the column path
+    {"LCSG_LEAFPAIR": "0"},                                 # height-1 combines through the staged kernel
     {"LCSG_NARROW": "0", "LCSG_THREAD_MAX_W1": "65"},
 ])
 def test_refinement_variants(env, monkeypatch):
