@@ -303,9 +303,12 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
         if (nd.kind == 2 && n1 * (int64_t)nd.w1 >= ((int64_t)1 << 32)) nd.kind = 1;
         (void)wu1;
         if (skel_stride == 1 && nd.kind == 2) nd.kind = 1;
+        // every table starts on a 128-byte boundary (vector / async copies)
+        tab_elems = (tab_elems + 31) / 32 * 32;
         nd.reach_off = tab_elems;
         tab_elems += n1 * nd.w1;
         if (t->with_trace) {
+            tab_elems = (tab_elems + 31) / 32 * 32;
             nd.trace_off = tab_elems;
             tab_elems += n1 * nd.w1;
         }
@@ -324,11 +327,13 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     if (!t->with_trace) {
         for (auto &nd : t->nodes)
             if (nd.upper >= 0 && nd.kind == 2) {
+                level_scratch[nd.height] = (level_scratch[nd.height] + 31) / 32 * 32;
                 nd.trace_off = level_scratch[nd.height];  // relative to the scratch base
                 level_scratch[nd.height] += n1 * nd.w1;
             }
         for (int64_t v : level_scratch) scratch_elems = std::max(scratch_elems, v);
     }
+    tab_elems = (tab_elems + 31) / 32 * 32;
     const int64_t scratch_base = tab_elems;
     tab_elems += scratch_elems;
     off = align_up(o_tab + (size_t)tab_elems * 4);
