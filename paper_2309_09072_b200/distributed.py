@@ -191,6 +191,29 @@ def _bcast(dist, group, t, src):
         dist.broadcast(t, src=src, group=group)
 
 
+def _bcast_finite_rows(dist, group, table, kmax_rows, src, inf):
+    """Broadcast rows of a reach table by their finite prefixes only.
+
+    Row i holds finite values in columns 0..kmax[i] and INF beyond, so only
+    those prefixes travel (about a third of a sigma=26 top-level table,
+    SURVEY.md 8(e)); every rank already has ``kmax_rows``, so payload sizes
+    need no exchange.  Receivers rebuild the rows with INF fill."""
+    import torch
+
+    if table.numel() == 0:
+        return
+    cols = torch.arange(table.shape[1], device=table.device, dtype=kmax_rows.dtype)
+    mask = cols[None, :] <= kmax_rows[:, None]
+    if dist.get_rank(group) == src:
+        payload = table[mask]
+    else:
+        payload = torch.empty(int(mask.sum().item()), dtype=table.dtype, device=table.device)
+    _bcast(dist, group, payload, src)
+    if dist.get_rank(group) != src:
+        table.fill_(inf)
+        table[mask] = payload
+
+
 def _allreduce_max(dist, group, t):
     from torch.distributed import ReduceOp
 
@@ -203,10 +226,12 @@ def _allreduce_max(dist, group, t):
 
 
 def solve_sharded(rows: bytes, cols: bytes, dist, group=None, backend=None, with_trace=True):
-    """Sharded build of the full-grid tree: returns (root, bands, backend).
+    """Sharded build of the full-grid tree: returns (root, bands, upper).
 
-    Every rank ends with the full tables of all upper nodes (root included)
-    and of all band roots; band subtrees stay on their owner ranks."""
+    Every rank ends with the full reach/kmax tables of all band roots and of
+    all upper nodes below the root; the root's rows (and every upper node's
+    traces) stay with their row owners (``table["spans"]``), band subtrees on
+    their owner ranks."""
     import torch
 
     rank, P = dist.get_rank(group), dist.get_world_size(group)
@@ -225,8 +250,8 @@ def solve_sharded(rows: bytes, cols: bytes, dist, group=None, backend=None, with
     backend.synchronize()
     for b in bands:
         owner = b.band % P
-        _bcast(dist, group, b.table["reach"], owner)
         _bcast(dist, group, b.table["kmax"], owner)
+        _bcast_finite_rows(dist, group, b.table["reach"], b.table["kmax"], owner, inf)
         ws = torch.tensor([b.table["wstar"]], dtype=torch.int32, device=b.table["reach"].device)
         _bcast(dist, group, ws, owner)
         b.table["wstar"] = int(ws.item())
@@ -243,10 +268,17 @@ def solve_sharded(rows: bytes, cols: bytes, dist, group=None, backend=None, with
         backend.combine_rows(U, L, out, lo, hi, inf)
         backend.synchronize()
         # reach/kmax row ranges go to every rank (the next level reads them as
-        # U and L); traces stay with their row owner (the walk fetches one cell)
-        for r, (a, b) in enumerate(spans):
-            for key in ("reach", "kmax"):
-                _bcast(dist, group, out[key][a:b], r)
+        # U and L; finite prefixes only); traces stay with their row owner
+        # (the walk fetches one cell).  The root feeds no further combine: its
+        # rows stay with their owners, only its start-column-1 kmax (the LCS
+        # length) is shared
+        if nd is not root:
+            for r, (a, b) in enumerate(spans):
+                _bcast(dist, group, out["kmax"][a:b], r)
+                _bcast_finite_rows(dist, group, out["reach"][a:b], out["kmax"][a:b], r, inf)
+        else:
+            r0 = next(r for r, (a, b) in enumerate(spans) if a <= 0 < b)
+            _bcast(dist, group, out["kmax"][0:1], r0)
         _allreduce_max(dist, group, out["wstar_dev"])
         out["wstar"] = int(out["wstar_dev"].item())
         out["spans"] = spans
@@ -286,7 +318,12 @@ def recover_sharded(root: Node, bands: List[Node], m: int, dist, group=None, bac
     for plist in gathered:
         for top, seg in plist:
             cols[top - 1: top - 1 + len(seg)] = seg
-    cols[m] = int(R["reach"][0, length].item())
+    # the path's end column: root cell (start column 1, weight length), held by
+    # the owner of row 0 (root rows are not replicated)
+    r0 = next(r for r, (a, b) in enumerate(R["spans"]) if a <= 0 < b)
+    end = R["reach"][0, length].reshape(1).clone()
+    _bcast(dist, group, end, r0)
+    cols[m] = int(end.item())
     return length, cols
 
 

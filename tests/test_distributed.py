@@ -84,6 +84,15 @@ class OracleBackend:
         pass
 
 
+def _node_id(tree, nd):
+    """Oracle node id of the plan node covering vertex rows [top, bottom)."""
+    for idx in range(len(tree)):
+        o = tree.node(idx)
+        if o.top_row == nd.top and o.bottom_row == nd.bottom:
+            return idx
+    raise KeyError((nd.top, nd.bottom))
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -116,11 +125,17 @@ def _cpu_worker(rank, world, port, seed, count):
             root, bands, upper = D.solve_sharded(rows, cols, dist, None, be)
             t = O.OracleTree(rows, cols)
             ref = t.node(t.root)
-            np.testing.assert_array_equal(root.table["reach"].numpy(), ref.reach)
-            lo, hi = root.table["spans"][rank]  # traces stay with their row owner
+            lo, hi = root.table["spans"][rank]  # root rows stay with their owner
+            np.testing.assert_array_equal(root.table["reach"].numpy()[lo:hi], ref.reach[lo:hi])
             np.testing.assert_array_equal(root.table["trace"].numpy()[lo:hi], ref.trace[lo:hi])
-            np.testing.assert_array_equal(root.table["kmax"].numpy(), ref.kmax)
+            np.testing.assert_array_equal(root.table["kmax"].numpy()[lo:hi], ref.kmax[lo:hi])
+            assert int(root.table["kmax"][0]) == int(ref.kmax[0])
             assert root.table["wstar"] == ref.wstar
+            # every table below the root is fully replicated (finite-prefix broadcasts)
+            for nd in list(bands) + [u for u in upper if u is not root]:
+                exp = t.node(_node_id(t, nd))
+                np.testing.assert_array_equal(np.asarray(nd.table["reach"]), exp.reach)
+                np.testing.assert_array_equal(np.asarray(nd.table["kmax"]), exp.kmax)
     finally:
         dist.destroy_process_group()
 
@@ -162,8 +177,8 @@ def _gpu_worker(rank, world, port, seed, count):
         be = D.CudaBackend(0)
         root, bands, upper = D.solve_sharded(rows, cols, dist, None, be)
         tab = L.build_cost_table(L.GridModel(rows, cols), 1, len(rows) + 1)
-        np.testing.assert_array_equal(root.table["reach"].cpu().numpy(), tab.reach)
         lo, hi = root.table["spans"][rank]
+        np.testing.assert_array_equal(root.table["reach"].cpu().numpy()[lo:hi], tab.reach[lo:hi])
         np.testing.assert_array_equal(root.table["trace"].cpu().numpy()[lo:hi], tab.trace[lo:hi])
         be.free()
         del rng
