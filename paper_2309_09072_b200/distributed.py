@@ -29,7 +29,7 @@ from __future__ import annotations
 
 import ctypes
 from dataclasses import dataclass, field
-from typing import List, Optional
+from typing import Dict, Tuple, List, Optional
 
 import numpy as np
 
@@ -204,12 +204,13 @@ def _bcast_finite_rows(dist, group, table, kmax_rows, src, inf):
         return
     cols = torch.arange(table.shape[1], device=table.device, dtype=kmax_rows.dtype)
     mask = cols[None, :] <= kmax_rows[:, None]
-    if dist.get_rank(group) == src:
+    me = dist.get_rank()  # global rank: src is a global rank (subgroups too)
+    if me == src:
         payload = table[mask]
     else:
         payload = torch.empty(int(mask.sum().item()), dtype=table.dtype, device=table.device)
     _bcast(dist, group, payload, src)
-    if dist.get_rank(group) != src:
+    if me != src:
         table.fill_(inf)
         table[mask] = payload
 
@@ -225,88 +226,181 @@ def _allreduce_max(dist, group, t):
         dist.all_reduce(t, op=ReduceOp.MAX, group=group)
 
 
-def solve_sharded(rows: bytes, cols: bytes, dist, group=None, backend=None, with_trace=True):
-    """Sharded build of the full-grid tree: returns (root, bands, upper).
+_SUBGROUPS: Dict[Tuple[int, Tuple[int, ...]], object] = {}
 
-    Every rank ends with the full reach/kmax tables of all band roots and of
-    all upper nodes below the root; the root's rows (and every upper node's
-    traces) stay with their row owners (``table["spans"]``), band subtrees on
-    their owner ranks."""
+
+def _subgroup(dist, parent, ranks: Tuple[int, ...]):
+    """Process group of a subtree's (global) ranks, created once per parent
+    group and rank set: every rank asks for the same sets in the same order,
+    so creation stays collective while repeated solves reuse communicators."""
+    key = (id(parent), ranks)
+    g = _SUBGROUPS.get(key)
+    if g is None:
+        g = dist.new_group(list(ranks))
+        _SUBGROUPS[key] = g
+    return g
+
+
+def _rank_sets(root: Node, P: int) -> Dict[int, Tuple[int, ...]]:
+    """Ranks that compute each node: a band its owner (band % P), an upper
+    node the union of its children's ranks (the ranks of its subtree)."""
+    rs: Dict[int, Tuple[int, ...]] = {}
+
+    def f(nd):
+        if nd.band >= 0:
+            key = (nd.band % P,)
+        else:
+            key = tuple(sorted(set(f(nd.upper)) | set(f(nd.lower))))
+        rs[id(nd)] = key
+        return key
+
+    f(root)
+    return rs
+
+
+def _replicate(dist, G, rank, ch: Node, ch_ranks, backend, n, inf):
+    """Make child table ``ch`` (reach, kmax, wstar) complete on every rank of
+    the parent's group ``G``: a band from its owner, an upper node from the
+    owners of its row ranges (spans first, so that every member knows them);
+    rows travel as finite prefixes."""
+    import torch
+
+    n1 = n + 1
+    w1 = min(ch.rows, n) + 1
+    if ch.band >= 0:
+        spans = [(ch_ranks[0], 0, n1)]  # a band's rank set is its owner
+    else:
+        meta = backend.empty((3 * len(ch_ranks),))
+        if ch.table is not None and "spans" in ch.table:
+            meta.copy_(torch.tensor([v for sp in ch.table["spans"] for v in sp], dtype=meta.dtype))
+        _bcast(dist, G, meta, ch_ranks[0])
+        mh = meta.cpu().tolist()
+        spans = [tuple(int(v) for v in mh[3 * t: 3 * t + 3]) for t in range(len(ch_ranks))]
+    if ch.table is None:
+        ch.table = {"handle": None}
+    T = ch.table
+    if "reach" not in T or T["reach"] is None:
+        T["reach"] = backend.empty((n1, w1))
+        T["kmax"] = backend.empty((n1,))
+    # every member takes part (each child is replicated once, for its parent);
+    # the owners of row ranges send, the others receive
+    for owner, lo, hi in spans:
+        _bcast(dist, G, T["kmax"][lo:hi], owner)
+        _bcast_finite_rows(dist, G, T["reach"][lo:hi], T["kmax"][lo:hi], owner, inf)
+    ws = torch.tensor([int(T.get("wstar", 0))], dtype=torch.int32, device=T["reach"].device)
+    _bcast(dist, G, ws, spans[0][0])
+    T["wstar"] = int(ws.item())
+    T["reach_full"] = True
+    T["spans"] = spans
+
+
+def solve_sharded(rows: bytes, cols: bytes, dist, group=None, backend=None, with_trace=True):
+    """Sharded build of the full-grid tree: returns (root, bands, upper, ctx).
+
+    Bands are built by their owners with no communication.  Each upper
+    combine is computed by the ranks of its own subtree (pairs, quads, ...,
+    all ranks at the root), sharded over start columns; before it, the two
+    children tables are replicated within that subtree's process group only
+    (finite row prefixes), so a rank receives its sibling subtrees' tables,
+    not every table of the level.  Traces and the root's rows stay with
+    their row owners (``table["spans"]`` = (rank, lo, hi))."""
     import torch
 
     rank, P = dist.get_rank(group), dist.get_world_size(group)
     m, n = len(rows), len(cols)
     n1, inf = n + 1, n + 2
     root, bands, upper = build_plan(m, P)
+    rs = _rank_sets(root, P)
+    glob = (lambda r: r) if group is None else (lambda r: dist.get_global_rank(group, r))
+    groups: Dict[Tuple[int, ...], object] = {}
+    for nd in upper:  # collective: same order on every rank
+        key = rs[id(nd)]
+        if key not in groups:
+            groups[key] = group if len(key) == P else _subgroup(dist, group, tuple(glob(r) for r in key))
     # 1. bands: independent subtrees, zero communication
     for b in bands:
-        w1 = min(b.rows, n) + 1
         if b.band % P == rank:
             h, reach, kmax, ws = backend.build_band(rows, cols, b.top, b.bottom, with_trace)
-            b.table = {"handle": h, "reach": reach, "kmax": kmax, "wstar": ws}
+            b.table = {"handle": h, "reach": reach, "kmax": kmax, "wstar": ws,
+                       "reach_full": True, "handle_owner": rank}
         else:
-            b.table = {"handle": None, "reach": backend.empty((n1, w1)),
-                       "kmax": backend.empty((n1,)), "wstar": 0}
+            b.table = None
     backend.synchronize()
-    for b in bands:
-        owner = b.band % P
-        _bcast(dist, group, b.table["kmax"], owner)
-        _bcast_finite_rows(dist, group, b.table["reach"], b.table["kmax"], owner, inf)
-        ws = torch.tensor([b.table["wstar"]], dtype=torch.int32, device=b.table["reach"].device)
-        _bcast(dist, group, ws, owner)
-        b.table["wstar"] = int(ws.item())
-    # 2. upper levels, bottom-up: each combine sharded over start columns
+    # 2. upper combines, bottom-up, each within its subtree's group
     for nd in upper:
+        key = rs[id(nd)]
+        if rank not in key:
+            nd.table = None
+            continue
+        G = groups[key]
+        for ch in (nd.upper, nd.lower):
+            _replicate(dist, G, rank, ch, [glob(r) for r in rs[id(ch)]], backend, n, inf)
         U, L = nd.upper.table, nd.lower.table
         w1 = min(nd.rows, n) + 1
         out = {"reach": backend.empty((n1, w1)), "trace": backend.empty((n1, w1)),
                "kmax": backend.empty((n1,)), "wstar_dev": backend.empty((1,))}
         out["wstar_dev"].zero_()
         weights = U["kmax"].cpu().numpy().astype(np.int64) + 1
-        spans = split_rows(weights, P)
-        lo, hi = spans[rank]
+        spans = split_rows(weights, len(key))
+        lo, hi = spans[key.index(rank)]
         backend.combine_rows(U, L, out, lo, hi, inf)
         backend.synchronize()
-        # reach/kmax row ranges go to every rank (the next level reads them as
-        # U and L; finite prefixes only); traces stay with their row owner
-        # (the walk fetches one cell).  The root feeds no further combine: its
-        # rows stay with their owners, only its start-column-1 kmax (the LCS
-        # length) is shared
-        if nd is not root:
-            for r, (a, b) in enumerate(spans):
-                _bcast(dist, group, out["kmax"][a:b], r)
-                _bcast_finite_rows(dist, group, out["reach"][a:b], out["kmax"][a:b], r, inf)
-        else:
-            r0 = next(r for r, (a, b) in enumerate(spans) if a <= 0 < b)
-            _bcast(dist, group, out["kmax"][0:1], r0)
-        _allreduce_max(dist, group, out["wstar_dev"])
+        _allreduce_max(dist, G, out["wstar_dev"])
         out["wstar"] = int(out["wstar_dev"].item())
-        out["spans"] = spans
+        out["spans"] = [(glob(key[t]), a, b) for t, (a, b) in enumerate(spans)]
         nd.table = out
-    return root, bands, upper
+    ctx = {"rs": rs, "groups": groups, "glob": glob, "group": group}
+    return root, bands, upper, ctx
 
 
-def recover_sharded(root: Node, bands: List[Node], m: int, dist, group=None, backend=None):
+def recover_sharded(root: Node, bands: List[Node], m: int, dist, group=None, backend=None,
+                    ctx=None):
     """Cross-vertex columns of the LCS path (solver.py:180-207), stitched from
-    the upper-level walk (every rank) and the band walks (owners)."""
+    the upper-level walk and the band walks.  Each rank walks only the path
+    towards its own band: at a node, the owner of the trace row broadcasts
+    (k, x) within the node's group; then every member follows the child
+    whose subtree holds it."""
+    import torch
+
     rank, P = dist.get_rank(group), dist.get_world_size(group)
+    rs, groups, glob = ctx["rs"], ctx["groups"], ctx["glob"]
+    grank = glob(rank)
     R = root.table
-    length = int(R["kmax"][0].item())
+    # row 0 of the root (LCS length, path end) lives on the first rank of the
+    # root's rank set (the first span is never empty); ranks outside the plan
+    # (more ranks than bands) hold nothing and only receive
+    r0 = glob(rs[id(root)][0])
+    head = backend.empty((1,))
+    if R is not None and grank == r0:
+        head.copy_(R["kmax"][0:1])
+    _bcast(dist, group, head, r0)
+    length = int(head.item())
     start = {}  # band -> (i, j)
+
+    def owner_of(nd, row):
+        return next(r for r, a, b in nd.table["spans"] if a <= row < b)
 
     def walk(nd, i, jj):
         if nd.band >= 0:
             start[nd.band] = (i, jj)
             return
-        owner = next(r for r, (a, b) in enumerate(nd.table["spans"]) if a <= i - 1 < b)
-        kt = nd.table["trace"][i - 1, jj].reshape(1).clone()
-        _bcast(dist, group, kt, owner)
-        k = int(kt.item())
-        x = int(nd.upper.table["reach"][i - 1, k].item())
-        walk(nd.upper, i, k)
-        walk(nd.lower, x, jj - k)
+        G = groups[rs[id(nd)]]
+        owner = owner_of(nd, i - 1)
+        dev = nd.table["reach"].device
+        kx = torch.zeros(2, dtype=torch.int32, device=dev)
+        if grank == owner:
+            k = int(nd.table["trace"][i - 1, jj].item())
+            kx[0] = k
+            kx[1] = int(nd.upper.table["reach"][i - 1, k].item())
+        _bcast(dist, G, kx, owner)
+        k, x = int(kx[0].item()), int(kx[1].item())
+        if rank in rs[id(nd.upper)]:
+            walk(nd.upper, i, k)
+        if rank in rs[id(nd.lower)]:
+            walk(nd.lower, x, jj - k)
 
-    walk(root, 1, length)
+    if rank in rs[id(root)]:
+        walk(root, 1, length)
     cols = np.zeros(m + 1, dtype=np.int32)
     pieces = []
     for b in bands:
@@ -320,9 +414,11 @@ def recover_sharded(root: Node, bands: List[Node], m: int, dist, group=None, bac
             cols[top - 1: top - 1 + len(seg)] = seg
     # the path's end column: root cell (start column 1, weight length), held by
     # the owner of row 0 (root rows are not replicated)
-    r0 = next(r for r, (a, b) in enumerate(R["spans"]) if a <= 0 < b)
-    end = R["reach"][0, length].reshape(1).clone()
-    _bcast(dist, group, end, r0)
+    end_owner = r0
+    end = backend.empty((1,))
+    if R is not None and grank == r0:
+        end.copy_(R["reach"][0, length].reshape(1))
+    _bcast(dist, group, end, end_owner)
     cols[m] = int(end.item())
     return length, cols
 
@@ -341,9 +437,9 @@ def lcs_sharded(a, b, *, group=None, device=None, low_memory=False, backend=None
     if own:
         backend = CudaBackend(0 if device is None else int(device))
     try:
-        root, bands, upper = solve_sharded(rows, cols, dist, group, backend,
-                                           with_trace=not low_memory)
-        length, path = recover_sharded(root, bands, len(rows), dist, group, backend)
+        root, bands, upper, ctx = solve_sharded(rows, cols, dist, group, backend,
+                                                with_trace=not low_memory)
+        length, path = recover_sharded(root, bands, len(rows), dist, group, backend, ctx)
     finally:
         if own:
             backend.free()
