@@ -429,8 +429,24 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
                 continue;
             }
             // skeleton + refinement passes
+            // per-height overrides (tuning knobs): LCSG_SKEL_STRIDE_H<h>, LCSG_COL_BLOCK_H<h>
+            const std::string hs = std::to_string(h);
+            // narrow-ish wide tables (w1 <= 513) of long strings: skeleton
+            // rows every 512 (row steps 64, 8, 1) -- cheaper than the
+            // skeleton bisection every 64 rows (measured at cfg5)
+            const int stride_def =
+                (getenv("LCSG_SKELETON_STRIDE") == nullptr && n1 > 8193 && maxw1 <= 513)
+                    ? 512 : skel_stride;
+            const int stride_h =
+                std::max(2, env_int(("LCSG_SKEL_STRIDE_H" + hs).c_str(), stride_def));
             int32_t S = 1;
-            while (S * 2 <= skel_stride) S *= 2;
+            while (S * 2 <= stride_h) S *= 2;
+            int32_t cb = col_block;
+            const int cb_env = env_int(("LCSG_COL_BLOCK_H" + hs).c_str(), 0);
+            if (cb_env > 0) {
+                cb = 1;
+                while (cb * 2 <= std::min(16, std::max(2, cb_env))) cb *= 2;
+            }
             // skeleton rows: thread-per-row DFS for narrow tables, warp-per-row
             // DFS for medium, CTA-per-row (cooperative top rounds) for wide
             L.kind = maxw1 <= skel_thread_max ? 5 : (maxw1 <= skel_warp_max ? 6 : 3);
@@ -439,7 +455,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             if (tiled) {  // column-refinement stages (row step S/B, S/B^2, .., 1) + finalize
                 int32_t rem = S;
                 while (rem > 1) {
-                    const int32_t B = std::min<int32_t>(col_block, rem);
+                    const int32_t B = std::min<int32_t>(cb, rem);
                     LaunchH P = L;
                     P.kind = 7;
                     P.stride_or_delta = B;

@@ -61,6 +61,28 @@ __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
+// Traces of the INF cells (kfin, w] of one output row whose finite prefix
+// [0, kfin] (reach and trace) is already in `tr`: Alg. 1 (_kernel.pyx:28-60)
+// visits the INF cells as nodes whose mid is INF; such a node fills
+// [mid, right] with its `top` (the split bound inherited from the last finite
+// mid on its path, else 0) and recurses left.  One replay of that path over
+// [0, colhi] therefore tiles (kfin, colhi] into <= log2(w)+1 segments; cells
+// beyond colhi get 0 (_kernel.pyx:79-82).
+__device__ __forceinline__ void inf_traces(int32_t *tr, int32_t kfin, int32_t colhi, int32_t w) {
+    for (int32_t qq = max(kfin, colhi) + 1; qq <= w; ++qq) tr[qq] = 0;
+    int32_t left = 0, right = colhi, top = 0;
+    while (right > kfin) {  // [left, right] still holds INF cells
+        const int32_t mid = (left + right + 1) >> 1;
+        if (mid <= kfin) {  // finite node: its trace bounds the right half
+            top = tr[mid];
+            left = mid + 1;
+        } else {  // INF node: mid..right get `top`
+            for (int32_t qq = mid; qq <= right; ++qq) tr[qq] = top;
+            right = mid - 1;
+        }
+    }
+}
+
 // rows [row0, row0 + nrows) of a table into shared memory at pitch PT
 // (columns >= w1 are INF).  A block of slab rows is one contiguous range of
 // the table, copied flat when w1 == PT (every power-of-two tree level).
@@ -266,28 +288,8 @@ __global__ void __launch_bounds__(NarrowGeom<P>::NT)
                 tr[j] = (int32_t)(best[q][j] & (((Key)1 << shift) - 1));
             }
         }
-        // INF cells: Alg. 1's node `top` (replay of the bisection path over
-        // the finite traces), 0 beyond colhi
-        const int32_t colhi = min(w, ku[q] + wstar_l);
-        for (int32_t qq = kfin + 1; qq <= w; ++qq) {
-            int32_t t = 0;
-            if (qq <= colhi) {
-                int32_t left = 0, right = colhi, top = 0;
-                for (;;) {
-                    const int32_t mid = (left + right + 1) >> 1;
-                    if (mid <= kfin) {  // finite node: qq lies to its right
-                        top = tr[mid];
-                        left = mid + 1;
-                    } else if (qq >= mid) {
-                        break;  // INF node: mid..right all get `top`
-                    } else {
-                        right = mid - 1;
-                    }
-                }
-                t = top;
-            }
-            tr[qq] = t;
-        }
+        // INF cells: Alg. 1's node `top`, 0 beyond colhi
+        inf_traces(tr, kfin, min(w, ku[q] + wstar_l), w);
         out_kmax[i0 + r] = kfin;
         wmax = max(wmax, kfin);
     }
@@ -358,26 +360,7 @@ __global__ void __launch_bounds__(LP_NT)
                 tr[j] = (int32_t)(best[j] & (((Key)1 << shift) - 1));
             }
         }
-        const int32_t colhi = min(w, ku + wstar_l);
-        for (int32_t qq = kfin + 1; qq <= w; ++qq) {  // Alg. 1 replay for INF cells
-            int32_t t = 0;
-            if (qq <= colhi) {
-                int32_t left = 0, right = colhi, top = 0;
-                for (;;) {
-                    const int32_t mid = (left + right + 1) >> 1;
-                    if (mid <= kfin) {
-                        top = tr[mid];
-                        left = mid + 1;
-                    } else if (qq >= mid) {
-                        break;
-                    } else {
-                        right = mid - 1;
-                    }
-                }
-                t = top;
-            }
-            tr[qq] = t;
-        }
+        inf_traces(tr, kfin, min(w, ku + wstar_l), w);  // Alg. 1 replay for INF cells
         out_kmax[i] = kfin;
         wmax = max(wmax, kfin);
     }

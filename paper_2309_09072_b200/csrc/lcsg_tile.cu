@@ -147,6 +147,13 @@ __global__ void __launch_bounds__(CR_THREADS)
             rbv = __ldg(out_reach + ibot * w1 + j);
             rbt = __ldg(out_trace + ibot * w1 + j);
         }
+        // top row INF over the whole warp: every interior cell is INF (reach
+        // is nondecreasing in the start row); their traces are finalize's
+        if (__all_sync(0xffffffffu, r0v >= inf)) {
+            if (active)
+                for (int r = 1; r < rb; ++r) out_reach[(i0 + (int64_t)r * rs) * w1 + j] = inf;
+            return;
+        }
         sR[0] = r0v;
         sT[0] = r0t;
         for (int r = 1; r <= S; ++r) {
@@ -319,6 +326,14 @@ __global__ void __launch_bounds__(CR_THREADS)
             rbv = __ldg(out_reach + (i0 + rb) * w1 + j);
             rbt = __ldg(out_trace + (i0 + rb) * w1 + j);
         }
+        // top row INF over the whole warp: every interior cell is INF
+        if (__all_sync(0xffffffffu, r0v >= inf)) {
+            if (active) {
+                int32_t *o = out_reach + i0 * w1 + j;
+                for (int r = 1; r < rb; ++r) o[(int64_t)r * w1] = inf;
+            }
+            return;
+        }
         sR[0] = r0v;
         sT[0] = r0t;
         for (int r = 1; r <= S; ++r) {
@@ -440,13 +455,15 @@ __global__ void __launch_bounds__(CR_THREADS)
     }
     // write every interior cell's reach (INF included: finalize finds each
     // row's finite prefix in it) and the finite cells' traces
+    if (active) {
+        int32_t *orr = out_reach + i0 * w1 + j, *otr = out_trace + i0 * w1 + j;
 #pragma unroll 1
-    for (int r = 1; r < S; ++r) {
-        const int32_t v = sR[r * CR_THREADS];
-        if (active && r < rb) {
-            const int64_t off = (i0 + r) * w1 + j;
-            out_reach[off] = v;
-            if (v < inf) out_trace[off] = sT[r * CR_THREADS];
+        for (int r = 1; r < rb; ++r) {
+            orr += w1;
+            otr += w1;
+            const int32_t v = sR[r * CR_THREADS];
+            *orr = v;
+            if (v < inf) *otr = sT[r * CR_THREADS];
         }
     }
 }

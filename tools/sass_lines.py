@@ -17,9 +17,9 @@ if func:
     lines = lines[start:end]
 cur, off2line = None, {}
 for l in lines:
-    m = re.search(r'line (\d+)', l)
+    m = re.search(r'File "([^"]+)", line (\d+)', l)
     if m:
-        cur = int(m.group(1))
+        cur = int(m.group(2)) if m.group(1).endswith(src_path.split("/")[-1]) else -int(m.group(2))
     m2 = re.search(r'/\*([0-9a-f]{4,})\*/', l)
     if m2 and cur is not None:
         off2line[int(m2.group(1), 16)] = cur
@@ -39,5 +39,5 @@ st = sum(v[1] for v in agg.values()) or 1
 src = open(src_path).read().split("\n")
 print(f"total warp instructions {tot:.4g}, stall samples {st:.0f}")
 for ln, (e, s, t) in sorted(agg.items(), key=lambda x: -x[1][0])[:top]:
-    text = src[ln - 1].strip()[:70] if ln > 0 else ""
+    text = src[ln - 1].strip()[:70] if 0 < ln <= len(src) else "(other file)"
     print(f"{ln:5d} instr {100 * e / tot:5.1f}% thr/inst {t / max(e, 1):4.1f} stall {100 * s / st:5.1f}%  {text}")
