@@ -431,12 +431,13 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             // skeleton + refinement passes
             // per-height overrides (tuning knobs): LCSG_SKEL_STRIDE_H<h>, LCSG_COL_BLOCK_H<h>
             const std::string hs = std::to_string(h);
-            // narrow-ish wide tables (w1 <= 513) of long strings: skeleton
-            // rows every 512 (row steps 64, 8, 1) -- cheaper than the
-            // skeleton bisection every 64 rows (measured at cfg5)
-            const int stride_def =
-                (getenv("LCSG_SKELETON_STRIDE") == nullptr && n1 > 8193 && maxw1 <= 513)
-                    ? 512 : skel_stride;
+            // many narrow-ish wide tables (w1 <= 513, >= 32 combines) of long
+            // strings: skeleton rows every 512 (row steps 64, 8, 1) -- cheaper
+            // than the skeleton bisection every 64 rows (measured: cfg5 levels
+            // s = 128..512 gain 0.4 ms; cfg4's 2..8-combine levels lose 0.2)
+            const int stride_def = (getenv("LCSG_SKELETON_STRIDE") == nullptr && n1 > 8193 &&
+                                    maxw1 <= 513 && L.count >= 32)
+                                       ? 512 : skel_stride;
             const int stride_h =
                 std::max(2, env_int(("LCSG_SKEL_STRIDE_H" + hs).c_str(), stride_def));
             int32_t S = 1;
