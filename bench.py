@@ -75,6 +75,16 @@ def load_counters(cfg, seed):
     return d.get(f"cfg{cfg}/seed{seed}", {}).get("counters")
 
 
+def load_traffic(cfg):
+    """DRAM bytes of one solve's combine launches from the committed ncu
+    launch list (profiles/traffic_cfgN.json, tools/traffic.py); None if absent."""
+    path = os.path.join(ROOT, "profiles", f"traffic_cfg{cfg}.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        return json.load(f)["dram_bytes"]
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -306,7 +316,9 @@ def run_ours(args, rank, world, dist):
         alg = 4 * counters["G"] + 8 * counters["OUT"] + 4 * counters["IN"]
         achieved = alg / (comb / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None,
+                "frac": achieved / peak, "traffic": load_traffic(args.config),
+                "traffic_source": "ncu dram__bytes_read+write of one solve's combine launches "
+                                  f"(profiles/traffic_cfg{args.config}.json)",
                 "kernel": "combine levels (all heights)", "combine_ms": comb,
                 "algorithmic_bytes": alg, "peak_source": peak_kind,
                 "compulsory_frac": (8 * counters["OUT"] + 4 * counters["IN"]) / (comb / 1e3) / 1e9 / peak}
