@@ -303,11 +303,13 @@ __global__ void __launch_bounds__(CR_THREADS)
     const int32_t blk = fdiv(slot, w1div);
     const int32_t j = slot - blk * w1div.d;
     const CombineDesc &d = descs[di];
-    const int64_t n1 = (int64_t)c.n + 1;
+    const int32_t n1 = c.n + 1;
     const int32_t inf = c.inf;
     const bool active = blk < nblk && j < d.w1;
-    const int64_t i0 = (int64_t)blk * S;
-    const int32_t rb = active ? (int32_t)min((int64_t)S, n1 - 1 - i0) : 0;
+    // 32-bit element offsets: every refined table has n1 * w1 < 2^32
+    // (lcsg_api.cu node kinds), so an address is one IMAD + one IMAD.WIDE
+    const uint32_t i0 = (uint32_t)blk * (uint32_t)S;
+    const int32_t rb = active ? min(S, n1 - 1 - (int32_t)i0) : 0;
     const int32_t *__restrict__ Ur = d.U.reach;
     const int32_t *__restrict__ Uk = d.U.kmax;
     const int32_t *__restrict__ Lr = d.L.reach;
@@ -321,16 +323,17 @@ __global__ void __launch_bounds__(CR_THREADS)
     {
         int32_t r0v = inf, r0t = 0, rbv = inf, rbt = 0;
         if (active && rb >= 2) {
-            r0v = __ldg(out_reach + i0 * w1 + j);
-            r0t = __ldg(out_trace + i0 * w1 + j);
-            rbv = __ldg(out_reach + (i0 + rb) * w1 + j);
-            rbt = __ldg(out_trace + (i0 + rb) * w1 + j);
+            const uint32_t o0 = i0 * (uint32_t)w1 + j, ob = (i0 + rb) * (uint32_t)w1 + j;
+            r0v = __ldg(out_reach + o0);
+            r0t = __ldg(out_trace + o0);
+            rbv = __ldg(out_reach + ob);
+            rbt = __ldg(out_trace + ob);
         }
         // top row INF over the whole warp: every interior cell is INF
         if (__all_sync(0xffffffffu, r0v >= inf)) {
             if (active) {
-                int32_t *o = out_reach + i0 * w1 + j;
-                for (int r = 1; r < rb; ++r) o[(int64_t)r * w1] = inf;
+                uint32_t o = i0 * (uint32_t)w1 + j;
+                for (int r = 1; r < rb; ++r) out_reach[o += w1] = inf;
             }
             return;
         }
@@ -347,8 +350,8 @@ __global__ void __launch_bounds__(CR_THREADS)
         for (int r = dl; r < S; r += 2 * dl) {
             const int a = r - dl, b = r + dl;  // b <= S; rows >= rb mirror the bottom row
             const bool real = active && r < rb;
-            const int64_t ci = i0 + r;
-            const int32_t *Uc = Ur + ci * uw1;
+            const uint32_t ci = i0 + r;
+            const int32_t *Uc = Ur + ci * (uint32_t)uw1;
             const int32_t kmc = real ? __ldg(Uk + ci) : -1;
             const int32_t Ra = sR[a * CR_THREADS], Rb = sR[b * CR_THREADS];
             bool tail = false, longr = false;
@@ -359,8 +362,9 @@ __global__ void __launch_bounds__(CR_THREADS)
                 const int32_t Tb = fb ? sT[b * CR_THREADS] : 0;
                 // both interleave windows hold <= dl+1 candidates: count them
                 // with independent loads (no dependent binary-search steps)
-                const int32_t Xa = __ldg(Ur + (i0 + a) * uw1 + Ta);
-                const int32_t Xb = fb ? __ldg(Ur + min(i0 + b, i0 + rb) * uw1 + Tb) : 0;
+                const int32_t Xa = __ldg(Ur + ((i0 + a) * (uint32_t)uw1 + Ta));
+                const int32_t Xb =
+                    fb ? __ldg(Ur + ((i0 + min(b, rb)) * (uint32_t)uw1 + Tb)) : 0;
                 const int32_t hi = min(Ta, kmc);
                 const int32_t lo = min(max(0, Ta - dl), hi);
                 const int32_t lo2 = min(Tb, kmc), hi2 = min(Tb + dl, kmc);
@@ -386,13 +390,13 @@ __global__ void __launch_bounds__(CR_THREADS)
                     } else if (kl == kh && Xa == Xb) {
                         // pinned crossing: X(c,j) = X(a,j) = X(b,j) = U[c,kl]
                         // is already known -- one gather, no U load
-                        outv = __ldg(Lr + (int64_t)(Xa - 1) * lw1 + (j - kl));
+                        outv = __ldg(Lr + ((uint32_t)(Xa - 1) * (uint32_t)lw1 + (j - kl)));
                         outk = kl;
                     } else {
                         Key best = ~(Key)0;
                         for (int32_t k = kl; k <= kh; ++k) {
                             const int32_t x = __ldg(Uc + k);  // finite: k <= kmax_c
-                            const int32_t v = __ldg(Lr + (int64_t)(x - 1) * lw1 + (j - k));
+                            const int32_t v = __ldg(Lr + ((uint32_t)(x - 1) * (uint32_t)lw1 + (j - k)));
                             const Key key = tpack<Key>(v, k, shift);
                             best = key < best ? key : best;
                         }
@@ -439,8 +443,8 @@ __global__ void __launch_bounds__(CR_THREADS)
                     const int32_t k = ws[o].kl + (g - ws[o].start), tj = ws[o].j;
                     int32_t v = inf;
                     if (tj - k <= wl)
-                        v = __ldg(Lr + (int64_t)(__ldg(Ur + (int64_t)ws[o].row * uw1 + k) - 1) * lw1 +
-                                  (tj - k));
+                        v = __ldg(Lr + ((uint32_t)(__ldg(Ur + ((uint32_t)ws[o].row * (uint32_t)uw1 + k)) - 1) *
+                                            (uint32_t)lw1 + (tj - k)));
                     key_atomic_min(&ws[o].key, tpack<Key>(v, k, shift));
                 }
                 __syncwarp();
@@ -456,7 +460,8 @@ __global__ void __launch_bounds__(CR_THREADS)
     // write every interior cell's reach (INF included: finalize finds each
     // row's finite prefix in it) and the finite cells' traces
     if (active) {
-        int32_t *orr = out_reach + i0 * w1 + j, *otr = out_trace + i0 * w1 + j;
+        const uint32_t o0 = i0 * (uint32_t)w1 + j;
+        int32_t *orr = out_reach + o0, *otr = out_trace + o0;
 #pragma unroll 1
         for (int r = 1; r < rb; ++r) {
             orr += w1;
