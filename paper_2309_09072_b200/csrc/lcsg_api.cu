@@ -1074,7 +1074,8 @@ int lcsg_combine_rows(const int32_t *upper_reach, int32_t wu1, const int32_t *up
     const int P = narrow_bucket(std::max(wu1, wl1) - 1);
     if (w1 <= thread_max_w1 && P > 0 && env_int("LCSG_NARROW", 1) != 0) {
         CKL(launch_narrow(&sc->d, 1, c, shift, key64, P, s));
-    } else if (w1 <= thread_max_w1 || S == 1 || rows < 3) {
+    } else if (w1 <= thread_max_w1 || S == 1 || rows < 3 ||
+               n1 * (int64_t)w1 >= ((int64_t)1 << 32)) {  // refinement: 32-bit offsets
         CKL(launch_combine(w1 <= 65 ? 0 : 1, &sc->d, 1, c, shift, key64, s));
     } else {
         if (w1 <= env_int("LCSG_SKEL_THREAD_MAX_W1", 65))

@@ -120,15 +120,17 @@ __global__ void __launch_bounds__(CR_THREADS)
     const int32_t blk = fdiv(slot, w1div);
     const int32_t j = slot - blk * w1div.d;
     const CombineDesc &d = descs[di];
-    const int64_t n1 = (int64_t)c.n + 1;
+    const int32_t n1 = c.n + 1;
     const int32_t inf = c.inf;
     const bool active = blk < nblk && j < d.w1;
-    const int64_t i0 = (int64_t)blk * S * rs;
-    const int64_t span = n1 - 1 - i0;  // actual rows from i0 to the last row
+    // 32-bit element offsets (n1 * w1 < 2^32 for every refined table)
+    const int32_t i0 = blk * S * rs;
+    const int32_t span = n1 - 1 - i0;  // actual rows from i0 to the last row
     // local rows r < rb are real; r >= rb mirror the bottom row
-    const int32_t rb = active ? (int32_t)min((int64_t)S, (span + rs - 1) / rs) : 0;
+    const int32_t rb = active ? min(S, (span + rs - 1) / rs) : 0;
     // bottom bounding row: the next block boundary if it exists, else the last row
-    const int64_t ibot = span >= (int64_t)S * rs ? i0 + (int64_t)S * rs : n1 - 1;
+    const int32_t ibot = span >= S * rs ? i0 + S * rs : n1 - 1;
+    const uint32_t uw1u = (uint32_t)d.U.w1, lw1u = (uint32_t)d.L.w1, w1u = (uint32_t)d.w1;
     const int32_t *__restrict__ Ur = d.U.reach;
     const int32_t *__restrict__ Uk = d.U.kmax;
     const int32_t *__restrict__ Lr = d.L.reach;
@@ -142,16 +144,17 @@ __global__ void __launch_bounds__(CR_THREADS)
     {
         int32_t r0v = inf, r0t = 0, rbv = inf, rbt = 0;
         if (active && rb >= 2) {
-            r0v = __ldg(out_reach + i0 * w1 + j);
-            r0t = __ldg(out_trace + i0 * w1 + j);
-            rbv = __ldg(out_reach + ibot * w1 + j);
-            rbt = __ldg(out_trace + ibot * w1 + j);
+            const uint32_t o0 = (uint32_t)i0 * w1u + j, ob = (uint32_t)ibot * w1u + j;
+            r0v = __ldg(out_reach + o0);
+            r0t = __ldg(out_trace + o0);
+            rbv = __ldg(out_reach + ob);
+            rbt = __ldg(out_trace + ob);
         }
         // top row INF over the whole warp: every interior cell is INF (reach
         // is nondecreasing in the start row); their traces are finalize's
         if (__all_sync(0xffffffffu, r0v >= inf)) {
             if (active)
-                for (int r = 1; r < rb; ++r) out_reach[(i0 + (int64_t)r * rs) * w1 + j] = inf;
+                for (int r = 1; r < rb; ++r) out_reach[(uint32_t)(i0 + r * rs) * w1u + j] = inf;
             return;
         }
         sR[0] = r0v;
@@ -168,10 +171,10 @@ __global__ void __launch_bounds__(CR_THREADS)
         for (int r = dl; r < S; r += 2 * dl) {
             const int a = r - dl, b = r + dl;  // b <= S; rows >= rb mirror the bottom row
             const bool real = active && r < rb;
-            const int64_t ci = i0 + (int64_t)r * rs;
-            const int64_t ai = i0 + (int64_t)a * rs;
-            const int64_t bi = b < rb ? i0 + (int64_t)b * rs : ibot;
-            const int32_t *Uc = Ur + ci * uw1;
+            const uint32_t ci = (uint32_t)(i0 + r * rs);
+            const uint32_t ai = (uint32_t)(i0 + a * rs);
+            const uint32_t bi = (uint32_t)(b < rb ? i0 + b * rs : ibot);
+            const int32_t *Uc = Ur + ci * uw1u;
             const int32_t kmc = real ? __ldg(Uk + ci) : -1;
             const int32_t Ra = sR[a * CR_THREADS], Rb = sR[b * CR_THREADS];
             bool tail = false;
@@ -180,8 +183,8 @@ __global__ void __launch_bounds__(CR_THREADS)
                 const bool fb = Rb < inf;
                 const int32_t Ta = sT[a * CR_THREADS];
                 const int32_t Tb = fb ? sT[b * CR_THREADS] : 0;
-                const int32_t Xa = __ldg(Ur + ai * uw1 + Ta);
-                const int32_t Xb = fb ? __ldg(Ur + bi * uw1 + Tb) : 0;
+                const int32_t Xa = __ldg(Ur + (ai * uw1u + Ta));
+                const int32_t Xb = fb ? __ldg(Ur + (bi * uw1u + Tb)) : 0;
                 const int32_t hi1 = min(Ta, kmc);
                 const int32_t lo1 = min(max(0, Ta - dist), hi1);
                 const int32_t lo2 = min(Tb, kmc), hi2 = min(Tb + dist, kmc);
@@ -218,7 +221,7 @@ __global__ void __launch_bounds__(CR_THREADS)
                     Key best = ~(Key)0;
                     for (int32_t k = kl; k <= kh; ++k) {
                         const int32_t x = __ldg(Uc + k);  // finite: k <= kmax_c
-                        const int32_t v = __ldg(Lr + (int64_t)(x - 1) * lw1 + (j - k));
+                        const int32_t v = __ldg(Lr + ((uint32_t)(x - 1) * lw1u + (j - k)));
                         const Key key = tpack<Key>(v, k, shift);
                         best = key < best ? key : best;
                     }
@@ -241,12 +244,12 @@ __global__ void __launch_bounds__(CR_THREADS)
                 const int32_t tj = __shfl_sync(0xffffffffu, j, src);
                 const int32_t tkl = __shfl_sync(0xffffffffu, kl, src);
                 const int32_t tkh = min(tj, __shfl_sync(0xffffffffu, kmc, src));
-                const int64_t trow = __shfl_sync(0xffffffffu, ci, src);
-                const int32_t *Ut = Ur + trow * uw1;
+                const uint32_t trow = __shfl_sync(0xffffffffu, ci, src);
+                const int32_t *Ut = Ur + trow * uw1u;
                 Key best = ~(Key)0;
                 for (int32_t k = tkl + lane; k <= tkh; k += 32) {
                     int32_t v = inf;
-                    if (tj - k <= wl) v = __ldg(Lr + (int64_t)(__ldg(Ut + k) - 1) * lw1 + (tj - k));
+                    if (tj - k <= wl) v = __ldg(Lr + ((uint32_t)(__ldg(Ut + k) - 1) * lw1u + (tj - k)));
                     const Key key = tpack<Key>(v, k, shift);
                     best = key < best ? key : best;
                 }
@@ -265,7 +268,7 @@ __global__ void __launch_bounds__(CR_THREADS)
     for (int r = 1; r < S; ++r) {
         const int32_t v = sR[r * CR_THREADS];
         if (active && r < rb) {
-            const int64_t off = (i0 + (int64_t)r * rs) * w1 + j;
+            const uint32_t off = (uint32_t)(i0 + r * rs) * w1u + j;
             out_reach[off] = v;
             if (v < inf) out_trace[off] = sT[r * CR_THREADS];
         }
@@ -488,10 +491,10 @@ __global__ void __launch_bounds__(32 * FN_WARPS)
     __shared__ int2 seg_all[FN_WARPS][32][FN_MAXSEG];
     __shared__ int nseg_all[FN_WARPS][32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int64_t n1 = (int64_t)c.n + 1;
+    const int32_t n1 = c.n + 1;
     const int32_t di = (int32_t)(blockIdx.z * 65535u + blockIdx.y);  // CTA-uniform
     if (di >= ndesc) return;
-    const int64_t r0 = ((int64_t)blockIdx.x * FN_WARPS + wid) * rpw;
+    const int32_t r0 = ((int32_t)blockIdx.x * FN_WARPS + wid) * rpw;
     if (r0 >= n1) return;  // warp-uniform
     const CombineDesc &d = descs[di];
     const int32_t inf = c.inf;
@@ -503,13 +506,14 @@ __global__ void __launch_bounds__(32 * FN_WARPS)
     int32_t *__restrict__ const out_kmax = d.out_kmax;
     const int32_t w1 = d.w1;
     // phase 1: lane = row
-    const int64_t i = r0 + lane;
+    const int32_t i = r0 + lane;
     const bool act = lane < rpw && i < n1 - 1 && (i & (S - 1)) != 0;  // S: power of two
     int32_t K = -1, colhi = -1, kmax_warp = -1;
     if (act) {
         colhi = min(w, tab_kmax(U, i, inf) + wstarL);
-        const int32_t *reach = out_reach + i * w1;
-        const int32_t *trace = out_trace + i * w1;
+        // 32-bit element offsets (n1 * w1 < 2^32 for every refined table)
+        const int32_t *reach = out_reach + (uint32_t)i * (uint32_t)w1;
+        const int32_t *trace = out_trace + (uint32_t)i * (uint32_t)w1;
         // the replay of Alg. 1's bisection over [0, colhi] IS a binary search
         // for the end of the row's finite prefix: finite mids go right, INF
         // mids are the INF nodes (their segments) and go left; K = left - 1
@@ -549,7 +553,7 @@ __global__ void __launch_bounds__(32 * FN_WARPS)
         const int32_t ch = __shfl_sync(0xffffffffu, colhi, rr);
         const int ns = nseg_all[wid][rr];
         const int2 *sg = seg_all[wid][rr];
-        int32_t *trace = out_trace + (r0 + rr) * w1;
+        int32_t *trace = out_trace + (uint32_t)(r0 + rr) * (uint32_t)w1;
         for (int32_t q = max(ch, Kr) + 1 + lane; q <= w; q += 32) trace[q] = 0;
         int32_t hi = ch;
         for (int sgi = 0; sgi < ns; ++sgi) {
