@@ -90,12 +90,22 @@ __global__ void __launch_bounds__(32 * SK_WARPS)
     const int64_t i = (r == nsk - 1) ? n1 - 1 : (int64_t)r * stride;
     const CombineDesc &d = descs[di];
     const int32_t inf = c.inf;
-    const TabAcc U = resolve(d.U, c), L = resolve(d.L, c);
-    const int32_t w = d.w1 - 1, wl = L.w1 - 1;
-    const int32_t kmaxU = tab_kmax(U, i, inf);
+    // skeleton combines always have materialised (slab) children, and every
+    // refined table has n1 * w1 < 2^32 (lcsg_api.cu): plain rows, 32-bit offsets
+    const int32_t *__restrict__ Urow = d.U.reach + (uint32_t)i * (uint32_t)d.U.w1;
+    const int32_t *__restrict__ Lr = d.L.reach;
+    const uint32_t lw1 = (uint32_t)d.L.w1;
+    const int32_t w = d.w1 - 1, wl = d.L.w1 - 1;
+    const int32_t kmaxU = __ldg(d.U.kmax + i);
     const int32_t colhi = min(w, kmaxU + *d.L.wstar);
-    int32_t *reach = d.out_reach + i * d.w1;
-    int32_t *trace = d.out_trace + i * d.w1;
+    int32_t *reach = d.out_reach + (uint32_t)i * (uint32_t)d.w1;
+    int32_t *trace = d.out_trace + (uint32_t)i * (uint32_t)d.w1;
+    // cell_value (_kernel.pyx:14-25) of split k at column j
+    auto cell = [&](int32_t k, int32_t j) -> int32_t {
+        const int32_t x = __ldg(Urow + k);
+        if (k > j || x >= inf || j - k > wl) return inf;
+        return __ldg(Lr + ((uint32_t)(x - 1) * lw1 + (uint32_t)(j - k)));
+    };
     if (threadIdx.x == 0) {
         front[0][0] = make_int4(0, colhi, 0, kmaxU);
         nfront[0] = 1;
@@ -118,7 +128,7 @@ __global__ void __launch_bounds__(32 * SK_WARPS)
             __syncthreads();
             Key best = ~(Key)0;
             for (int32_t k = nd.z + (int32_t)threadIdx.x; k <= nd.w; k += 32 * SK_WARPS) {
-                const Key key = rpack<Key>(rcell(L, tab_get(U, i, k), k, mid, inf, wl), k, shift);
+                const Key key = rpack<Key>(cell(k, mid), k, shift);
                 best = key < best ? key : best;
             }
             best = rwarp_min(best);
@@ -160,7 +170,7 @@ __global__ void __launch_bounds__(32 * SK_WARPS)
                 const int32_t mid = (left + right + 1) >> 1;
                 Key best = ~(Key)0;
                 for (int32_t k = top + lane; k <= bottom; k += 32) {
-                    const Key key = rpack<Key>(rcell(L, tab_get(U, i, k), k, mid, inf, wl), k, shift);
+                    const Key key = rpack<Key>(cell(k, mid), k, shift);
                     best = key < best ? key : best;
                 }
                 best = rwarp_min(best);
