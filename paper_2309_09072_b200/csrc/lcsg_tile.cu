@@ -17,6 +17,7 @@
 // [lower bound, min(j, kmax_c)].
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 #include "lcsg_internal.cuh"
 
@@ -292,10 +293,13 @@ __device__ __forceinline__ CoopSlot<Key> *coop_slots() {
 }
 
 // rs == 1 specialisation (the hot one): identical cell logic, fewer registers.
-template <typename Key>
+// SC: block size S as a compile-time constant (0: runtime S) -- constant
+// shared-memory offsets and unrolled init / write loops
+template <typename Key, int SC>
 __global__ void __launch_bounds__(CR_THREADS)
     column_refine_fine_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int shift,
-                         int32_t S, int32_t nblk, FastDiv w1div) {
+                         int32_t S_arg, int32_t nblk, FastDiv w1div) {
+    const int32_t S = SC > 0 ? SC : S_arg;
     extern __shared__ int32_t csm[];
     int32_t *sR = csm + threadIdx.x;                     // sR[r * CR_THREADS]
     int32_t *sT = csm + (S + 1) * CR_THREADS + threadIdx.x;
@@ -342,6 +346,7 @@ __global__ void __launch_bounds__(CR_THREADS)
         }
         sR[0] = r0v;
         sT[0] = r0t;
+#pragma unroll
         for (int r = 1; r <= S; ++r) {
             sR[r * CR_THREADS] = r >= rb ? rbv : inf;
             sT[r * CR_THREADS] = r >= rb ? rbt : 0;
@@ -465,13 +470,24 @@ __global__ void __launch_bounds__(CR_THREADS)
     if (active) {
         const uint32_t o0 = i0 * (uint32_t)w1 + j;
         int32_t *orr = out_reach + o0, *otr = out_trace + o0;
+        if (SC > 0) {
+#pragma unroll
+            for (int r = 1; r < S; ++r) {
+                if (r < rb) {
+                    const int32_t v = sR[r * CR_THREADS];
+                    orr[r * w1] = v;
+                    if (v < inf) otr[r * w1] = sT[r * CR_THREADS];
+                }
+            }
+        } else {
 #pragma unroll 1
-        for (int r = 1; r < rb; ++r) {
-            orr += w1;
-            otr += w1;
-            const int32_t v = sR[r * CR_THREADS];
-            *orr = v;
-            if (v < inf) *otr = sT[r * CR_THREADS];
+            for (int r = 1; r < rb; ++r) {
+                orr += w1;
+                otr += w1;
+                const int32_t v = sR[r * CR_THREADS];
+                *orr = v;
+                if (v < inf) *otr = sT[r * CR_THREADS];
+            }
         }
     }
 }
@@ -583,17 +599,35 @@ int launch_block_refine(const CombineDesc *descs, int32_t ndesc, Ctx c, int shif
     if (!attr) {
         cudaFuncSetAttribute(column_refine_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
         cudaFuncSetAttribute(column_refine_kernel<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
-        cudaFuncSetAttribute(column_refine_fine_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
-        cudaFuncSetAttribute(column_refine_fine_kernel<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
+        cudaFuncSetAttribute(column_refine_fine_kernel<uint32_t, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
+        cudaFuncSetAttribute(column_refine_fine_kernel<uint64_t, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
         attr = true;
     }
     if (rs == 1) {  // last stage: lean kernel (finite cells only; finalize writes INF)
-        if (key64)
-            column_refine_fine_kernel<uint64_t><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift,
-                                                                                S, nblk, w1div);
-        else
-            column_refine_fine_kernel<uint32_t><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift,
-                                                                                S, nblk, w1div);
+#define FINE_LAUNCH(K, SCV)                                                                      \
+    column_refine_fine_kernel<K, SCV><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift, S, \
+                                                                      nblk, w1div)
+        // compile-time S (32 registers, full occupancy) pays on narrower
+        // tables; the widest levels keep the runtime-S build (measured)
+        const char *sc_env = getenv("LCSG_FINE_SC_MAXW1");
+        const int sc_max = sc_env ? atoi(sc_env) : 2049;
+        const int32_t Ssel = maxw1 <= sc_max ? S : 0;
+        if (key64) {
+            switch (Ssel) {
+                case 2: FINE_LAUNCH(uint64_t, 2); break;
+                case 4: FINE_LAUNCH(uint64_t, 4); break;
+                case 8: FINE_LAUNCH(uint64_t, 8); break;
+                default: FINE_LAUNCH(uint64_t, 0); break;
+            }
+        } else {
+            switch (Ssel) {
+                case 2: FINE_LAUNCH(uint32_t, 2); break;
+                case 4: FINE_LAUNCH(uint32_t, 4); break;
+                case 8: FINE_LAUNCH(uint32_t, 8); break;
+                default: FINE_LAUNCH(uint32_t, 0); break;
+            }
+        }
+#undef FINE_LAUNCH
     } else if (key64) {
         column_refine_kernel<uint64_t><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift, S,
                                                                        rs, nblk, w1div);
