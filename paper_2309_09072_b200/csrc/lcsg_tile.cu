@@ -499,8 +499,11 @@ __global__ void __launch_bounds__(CR_THREADS)
 // consecutive rows: lane r replays row r's path (no gathers; the INF nodes'
 // mids tile (K, colhi] in descending order), then the warp fills the rows
 // one after another with coalesced stores.
-constexpr int FN_MAXSEG = 34;
-
+// FN_MAXSEG: INF nodes on one bisection path over [0, colhi] -- at most one
+// per halving step, i.e. <= bit_length(colhi + 1) + 1: 18 covers w < 65536
+// (the segment buffers bound the kernel's occupancy, so the wide case is a
+// separate instantiation)
+template <int FN_MAXSEG>
 __global__ void __launch_bounds__(32 * FN_WARPS)
     finalize_rows_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int32_t S,
                          int rpw) {
@@ -648,7 +651,10 @@ int launch_finalize_rows(const CombineDesc *descs, int32_t ndesc, Ctx c, int32_t
     const int64_t warps = (n1 + rpw - 1) / rpw;  // per combine
     const dim3 blocks((unsigned)((warps + FN_WARPS - 1) / FN_WARPS),
                       (unsigned)std::min<int32_t>(ndesc, 65535), (unsigned)((ndesc + 65534) / 65535));
-    finalize_rows_kernel<<<blocks, 32 * FN_WARPS, 0, s>>>(descs, ndesc, c, S, rpw);
+    if (maxw1 <= 65536)
+        finalize_rows_kernel<18><<<blocks, 32 * FN_WARPS, 0, s>>>(descs, ndesc, c, S, rpw);
+    else
+        finalize_rows_kernel<34><<<blocks, 32 * FN_WARPS, 0, s>>>(descs, ndesc, c, S, rpw);
     LCSG_LAUNCH_CHECK();
     return 0;
 }

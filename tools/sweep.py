@@ -45,6 +45,15 @@ def solve():
     return length.value, st[1].value
 
 
+def clocks():
+    import subprocess
+    q = "clocks.sm,clocks.max.sm,clocks_throttle_reasons.active,temperature.gpu,power.draw"
+    r = subprocess.run(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader"],
+                       capture_output=True, text=True)
+    return r.stdout.strip()
+
+
+print("# clocks before:", clocks(), flush=True)
 base_env = {k2: v for k2, v in os.environ.items() if k2.startswith("LCSG_")}
 ref_len = None
 for setting in [("" if x == "default" else x) for x in (args.settings or ["default"])]:
@@ -65,6 +74,7 @@ for setting in [("" if x == "default" else x) for x in (args.settings or ["defau
     ok = "" if ln == ref_len else f"  LENGTH MISMATCH {ln} vs {ref_len}"
     print(f"{setting or 'default':60s} combine {statistics.median(ts):8.3f} ms "
           f"(min {min(ts):.3f}){ok}", flush=True)
+    print("#   clocks:", clocks(), flush=True)
     if args.levels:
         from torch.profiler import profile, ProfilerActivity
         flush.zero_(); torch.cuda.synchronize()
