@@ -71,7 +71,13 @@ __device__ __forceinline__ int32_t rcell(const TabAcc &L, int32_t x, int32_t k, 
 // 1. skeleton rows: exact Alg. 1, one CTA (8 warps) per row.
 // ---------------------------------------------------------------------------
 constexpr int SK_WARPS = 8;
-constexpr int SK_STACK = 34;
+// per-warp stack of the batched DFS: a step pops up to 32 nodes and pushes
+// <= 2 per node; within SK_SLACK of the top it pops one node at a time (plain
+// DFS: the stack then grows by <= 1 per tree level, and the tree height is
+// < 34), so it never overflows
+constexpr int SK_STACK = 320;
+constexpr int SK_SLACK = 40;
+constexpr int SK_SERIAL = 24;  // ranges / fills up to this length: one lane
 
 template <typename Key>
 __global__ void __launch_bounds__(32 * SK_WARPS)
@@ -80,7 +86,7 @@ __global__ void __launch_bounds__(32 * SK_WARPS)
     __shared__ int4 front[2][SK_WARPS];
     __shared__ int nfront[2];
     __shared__ Key node_key;
-    __shared__ int4 stk_all[SK_WARPS][SK_STACK];
+    extern __shared__ int4 stk_all[];  // SK_WARPS x SK_STACK
     __shared__ int kfin_sh;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int64_t di = blockIdx.x / nsk;
@@ -158,51 +164,96 @@ __global__ void __launch_bounds__(32 * SK_WARPS)
         }
         cur ^= 1;
     }
-    // --- one warp per remaining sub-tree: DFS as in combine_warp_kernel ---
+    // --- one warp per remaining sub-tree, up to 32 independent nodes per
+    // step: every node's (value, trace) depends only on its own (left, right,
+    // top, bottom), so the DFS stack is consumed in batches -- lane l takes
+    // the l-th node, scans a short split range [top, bottom] serially, and
+    // long ranges / long INF fills are done cooperatively by the whole warp.
+    // Outputs equal the reference's node by node (order-independent writes to
+    // disjoint cells); the batch turns the one-node-at-a-time chain of
+    // dependent gathers (~colhi nodes per row) into ~colhi / 32 steps.
     const int nf = nfront[cur];
     if (wid < nf) {
-        int4 *stk = stk_all[wid];
+        int4 *stk = stk_all + wid * SK_STACK;
         int sp = 0;
-        int4 nd = front[cur][wid];
-        int32_t left = nd.x, right = nd.y, top = nd.z, bottom = nd.w;
-        for (;;) {
-            while (right >= left) {
-                const int32_t mid = (left + right + 1) >> 1;
-                Key best = ~(Key)0;
-                for (int32_t k = top + lane; k <= bottom; k += 32) {
+        if (lane == 0) stk[0] = front[cur][wid];
+        sp = 1;
+        __syncwarp();
+        while (sp > 0) {
+            const int nb = min(min(sp, 32), max(1, SK_STACK - SK_SLACK - sp));
+            const bool has = lane < nb;
+            const int4 nd = has ? stk[sp - nb + lane] : make_int4(1, 0, 0, -1);
+            __syncwarp();
+            sp -= nb;
+            const int32_t left = nd.x, right = nd.y, top = nd.z, bottom = nd.w;
+            const int32_t mid = (left + right + 1) >> 1;
+            const bool serial = has && bottom - top < SK_SERIAL;
+            Key best = ~(Key)0;
+            if (serial) {
+                for (int32_t k = top; k <= bottom; ++k) {
                     const Key key = rpack<Key>(cell(k, mid), k, shift);
                     best = key < best ? key : best;
                 }
-                best = rwarp_min(best);
-                const int32_t bv = rval<Key>(best, shift), bk = rk<Key>(best, shift);
-                if (lane == 0) {
-                    reach[mid] = bv;
-                    trace[mid] = bk;
+            }
+            unsigned lm = __ballot_sync(0xffffffffu, has && !serial);
+            while (lm) {  // long split ranges: whole warp, one node at a time
+                const int src = __ffs(lm) - 1;
+                lm &= lm - 1;
+                const int32_t t0 = __shfl_sync(0xffffffffu, top, src);
+                const int32_t t1 = __shfl_sync(0xffffffffu, bottom, src);
+                const int32_t mj = __shfl_sync(0xffffffffu, mid, src);
+                Key b2 = ~(Key)0;
+                for (int32_t k = t0 + lane; k <= t1; k += 32) {
+                    const Key key = rpack<Key>(cell(k, mj), k, shift);
+                    b2 = key < b2 ? key : b2;
                 }
-                if (bv != inf) {
-                    kfin = max(kfin, mid);
-                    if (mid + 1 <= right) {
-                        if (lane == 0) stk[sp] = make_int4(mid + 1, right, bk, bottom);
-                        ++sp;
-                    }
-                    right = mid - 1;
-                    bottom = bk;
-                } else {
-                    for (int32_t q = mid + 1 + lane; q <= right; q += 32) {
-                        reach[q] = inf;
-                        trace[q] = top;
-                    }
-                    right = mid - 1;
+                b2 = rwarp_min(b2);
+                if (lane == src) best = b2;
+            }
+            const int32_t bv = rval<Key>(best, shift), bk = rk<Key>(best, shift);
+            const bool fin = has && bv != inf;
+            if (has) {
+                reach[mid] = bv;
+                trace[mid] = bk;
+            }
+            if (fin) kfin = max(kfin, mid);
+            // INF node: (mid, right] gets (INF, top); short fills serially
+            const bool infn = has && !fin && right > mid;
+            const bool longfill = infn && right - mid > SK_SERIAL;
+            if (infn && !longfill)
+                for (int32_t q = mid + 1; q <= right; ++q) {
+                    reach[q] = inf;
+                    trace[q] = top;
+                }
+            unsigned fm = __ballot_sync(0xffffffffu, longfill);
+            while (fm) {
+                const int src = __ffs(fm) - 1;
+                fm &= fm - 1;
+                const int32_t q0 = __shfl_sync(0xffffffffu, mid, src) + 1;
+                const int32_t q1 = __shfl_sync(0xffffffffu, right, src);
+                const int32_t tt = __shfl_sync(0xffffffffu, top, src);
+                for (int32_t q = q0 + lane; q <= q1; q += 32) {
+                    reach[q] = inf;
+                    trace[q] = tt;
                 }
             }
-            if (sp == 0) break;
+            // children: finite -> [left, mid-1] (bottom = bk), [mid+1, right]
+            // (top = bk); INF -> [left, mid-1] with the node's own split range
+            const bool cl = has && mid - 1 >= left;
+            const bool cr = fin && right >= mid + 1;
+            const int nc = (int)cl + (int)cr;
+            int pos = nc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, pos, o);
+                if (lane >= o) pos += t;
+            }
+            const int tot = __shfl_sync(0xffffffffu, pos, 31);
+            pos = sp + pos - nc;
+            if (cr) stk[pos++] = make_int4(mid + 1, right, bk, bottom);
+            if (cl) stk[pos] = make_int4(left, mid - 1, top, fin ? bk : bottom);
+            sp += tot;
             __syncwarp();
-            const int4 e = stk[--sp];
-            __syncwarp();
-            left = e.x;
-            right = e.y;
-            top = e.z;
-            bottom = e.w;
         }
     }
     if (lane == 0 && kfin >= 0) atomicMax(&kfin_sh, kfin);
@@ -401,10 +452,17 @@ int launch_skeleton(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, b
     const int64_t n1 = (int64_t)c.n + 1;
     const int32_t nsk = (int32_t)((n1 - 1 + stride - 1) / stride) + 1;
     const unsigned blocks = (unsigned)(nsk * (int64_t)ndesc);
+    const size_t smem = (size_t)SK_WARPS * SK_STACK * sizeof(int4);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(skeleton_kernel<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(skeleton_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
     if (key64)
-        skeleton_kernel<uint64_t><<<blocks, 32 * SK_WARPS, 0, s>>>(descs, ndesc, c, shift, stride, nsk);
+        skeleton_kernel<uint64_t><<<blocks, 32 * SK_WARPS, smem, s>>>(descs, ndesc, c, shift, stride, nsk);
     else
-        skeleton_kernel<uint32_t><<<blocks, 32 * SK_WARPS, 0, s>>>(descs, ndesc, c, shift, stride, nsk);
+        skeleton_kernel<uint32_t><<<blocks, 32 * SK_WARPS, smem, s>>>(descs, ndesc, c, shift, stride, nsk);
     LCSG_LAUNCH_CHECK();
     return 0;
 }
