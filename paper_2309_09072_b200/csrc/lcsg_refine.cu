@@ -190,6 +190,7 @@ __global__ void __launch_bounds__(32 * SK_WARPS)
             const bool serial = has && bottom - top < SK_SERIAL;
             Key best = ~(Key)0;
             if (serial) {
+#pragma unroll 4
                 for (int32_t k = top; k <= bottom; ++k) {
                     const Key key = rpack<Key>(cell(k, mid), k, shift);
                     best = key < best ? key : best;

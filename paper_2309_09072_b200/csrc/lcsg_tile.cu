@@ -607,13 +607,24 @@ int launch_block_refine(const CombineDesc *descs, int32_t ndesc, Ctx c, int shif
         attr = true;
     }
     if (rs == 1) {  // last stage: lean kernel (finite cells only; finalize writes INF)
+        // shared-memory carveout (percent; -1 = driver default) of the fine
+        // kernels.  Long strings: 72% keeps ~27 resident CTAs per SM and leaves
+        // the rest to L1, which holds the U rows the interleave windows re-read
+        // (cfg5 28.16 -> 27.69 ms, cfg4 6.78 -> 6.58; 50% and 80% both lose).
+        // Short strings (n < 8193) keep the max-occupancy default (cfg2/cfg3
+        // lose 5% at 72%).  Set at every launch: the attribute is per function.
+        const char *co_env = getenv("LCSG_FINE_CARVEOUT");
+        const int carve = co_env ? atoi(co_env) : (n1 > 8193 ? 72 : -1);
 #define FINE_LAUNCH(K, SCV)                                                                      \
-    column_refine_fine_kernel<K, SCV><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift, S, \
-                                                                      nblk, w1div)
-        // compile-time S (32 registers, full occupancy) pays on narrower
-        // tables; the widest levels keep the runtime-S build (measured)
+    do {                                                                                         \
+        cudaFuncSetAttribute(column_refine_fine_kernel<K, SCV>,                                  \
+                             cudaFuncAttributePreferredSharedMemoryCarveout, carve);             \
+        column_refine_fine_kernel<K, SCV><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift, \
+                                                                          S, nblk, w1div);       \
+    } while (0)
+        // compile-time S (32 registers) for every width up to LCSG_FINE_SC_MAXW1
         const char *sc_env = getenv("LCSG_FINE_SC_MAXW1");
-        const int sc_max = sc_env ? atoi(sc_env) : 2049;
+        const int sc_max = sc_env ? atoi(sc_env) : INT_MAX;
         const int32_t Ssel = maxw1 <= sc_max ? S : 0;
         if (key64) {
             switch (Ssel) {
@@ -631,12 +642,22 @@ int launch_block_refine(const CombineDesc *descs, int32_t ndesc, Ctx c, int shif
             }
         }
 #undef FINE_LAUNCH
-    } else if (key64) {
-        column_refine_kernel<uint64_t><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift, S,
-                                                                       rs, nblk, w1div);
     } else {
-        column_refine_kernel<uint32_t><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift, S,
-                                                                       rs, nblk, w1div);
+        // carveout of the row-step stages (measured: 50% for long strings,
+        // 30% below n = 8193; cfg5 -0.03 ms, cfg2 -0.1 ms vs the default)
+        const char *co_env = getenv("LCSG_RS_CARVEOUT");
+        const int carve = co_env ? atoi(co_env) : (n1 > 8193 ? 50 : 30);
+        if (key64) {
+            cudaFuncSetAttribute(column_refine_kernel<uint64_t>,
+                                 cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+            column_refine_kernel<uint64_t><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift, S,
+                                                                           rs, nblk, w1div);
+        } else {
+            cudaFuncSetAttribute(column_refine_kernel<uint32_t>,
+                                 cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+            column_refine_kernel<uint32_t><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift, S,
+                                                                           rs, nblk, w1div);
+        }
     }
     LCSG_LAUNCH_CHECK();
     return 0;
