@@ -15,6 +15,7 @@ ap.add_argument("cfg", type=int)
 ap.add_argument("settings", nargs="*")
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--levels", action="store_true")
+ap.add_argument("--lowmem", action="store_true", help="build without stored traces")
 args = ap.parse_intermixed_args()
 lib = _lib.load()
 a, b = workloads.generate(args.cfg)
@@ -33,7 +34,7 @@ sub = np.empty(k, np.uint8); rp = np.empty(k, np.int32); cp = np.empty(k, np.int
 def solve():
     h = ctypes.c_void_p()
     _lib.check(lib.lcsg_build_device(d_rows.data_ptr(), m, d_cols.data_ptr(), n, 1, m + 1,
-                                     _lib.LCSG_WITH_TRACE | _lib.LCSG_TIMING, 0, sp,
+                                     (0 if args.lowmem else _lib.LCSG_WITH_TRACE) | _lib.LCSG_TIMING, 0, sp,
                                      ctypes.byref(h)), "build")
     length = ctypes.c_int32()
     _lib.check(lib.lcsg_extract(h, -1, ctypes.byref(length), sub.ctypes.data, rp.ctypes.data,
