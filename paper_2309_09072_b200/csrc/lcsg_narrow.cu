@@ -17,6 +17,9 @@
 // the column (replayed from the finite traces, O(log w)), and (INF, 0) beyond
 // colhi = min(w, kmax_U + wstar_L) (_kernel.pyx:79-82).  Rows leave through a
 // shared-memory transpose as one contiguous, fully coalesced block.
+#include <cstdlib>
+#include <type_traits>
+
 #include "lcsg_internal.cuh"
 
 namespace lcsg {
@@ -303,6 +306,179 @@ __global__ void __launch_bounds__(NarrowGeom<P>::NT)
     if (tid == 0 && s_wstar >= 0) atomicMax(out_wstar, s_wstar);
 }
 
+// narrow<32> with a ROLLED k-chunk loop (32-bit keys only).  The unrolled
+// fold of narrow_combine_kernel<32> is ~107 KB of code -- a fifth of its
+// stall samples were instruction-cache misses.  Here one chunk body serves
+// every chunk: the thread's keys live in a 40-register window W[t] = output
+// column 8c + t; chunk c (splits k = 8c .. 8c+7) folds into W[kk + e] with
+// compile-time indices, after which columns 8c .. 8c+7 are final (later
+// splits only reach larger columns).  They are parked in the thread's own U
+// row -- slots 8c .. 8c+7 were that chunk's split columns, never read again
+// (chunk c+1 reads row 0's slot 8(c+1) as its window base, untouched) -- and
+// the window shifts by 8.  Split k = 32 (the last chunk) is folded after the
+// loop, then the epilogue is the same as narrow_combine_kernel's.  Same
+// candidates and first-wins keys, hence the same output.
+constexpr int R32_NT = 128, R32_KC = 8, R32_PT = 33, R32_BYTES = 72 * 1024;
+
+__global__ void __launch_bounds__(R32_NT)
+    narrow32_roll_kernel(const CombineDesc *__restrict__ descs, Ctx c, int shift, int32_t bpd,
+                         int32_t lcap) {
+    constexpr int P = 32, PT = R32_PT, NT = R32_NT, ROWS = R32_NT, KC = R32_KC;
+    constexpr int NCH = 5;  // chunks 0..3 rolled (k < 32), chunk 4 = k 32
+    extern __shared__ int32_t nsm[];
+    int32_t *sU = nsm;
+    int32_t *sL = nsm + ROWS * PT;
+    __shared__ int32_t s_xmax[NCH], s_wstar;
+    const int32_t di = blockIdx.x / bpd;
+    const int64_t i0 = (int64_t)(blockIdx.x - di * bpd) * ROWS;
+    const CombineDesc &d = descs[di];
+    const int64_t n1 = (int64_t)c.n + 1;
+    const int nr = (int)min((int64_t)ROWS, n1 - i0);
+    const int32_t inf = c.inf;
+    const TabAcc U = resolve(d.U, c), L = resolve(d.L, c);
+    const int tid = threadIdx.x;
+    const int r = tid;
+    const uint32_t mul = 1u << (shift & 31);
+    if (tid < NCH) s_xmax[tid] = 0;
+    if (tid == 0) s_wstar = -1;
+    stage_rows<PT, NT>(sU, U, i0, nr, inf);
+    __syncthreads();
+    int32_t ku = -1;
+    int32_t xlast[NCH];
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) xlast[ch] = 0;
+    if (r < nr) {
+#pragma unroll
+        for (int k = 0; k <= P; ++k) {
+            const int32_t x = sU[r * PT + k];
+            if (x < inf) {
+                ku = k;
+                xlast[k / KC] = max(xlast[k / KC], x);
+            }
+        }
+    }
+#pragma unroll
+    for (int ch = 0; ch < NCH; ++ch) {
+        const int32_t m = __reduce_max_sync(0xffffffffu, xlast[ch]);
+        if ((tid & 31) == 0 && m > 0) atomicMax(&s_xmax[ch], m);
+    }
+    uint32_t W[40];
+#pragma unroll
+    for (int t = 0; t < 40; ++t) W[t] = ~0u;
+    // chunk body: fold splits k0 + kk (kk < nk) into W[kk + e]
+    auto chunk = [&](int ch, int k0, auto nk_c) {
+        constexpr int NK = decltype(nk_c)::value;
+        __syncthreads();  // previous window consumed / U block and xmax ready
+        const int32_t x0 = sU[k0];
+        if (x0 >= inf) return false;  // CTA-uniform: no finite split from here on
+        const int64_t base = (int64_t)x0 - 1;
+        const int64_t need = (int64_t)s_xmax[ch] - base;
+        for (int64_t w0 = 0; w0 < need; w0 += lcap) {
+            const int32_t nL = (int32_t)min(need - w0, (int64_t)lcap);
+            if (w0 > 0) __syncthreads();
+            const int sh = L.nx ? 0 : (int)(((uintptr_t)(L.reach + (base + w0) * PT) >> 2) & 3);
+            int32_t *sLw = sL + sh;
+            stage_rows_call<PT, NT>(sLw, L, base + w0, nL, inf);
+            __syncthreads();
+            if (r < nr) {
+#pragma unroll
+                for (int kk = 0; kk < NK; ++kk) {
+                    const int32_t k = k0 + kk;
+                    const int32_t x = sU[r * PT + k];
+                    const int64_t lr = (int64_t)x - 1 - base - w0;
+                    if (x < inf && lr >= 0 && lr < nL) {
+                        const int32_t *row = sLw + lr * PT;
+#pragma unroll
+                        for (int e = 0; e <= P; ++e) {
+                            const uint32_t key = (uint32_t)row[e] * mul + (uint32_t)k;
+                            W[kk + e] = key < W[kk + e] ? key : W[kk + e];
+                        }
+                    }
+                }
+            }
+            if (w0 + lcap < need) __syncthreads();
+        }
+        return true;
+    };
+    // every chunk runs (a chunk without finite splits folds nothing) so that
+    // the window always ends aligned to column 32
+#pragma unroll 1
+    for (int ch = 0; ch < 4; ++ch) {
+        chunk(ch, ch * KC, std::integral_constant<int, KC>{});
+        // columns 8ch .. 8ch+7 are final: park them in this row's consumed
+        // split slots, shift the window (also when the chunk had no split:
+        // the parked keys are then the untouched ~0 = INF)
+        __syncthreads();  // every thread is done reading row 0's slot 8ch
+        if (r < nr) {
+#pragma unroll
+            for (int t = 0; t < KC; ++t) sU[r * PT + ch * KC + t] = (int32_t)W[t];
+        }
+#pragma unroll
+        for (int t = 0; t < 32; ++t) W[t] = W[t + 8];
+#pragma unroll
+        for (int t = 32; t < 40; ++t) W[t] = ~0u;
+    }
+    chunk(4, 32, std::integral_constant<int, 1>{});
+    __syncthreads();  // folds done; sU keeps the parked columns 0..31
+    const int32_t w1 = d.w1, w = w1 - 1;
+    const int32_t wstar_l = *d.L.wstar;
+    int32_t *__restrict__ const out_kmax = d.out_kmax;
+    int32_t *__restrict__ const out_reach = d.out_reach;
+    int32_t *__restrict__ const out_trace = d.out_trace;
+    int32_t *const out_wstar = d.out_wstar;
+    // all 65 keys of the row into registers (the staging area overlaps sU)
+    uint32_t best[2 * P + 1];
+    if (r < nr) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) best[j] = (uint32_t)sU[r * PT + j];
+    }
+#pragma unroll
+    for (int j = 32; j <= 2 * P; ++j) best[j] = W[j - 32];
+    __syncthreads();
+    int32_t *sR = nsm;
+    int32_t *sT = nsm + ROWS * w1;
+    int32_t wmax = -1;
+    if (r < nr) {
+        int32_t *rr = sR + r * w1;
+        int32_t *tr = sT + r * w1;
+        int32_t kfin = -1;
+#pragma unroll
+        for (int j = 0; j <= 2 * P; ++j) {
+            if (j <= w) {
+                const int32_t v = (int32_t)(best[j] >> shift);
+                if (v < inf) kfin = j;
+                rr[j] = v < inf ? v : inf;
+                tr[j] = (int32_t)(best[j] & ((1u << shift) - 1));
+            }
+        }
+        inf_traces(tr, kfin, min(w, ku + wstar_l), w);
+        out_kmax[i0 + r] = kfin;
+        wmax = kfin;
+    }
+    wmax = __reduce_max_sync(0xffffffffu, wmax);
+    if ((tid & 31) == 0 && wmax >= 0) atomicMax(&s_wstar, wmax);
+    __syncthreads();
+    const int tot = nr * w1;
+    copy_out<NT>(out_reach + i0 * w1, sR, tot);
+    if (out_trace) copy_out<NT>(out_trace + i0 * w1, sT, tot);
+    if (tid == 0 && s_wstar >= 0) atomicMax(out_wstar, s_wstar);
+}
+
+static int launch_narrow32_roll(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift,
+                                cudaStream_t s) {
+    cudaError_t e = cudaFuncSetAttribute(narrow32_roll_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, R32_BYTES);
+    if (e != cudaSuccess) return (int)e;
+    const int64_t n1 = (int64_t)c.n + 1;
+    const int32_t bpd = (int32_t)((n1 + R32_NT - 1) / R32_NT);
+    const int32_t lcap = (int32_t)(R32_BYTES / 4 - R32_NT * R32_PT - 3) / R32_PT;
+    const int64_t blocks = (int64_t)ndesc * bpd;
+    if (blocks == 0) return 0;
+    if (blocks >= ((int64_t)1 << 31)) return (int)cudaErrorInvalidConfiguration;
+    narrow32_roll_kernel<<<(unsigned)blocks, R32_NT, R32_BYTES, s>>>(descs, c, shift, bpd, lcap);
+    return (int)cudaGetLastError();
+}
+
 // Height-1 combines (two leaf children, rows of 3 cells): the fold needs only
 // NX_a[i], NX_b[i] and NX_b[NX_a[i] - 1] (breakout.py:37-55 leaf rows), all in
 // L2 (26 symbols x (n+1) ints), so nothing is staged on the way in; rows
@@ -425,7 +601,13 @@ int launch_narrow(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, boo
         NARROW_CASE(4)
         NARROW_CASE(8)
         NARROW_CASE(16)
-        NARROW_CASE(32)
+        case 32: {
+            const char *e = getenv("LCSG_NARROW32_ROLL");
+            if (!key64 && (e == nullptr || atoi(e) != 0))
+                return launch_narrow32_roll(descs, ndesc, c, shift, s);
+            return key64 ? launch_narrow_t<32, uint64_t>(descs, ndesc, c, shift, s)
+                         : launch_narrow_t<32, uint32_t>(descs, ndesc, c, shift, s);
+        }
         default:
             return (int)cudaErrorInvalidValue;
     }

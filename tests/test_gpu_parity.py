@@ -301,6 +301,9 @@ def test_skeleton_refine_strides(stride, monkeypatch):
     {"LCSG_THREAD_MAX_W1": "33"},                           # 65-wide tables through the column path
     {"LCSG_LEAFPAIR": "0"},                                 # height-1 combines through the staged kernel
     {"LCSG_NARROW": "0", "LCSG_THREAD_MAX_W1": "65"},
+    {"LCSG_NARROW32_ROLL": "0"},                            # unrolled-fold narrow<32> kernel
+    {"LCSG_FINE_SC_MAXW1": "0"},                            # runtime block size in the fine kernel
+    {"LCSG_SKELETON_STRIDE": "512", "LCSG_COL_BLOCK": "8"},  # row-step 64 / 8 / 1 stages
 ])
 def test_refinement_variants(env, monkeypatch):
     """Every geometry / schedule of the wide-table combine is bit-exact."""
