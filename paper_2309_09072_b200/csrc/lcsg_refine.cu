@@ -257,6 +257,8 @@ __global__ void __launch_bounds__(32 * SK_WARPS)
             __syncwarp();
         }
     }
+    // the batched DFS leaves each lane with the largest finite mid IT visited
+    kfin = __reduce_max_sync(0xffffffffu, kfin);
     if (lane == 0 && kfin >= 0) atomicMax(&kfin_sh, kfin);
     for (int32_t q = colhi + 1 + (int32_t)threadIdx.x; q <= w; q += 32 * SK_WARPS) {
         reach[q] = inf;

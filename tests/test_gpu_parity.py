@@ -330,6 +330,28 @@ def test_refinement_variants(env, monkeypatch):
             assert nodes[idx].wstar == exp.wstar
 
 
+def test_skeleton_cta_wide_rows(monkeypatch):
+    """The CTA-per-row skeleton kernel on long rows (batched per-warp DFS with
+    many nodes per batch, so the largest finite column is found by lanes other
+    than lane 0): every node's kmax, wstar, reach and trace stay bit-exact."""
+    monkeypatch.setenv("LCSG_SKEL_THREAD_MAX_W1", "1")
+    monkeypatch.setenv("LCSG_SKEL_WARP_MAX_W1", "1")
+    rng = np.random.default_rng(777)
+    for m, n, sigma in ((300, 2500, 26), (520, 1800, 4), (260, 3100, 20)):
+        a, b = workloads.random_pair(rng, m, n, sigma)
+        g = L.GridModel(a, b)
+        t = O.OracleTree(a, b)
+        nodes = gpu_tree_nodes(L.build_cost_table(g, 1, m + 1))
+        for idx in range(len(t)):
+            exp = t.node(idx)
+            if exp.upper < 0:
+                continue
+            np.testing.assert_array_equal(nodes[idx].kmax, exp.kmax, err_msg=f"{m}x{n} {idx}")
+            assert nodes[idx].wstar == exp.wstar
+            np.testing.assert_array_equal(nodes[idx].reach, exp.reach, err_msg=f"{m}x{n} {idx}")
+            np.testing.assert_array_equal(nodes[idx].trace, exp.trace, err_msg=f"{m}x{n} {idx}")
+
+
 def test_narrow_window_overflow():
     """Sparse matches (256 symbols, long columns): the reach of a 16-row slab
     runs far past the narrow kernel's staged L window, so its direct-read path
