@@ -486,7 +486,9 @@ static int launch_narrow32_roll(const CombineDesc *descs, int32_t ndesc, Ctx c, 
 // traces and INF replay as narrow_combine_kernel<1>.
 constexpr int LP_NT = 256, LP_RPT = 4, LP_ROWS = LP_NT * LP_RPT;
 
-template <typename Key>
+// W3: the output width is 3 (n >= 2, every leaf is 2 wide) -- constant
+// shared-memory offsets and a closed-form INF replay
+template <typename Key, bool W3>
 __global__ void __launch_bounds__(LP_NT)
     narrow_leafpair_kernel(const CombineDesc *__restrict__ descs, Ctx c, int shift, int32_t bpd) {
     __shared__ int32_t sR[LP_ROWS * 3], sT[LP_ROWS * 3];
@@ -498,7 +500,7 @@ __global__ void __launch_bounds__(LP_NT)
     const int nr = (int)min((int64_t)LP_ROWS, n1 - i0);
     const int32_t inf = c.inf;
     const TabAcc U = resolve(d.U, c), L = resolve(d.L, c);  // both leaves
-    const int32_t w1 = d.w1, w = w1 - 1;
+    const int32_t w1 = W3 ? 3 : d.w1, w = w1 - 1;
     const int32_t wstar_l = *d.L.wstar;
     int32_t *__restrict__ const out_kmax = d.out_kmax;
     int32_t *__restrict__ const out_reach = d.out_reach;
@@ -513,9 +515,9 @@ __global__ void __launch_bounds__(LP_NT)
         if (r >= nr) continue;
         const int64_t i = i0 + r;
         // U row (i+1, NX_a[i]); L row x-1: (x, NX_b[x-1])
-        const int32_t xa = U.w1 > 1 ? __ldg(U.nx + i) : inf;
-        const int32_t nb = L.w1 > 1 ? __ldg(L.nx + i) : inf;
-        const int32_t nb2 = (xa < inf && L.w1 > 1) ? __ldg(L.nx + (xa - 1)) : inf;
+        const int32_t xa = (W3 || U.w1 > 1) ? __ldg(U.nx + i) : inf;
+        const int32_t nb = (W3 || L.w1 > 1) ? __ldg(L.nx + i) : inf;
+        const int32_t nb2 = (xa < inf && (W3 || L.w1 > 1)) ? __ldg(L.nx + (xa - 1)) : inf;
         // candidates (k, e): j = k + e; first-wins min of packed keys
         Key best[3];
         best[0] = npack((Key)(uint32_t)(i + 1), 0, shift, mul);  // (0,0): L[i][0] = i+1
@@ -536,7 +538,18 @@ __global__ void __launch_bounds__(LP_NT)
                 tr[j] = (int32_t)(best[j] & (((Key)1 << shift) - 1));
             }
         }
-        inf_traces(tr, kfin, min(w, ku + wstar_l), w);  // Alg. 1 replay for INF cells
+        if (W3) {
+            // Alg. 1 over [0, colhi], w = 2: its first mid is 1; finite (kfin
+            // >= 1) -> the only INF cell left is 2, in the node with top =
+            // trace[1]; INF -> every INF node keeps top = 0; 0 beyond colhi
+            const int32_t colhi = min(2, ku + wstar_l);
+            const int32_t top = kfin >= 1 ? tr[1] : 0;
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+                if (j > kfin) tr[j] = j <= colhi ? top : 0;
+        } else {
+            inf_traces(tr, kfin, min(w, ku + wstar_l), w);  // Alg. 1 replay for INF cells
+        }
         out_kmax[i] = kfin;
         wmax = max(wmax, kfin);
     }
@@ -556,10 +569,14 @@ int launch_narrow_leafpair(const CombineDesc *descs, int32_t ndesc, Ctx c, int s
     const int64_t blocks = (int64_t)ndesc * bpd;
     if (blocks == 0) return 0;
     if (blocks >= ((int64_t)1 << 31)) return (int)cudaErrorInvalidConfiguration;
-    if (key64)
-        narrow_leafpair_kernel<uint64_t><<<(unsigned)blocks, LP_NT, 0, s>>>(descs, c, shift, bpd);
-    else
-        narrow_leafpair_kernel<uint32_t><<<(unsigned)blocks, LP_NT, 0, s>>>(descs, c, shift, bpd);
+    const bool w3 = c.n >= 2;  // every height-1 output is 3 wide
+    if (key64) {
+        if (w3) narrow_leafpair_kernel<uint64_t, true><<<(unsigned)blocks, LP_NT, 0, s>>>(descs, c, shift, bpd);
+        else narrow_leafpair_kernel<uint64_t, false><<<(unsigned)blocks, LP_NT, 0, s>>>(descs, c, shift, bpd);
+    } else {
+        if (w3) narrow_leafpair_kernel<uint32_t, true><<<(unsigned)blocks, LP_NT, 0, s>>>(descs, c, shift, bpd);
+        else narrow_leafpair_kernel<uint32_t, false><<<(unsigned)blocks, LP_NT, 0, s>>>(descs, c, shift, bpd);
+    }
     return (int)cudaGetLastError();
 }
 

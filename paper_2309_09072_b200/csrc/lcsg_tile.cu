@@ -402,6 +402,7 @@ __global__ void __launch_bounds__(CR_THREADS)
                         outk = kl;
                     } else {
                         Key best = ~(Key)0;
+#pragma unroll 2
                         for (int32_t k = kl; k <= kh; ++k) {
                             const int32_t x = __ldg(Uc + k);  // finite: k <= kmax_c
                             const int32_t v = __ldg(Lr + ((uint32_t)(x - 1) * (uint32_t)lw1 + (j - k)));
