@@ -105,10 +105,12 @@ __device__ __forceinline__ void window_counts_n(const int32_t *Uc, int32_t D, in
 }
 
 
-template <typename Key>
+// SC: block size as a compile-time constant (0: runtime S)
+template <typename Key, int SC = 0>
 __global__ void __launch_bounds__(CR_THREADS)
     column_refine_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int shift,
-                         int32_t S, int32_t rs, int32_t nblk, FastDiv w1div) {
+                         int32_t S_arg, int32_t rs, int32_t nblk, FastDiv w1div) {
+    const int32_t S = SC > 0 ? SC : S_arg;
     // local row r of block blk is the actual row i0 + r*rs (rs = row step of
     // this refinement stage); rows 0 and S of the block are already known
     extern __shared__ int32_t csm[];
@@ -653,6 +655,11 @@ int launch_block_refine(const CombineDesc *descs, int32_t ndesc, Ctx c, int shif
                                  cudaFuncAttributePreferredSharedMemoryCarveout, carve);
             column_refine_kernel<uint64_t><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift, S,
                                                                            rs, nblk, w1div);
+        } else if (S == 8) {
+            cudaFuncSetAttribute(column_refine_kernel<uint32_t, 8>,
+                                 cudaFuncAttributePreferredSharedMemoryCarveout, carve);
+            column_refine_kernel<uint32_t, 8><<<blocks, CR_THREADS, smem, s>>>(descs, ndesc, c, shift,
+                                                                              S, rs, nblk, w1div);
         } else {
             cudaFuncSetAttribute(column_refine_kernel<uint32_t>,
                                  cudaFuncAttributePreferredSharedMemoryCarveout, carve);
