@@ -435,12 +435,10 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             // strings: skeleton rows every 512 (row steps 64, 8, 1) -- cheaper
             // than the skeleton bisection every 64 rows (measured: cfg5 levels
             // s = 128..512 gain 0.4 ms; cfg4's 2..8-combine levels lose 0.2)
-            // the widest tables (w1 > 8193): skeleton rows every 32 (measured
-            // -0.1 ms on the cfg5 root now that skeleton rows are batched)
+            // (re-measured after the fine-kernel changes: the root's stride 32
+            // now loses 0.14 ms against 64, so only the 512 rule remains)
             const bool dflt = getenv("LCSG_SKELETON_STRIDE") == nullptr && n1 > 8193;
-            const int stride_def = (dflt && maxw1 <= 513 && L.count >= 32) ? 512
-                                   : (dflt && maxw1 > 8193)                  ? 32
-                                                                             : skel_stride;
+            const int stride_def = (dflt && maxw1 <= 513 && L.count >= 32) ? 512 : skel_stride;
             const int stride_h =
                 std::max(2, env_int(("LCSG_SKEL_STRIDE_H" + hs).c_str(), stride_def));
             int32_t S = 1;

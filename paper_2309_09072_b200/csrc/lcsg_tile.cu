@@ -641,6 +641,7 @@ int launch_block_refine(const CombineDesc *descs, int32_t ndesc, Ctx c, int shif
                 case 2: FINE_LAUNCH(uint32_t, 2); break;
                 case 4: FINE_LAUNCH(uint32_t, 4); break;
                 case 8: FINE_LAUNCH(uint32_t, 8); break;
+                case 16: FINE_LAUNCH(uint32_t, 16); break;
                 default: FINE_LAUNCH(uint32_t, 0); break;
             }
         }
