@@ -682,7 +682,14 @@ int launch_finalize_rows(const CombineDesc *descs, int32_t ndesc, Ctx c, int32_t
     const dim3 blocks((unsigned)((warps + FN_WARPS - 1) / FN_WARPS),
                       (unsigned)std::min<int32_t>(ndesc, 65535), (unsigned)((ndesc + 65534) / 65535));
     if (maxw1 <= 65536)
+    {
+        // shared-memory carveout 75%: fewer resident CTAs, L1 for the reach
+        // cells the replay probes (cfg5 26.55 -> 26.40 ms vs the default)
+        const char *e = getenv("LCSG_FIN_CARVEOUT");
+        cudaFuncSetAttribute(finalize_rows_kernel<18>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             e ? atoi(e) : 75);
         finalize_rows_kernel<18><<<blocks, 32 * FN_WARPS, 0, s>>>(descs, ndesc, c, S, rpw);
+    }
     else
         finalize_rows_kernel<34><<<blocks, 32 * FN_WARPS, 0, s>>>(descs, ndesc, c, S, rpw);
     LCSG_LAUNCH_CHECK();
