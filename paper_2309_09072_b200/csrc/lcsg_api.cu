@@ -572,6 +572,9 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             BCKL(launch_narrow_leafpair(dd, L.count, c, L.shift, L.key64, s));
         else if (L.kind == 3)
             BCKL(launch_skeleton(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s));
+        else if (L.kind == 6 && L.stride_or_delta > 1 && t->with_trace &&
+                 env_int("LCSG_SKEL_WARP_BATCHED", 1))
+            BCKL(launch_skeleton_warp(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s));
         else if (L.kind == 5 || L.kind == 6)
             BCKL(launch_combine(L.kind == 5 ? 0 : 1, dd, L.count, c, L.shift, L.key64, s,
                                 L.stride_or_delta));

@@ -127,6 +127,9 @@ int launch_narrow(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, boo
 // skeleton rows 0, S, 2S, ..., n by exact Alg. 1 (one CTA per row)
 int launch_skeleton(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
                     int32_t stride, cudaStream_t s);
+// skeleton rows, one warp per row (batched DFS; slab children, w1 <= 257)
+int launch_skeleton_warp(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
+                         int32_t stride, cudaStream_t s);
 // refinement pass: rows (2t+1)*delta from rows (2t)*delta and (2t+2)*delta
 int launch_refine(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
                   int32_t delta, cudaStream_t s);

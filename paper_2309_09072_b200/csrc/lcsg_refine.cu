@@ -81,6 +81,98 @@ constexpr int SK_STACK = 320;
 constexpr int SK_SLACK = 40;
 constexpr int SK_SERIAL = 24;  // ranges / fills up to this length: one lane
 
+// Batched DFS of Alg. 1's bisection tree (_kernel.pyx:28-60) for one output
+// row, by one warp: every node's (value, trace) depends only on its own
+// (left, right, top, bottom), so the stack is consumed in batches -- lane l
+// takes the l-th node, scans a short split range [top, bottom] serially, and
+// long ranges / long INF fills are done cooperatively by the whole warp.
+// Outputs equal the reference's node by node (order-independent writes to
+// disjoint cells); the batch turns the one-node-at-a-time chain of dependent
+// gathers (~colhi nodes per row) into ~colhi / 32 steps.  `stk` holds `sp`
+// pending nodes on entry; each lane's kfin gets the largest finite mid it saw.
+template <typename Key, typename Cell>
+__device__ __forceinline__ void batched_dfs(int4 *stk, int sp, const Cell &cell, int32_t *reach,
+                                            int32_t *trace, int32_t inf, int shift, int lane,
+                                            int32_t &kfin) {
+    while (sp > 0) {
+        const int nb = min(min(sp, 32), max(1, SK_STACK - SK_SLACK - sp));
+        const bool has = lane < nb;
+        const int4 nd = has ? stk[sp - nb + lane] : make_int4(1, 0, 0, -1);
+        __syncwarp();
+        sp -= nb;
+        const int32_t left = nd.x, right = nd.y, top = nd.z, bottom = nd.w;
+        const int32_t mid = (left + right + 1) >> 1;
+        const bool serial = has && bottom - top < SK_SERIAL;
+        Key best = ~(Key)0;
+        if (serial) {
+#pragma unroll 4
+            for (int32_t k = top; k <= bottom; ++k) {
+                const Key key = rpack<Key>(cell(k, mid), k, shift);
+                best = key < best ? key : best;
+            }
+        }
+        unsigned lm = __ballot_sync(0xffffffffu, has && !serial);
+        while (lm) {  // long split ranges: whole warp, one node at a time
+            const int src = __ffs(lm) - 1;
+            lm &= lm - 1;
+            const int32_t t0 = __shfl_sync(0xffffffffu, top, src);
+            const int32_t t1 = __shfl_sync(0xffffffffu, bottom, src);
+            const int32_t mj = __shfl_sync(0xffffffffu, mid, src);
+            Key b2 = ~(Key)0;
+            for (int32_t k = t0 + lane; k <= t1; k += 32) {
+                const Key key = rpack<Key>(cell(k, mj), k, shift);
+                b2 = key < b2 ? key : b2;
+            }
+            b2 = rwarp_min(b2);
+            if (lane == src) best = b2;
+        }
+        const int32_t bv = rval<Key>(best, shift), bk = rk<Key>(best, shift);
+        const bool fin = has && bv != inf;
+        if (has) {
+            reach[mid] = bv;
+            trace[mid] = bk;
+        }
+        if (fin) kfin = max(kfin, mid);
+        // INF node: (mid, right] gets (INF, top); short fills serially
+        const bool infn = has && !fin && right > mid;
+        const bool longfill = infn && right - mid > SK_SERIAL;
+        if (infn && !longfill)
+            for (int32_t q = mid + 1; q <= right; ++q) {
+                reach[q] = inf;
+                trace[q] = top;
+            }
+        unsigned fm = __ballot_sync(0xffffffffu, longfill);
+        while (fm) {
+            const int src = __ffs(fm) - 1;
+            fm &= fm - 1;
+            const int32_t q0 = __shfl_sync(0xffffffffu, mid, src) + 1;
+            const int32_t q1 = __shfl_sync(0xffffffffu, right, src);
+            const int32_t tt = __shfl_sync(0xffffffffu, top, src);
+            for (int32_t q = q0 + lane; q <= q1; q += 32) {
+                reach[q] = inf;
+                trace[q] = tt;
+            }
+        }
+        // children: finite -> [left, mid-1] (bottom = bk), [mid+1, right]
+        // (top = bk); INF -> [left, mid-1] with the node's own split range
+        const bool cl = has && mid - 1 >= left;
+        const bool cr = fin && right >= mid + 1;
+        const int nc = (int)cl + (int)cr;
+        int pos = nc;
+    #pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(0xffffffffu, pos, o);
+            if (lane >= o) pos += t;
+        }
+        const int tot = __shfl_sync(0xffffffffu, pos, 31);
+        pos = sp + pos - nc;
+        if (cr) stk[pos++] = make_int4(mid + 1, right, bk, bottom);
+        if (cl) stk[pos] = make_int4(left, mid - 1, top, fin ? bk : bottom);
+        sp += tot;
+        __syncwarp();
+    }
+}
+
 template <typename Key>
 __global__ void __launch_bounds__(32 * SK_WARPS)
     skeleton_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int shift,
@@ -166,14 +258,7 @@ __global__ void __launch_bounds__(32 * SK_WARPS)
         }
         cur ^= 1;
     }
-    // --- one warp per remaining sub-tree, up to 32 independent nodes per
-    // step: every node's (value, trace) depends only on its own (left, right,
-    // top, bottom), so the DFS stack is consumed in batches -- lane l takes
-    // the l-th node, scans a short split range [top, bottom] serially, and
-    // long ranges / long INF fills are done cooperatively by the whole warp.
-    // Outputs equal the reference's node by node (order-independent writes to
-    // disjoint cells); the batch turns the one-node-at-a-time chain of
-    // dependent gathers (~colhi nodes per row) into ~colhi / 32 steps.
+    // --- one warp per remaining sub-tree: batched DFS (up to 32 nodes a step)
     const int nf = nfront[cur];
     if (wid < nf) {
         int4 *stk = stk_all + wid * SK_STACK;
@@ -181,83 +266,7 @@ __global__ void __launch_bounds__(32 * SK_WARPS)
         if (lane == 0) stk[0] = front[cur][wid];
         sp = 1;
         __syncwarp();
-        while (sp > 0) {
-            const int nb = min(min(sp, 32), max(1, SK_STACK - SK_SLACK - sp));
-            const bool has = lane < nb;
-            const int4 nd = has ? stk[sp - nb + lane] : make_int4(1, 0, 0, -1);
-            __syncwarp();
-            sp -= nb;
-            const int32_t left = nd.x, right = nd.y, top = nd.z, bottom = nd.w;
-            const int32_t mid = (left + right + 1) >> 1;
-            const bool serial = has && bottom - top < SK_SERIAL;
-            Key best = ~(Key)0;
-            if (serial) {
-#pragma unroll 4
-                for (int32_t k = top; k <= bottom; ++k) {
-                    const Key key = rpack<Key>(cell(k, mid), k, shift);
-                    best = key < best ? key : best;
-                }
-            }
-            unsigned lm = __ballot_sync(0xffffffffu, has && !serial);
-            while (lm) {  // long split ranges: whole warp, one node at a time
-                const int src = __ffs(lm) - 1;
-                lm &= lm - 1;
-                const int32_t t0 = __shfl_sync(0xffffffffu, top, src);
-                const int32_t t1 = __shfl_sync(0xffffffffu, bottom, src);
-                const int32_t mj = __shfl_sync(0xffffffffu, mid, src);
-                Key b2 = ~(Key)0;
-                for (int32_t k = t0 + lane; k <= t1; k += 32) {
-                    const Key key = rpack<Key>(cell(k, mj), k, shift);
-                    b2 = key < b2 ? key : b2;
-                }
-                b2 = rwarp_min(b2);
-                if (lane == src) best = b2;
-            }
-            const int32_t bv = rval<Key>(best, shift), bk = rk<Key>(best, shift);
-            const bool fin = has && bv != inf;
-            if (has) {
-                reach[mid] = bv;
-                trace[mid] = bk;
-            }
-            if (fin) kfin = max(kfin, mid);
-            // INF node: (mid, right] gets (INF, top); short fills serially
-            const bool infn = has && !fin && right > mid;
-            const bool longfill = infn && right - mid > SK_SERIAL;
-            if (infn && !longfill)
-                for (int32_t q = mid + 1; q <= right; ++q) {
-                    reach[q] = inf;
-                    trace[q] = top;
-                }
-            unsigned fm = __ballot_sync(0xffffffffu, longfill);
-            while (fm) {
-                const int src = __ffs(fm) - 1;
-                fm &= fm - 1;
-                const int32_t q0 = __shfl_sync(0xffffffffu, mid, src) + 1;
-                const int32_t q1 = __shfl_sync(0xffffffffu, right, src);
-                const int32_t tt = __shfl_sync(0xffffffffu, top, src);
-                for (int32_t q = q0 + lane; q <= q1; q += 32) {
-                    reach[q] = inf;
-                    trace[q] = tt;
-                }
-            }
-            // children: finite -> [left, mid-1] (bottom = bk), [mid+1, right]
-            // (top = bk); INF -> [left, mid-1] with the node's own split range
-            const bool cl = has && mid - 1 >= left;
-            const bool cr = fin && right >= mid + 1;
-            const int nc = (int)cl + (int)cr;
-            int pos = nc;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int t = __shfl_up_sync(0xffffffffu, pos, o);
-                if (lane >= o) pos += t;
-            }
-            const int tot = __shfl_sync(0xffffffffu, pos, 31);
-            pos = sp + pos - nc;
-            if (cr) stk[pos++] = make_int4(mid + 1, right, bk, bottom);
-            if (cl) stk[pos] = make_int4(left, mid - 1, top, fin ? bk : bottom);
-            sp += tot;
-            __syncwarp();
-        }
+        batched_dfs<Key>(stk, sp, cell, reach, trace, inf, shift, lane, kfin);
     }
     // the batched DFS leaves each lane with the largest finite mid IT visited
     kfin = __reduce_max_sync(0xffffffffu, kfin);
@@ -476,6 +485,76 @@ int launch_skeleton(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, b
         skeleton_kernel<uint64_t><<<blocks, 32 * SK_WARPS, smem, s>>>(descs, ndesc, c, shift, stride, nsk);
     else
         skeleton_kernel<uint32_t><<<blocks, 32 * SK_WARPS, smem, s>>>(descs, ndesc, c, shift, stride, nsk);
+    LCSG_LAUNCH_CHECK();
+    return 0;
+}
+
+// Skeleton rows of the narrower wide tables (w1 <= 257): one warp per row,
+// the whole Alg. 1 tree by the batched DFS (the per-node chain of
+// combine_warp_kernel took ~colhi dependent steps per row).
+constexpr int SKW_WARPS = 4;
+
+template <typename Key>
+__global__ void __launch_bounds__(32 * SKW_WARPS)
+    skeleton_warp_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int shift,
+                         int32_t stride, int32_t nsk) {
+    extern __shared__ int4 stkw_all[];  // SKW_WARPS x SK_STACK
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int64_t gw = blockIdx.x * (int64_t)SKW_WARPS + wid;
+    const int64_t di = gw / nsk;
+    if (di >= ndesc) return;  // warp-uniform
+    const int32_t r = (int32_t)(gw - di * nsk);
+    const int64_t n1 = (int64_t)c.n + 1;
+    const int64_t i = (r == nsk - 1) ? n1 - 1 : (int64_t)r * stride;
+    const CombineDesc &d = descs[di];
+    const int32_t inf = c.inf;
+    const int32_t *__restrict__ Urow = d.U.reach + (uint32_t)i * (uint32_t)d.U.w1;
+    const int32_t *__restrict__ Lr = d.L.reach;
+    const uint32_t lw1 = (uint32_t)d.L.w1;
+    const int32_t w = d.w1 - 1, wl = d.L.w1 - 1;
+    const int32_t kmaxU = __ldg(d.U.kmax + i);
+    const int32_t colhi = min(w, kmaxU + *d.L.wstar);
+    int32_t *reach = d.out_reach + (uint32_t)i * (uint32_t)d.w1;
+    int32_t *trace = d.out_trace + (uint32_t)i * (uint32_t)d.w1;
+    auto cell = [&](int32_t k, int32_t j) -> int32_t {
+        const int32_t x = __ldg(Urow + k);
+        if (k > j || x >= inf || j - k > wl) return inf;
+        return __ldg(Lr + ((uint32_t)(x - 1) * lw1 + (uint32_t)(j - k)));
+    };
+    int4 *stk = stkw_all + wid * SK_STACK;
+    if (lane == 0) stk[0] = make_int4(0, colhi, 0, kmaxU);
+    __syncwarp();
+    int32_t kfin = -1;
+    batched_dfs<Key>(stk, 1, cell, reach, trace, inf, shift, lane, kfin);
+    for (int32_t q = colhi + 1 + lane; q <= w; q += 32) {
+        reach[q] = inf;
+        trace[q] = 0;
+    }
+    kfin = __reduce_max_sync(0xffffffffu, kfin);
+    if (lane == 0) {
+        d.out_kmax[i] = kfin;
+        atomicMax(d.out_wstar, kfin);
+    }
+}
+
+int launch_skeleton_warp(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
+                         int32_t stride, cudaStream_t s) {
+    if (ndesc <= 0) return 0;
+    const int64_t n1 = (int64_t)c.n + 1;
+    const int32_t nsk = (int32_t)((n1 - 1 + stride - 1) / stride) + 1;
+    const int64_t warps = (int64_t)nsk * ndesc;
+    const unsigned blocks = (unsigned)((warps + SKW_WARPS - 1) / SKW_WARPS);
+    const size_t smem = (size_t)SKW_WARPS * SK_STACK * sizeof(int4);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(skeleton_warp_kernel<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(skeleton_warp_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    if (key64)
+        skeleton_warp_kernel<uint64_t><<<blocks, 32 * SKW_WARPS, smem, s>>>(descs, ndesc, c, shift, stride, nsk);
+    else
+        skeleton_warp_kernel<uint32_t><<<blocks, 32 * SKW_WARPS, smem, s>>>(descs, ndesc, c, shift, stride, nsk);
     LCSG_LAUNCH_CHECK();
     return 0;
 }

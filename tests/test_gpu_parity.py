@@ -304,6 +304,7 @@ def test_skeleton_refine_strides(stride, monkeypatch):
     {"LCSG_NARROW32_ROLL": "0"},                            # unrolled-fold narrow<32> kernel
     {"LCSG_FINE_SC_MAXW1": "0"},                            # runtime block size in the fine kernel
     {"LCSG_SKELETON_STRIDE": "512", "LCSG_COL_BLOCK": "8"},  # row-step 64 / 8 / 1 stages
+    {"LCSG_SKEL_WARP_BATCHED": "0"},                        # per-node warp DFS for w1 <= 257 skeletons
 ])
 def test_refinement_variants(env, monkeypatch):
     """Every geometry / schedule of the wide-table combine is bit-exact."""
