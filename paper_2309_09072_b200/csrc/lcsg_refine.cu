@@ -79,7 +79,7 @@ constexpr int SK_WARPS = 8;
 // < 34), so it never overflows
 constexpr int SK_STACK = 320;
 constexpr int SK_SLACK = 40;
-constexpr int SK_SERIAL = 24;  // ranges / fills up to this length: one lane
+constexpr int SK_SERIAL = 12;  // ranges / fills up to this length: one lane (24/48 slower, 6/8 equal)
 
 // Batched DFS of Alg. 1's bisection tree (_kernel.pyx:28-60) for one output
 // row, by one warp: every node's (value, trace) depends only on its own
