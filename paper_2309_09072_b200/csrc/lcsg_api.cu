@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -196,8 +197,11 @@ int32_t build_tree(lcsg_tree_s *t, int32_t top, int32_t bottom, int32_t depth) {
     return (int32_t)t->nodes.size() - 1;
 }
 
+thread_local std::vector<NodeH> t_spare_nodes;  // node storage reused across solves
+
 void destroy(lcsg_tree_s *t) {
     if (!t) return;
+    if (t->nodes.capacity() > t_spare_nodes.capacity()) t->nodes.swap(t_spare_nodes);
     int prev = -1;
     cudaGetDevice(&prev);
     cudaSetDevice(t->device);
@@ -213,6 +217,41 @@ void destroy(lcsg_tree_s *t) {
     delete t;
 }
 
+// Host staging of the plan metadata, one pinned buffer per host thread and
+// device, reused across solves: no page faults on a fresh multi-MB vector
+// (they cost 1-3 ms per cfg5 solve) and a truly asynchronous upload.  `done`
+// is recorded after the upload; the next solve on this thread waits on it
+// before rewriting the buffer (it has normally long completed).
+struct MetaStage {
+    char *buf = nullptr;
+    size_t cap = 0;
+    cudaEvent_t done = nullptr;
+    int device = -1;
+};
+
+char *meta_stage_acquire(MetaStage &ms, int device, size_t bytes) {
+    if (ms.device != device && ms.buf) {  // another device: start over
+        cudaFreeHost(ms.buf);
+        if (ms.done) cudaEventDestroy(ms.done);
+        ms = MetaStage();
+    }
+    ms.device = device;
+    if (ms.done) cudaEventSynchronize(ms.done);  // previous upload finished
+    if (ms.cap < bytes) {
+        if (ms.buf) cudaFreeHost(ms.buf);
+        ms.cap = std::max(bytes, ms.cap * 2);
+        if (cudaMallocHost((void **)&ms.buf, ms.cap) != cudaSuccess) {
+            ms.buf = nullptr;
+            ms.cap = 0;
+            return nullptr;
+        }
+    }
+    if (!ms.done && cudaEventCreateWithFlags(&ms.done, cudaEventDisableTiming) != cudaSuccess)
+        ms.done = nullptr;
+    return ms.buf;
+}
+
+thread_local MetaStage t_meta_stage;
 int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *cols, bool cols_dev,
                int64_t n, int32_t top_row, int32_t bottom_row, uint32_t flags, int device,
                void *stream, lcsg_handle *out) {
@@ -250,6 +289,15 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             if (cudaEventCreate(&e) != cudaSuccess) t->ev_ok = false;
     }
 
+    // LCSG_HOST_PROFILE=1: host-side phase times of this call to stderr
+    const bool hprof = env_int("LCSG_HOST_PROFILE", 0) != 0;
+    auto hclock = [] { return std::chrono::steady_clock::now(); };
+    auto hms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+        return std::chrono::duration<double, std::milli>(b - a).count();
+    };
+    const auto h0 = hclock();
+    t->nodes.swap(t_spare_nodes);  // keeps the capacity of an earlier solve
+    t->nodes.clear();
     t->nodes.reserve(2 * t->m_slab);
     t->root = build_tree(t, top_row, bottom_row, 0);
     const int32_t nn = (int32_t)t->nodes.size();
@@ -347,7 +395,9 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     size_t meta_end = off;
     t->arena_bytes = off;
 
+    const auto h1 = hclock();
     cudaError_t ae = cudaMallocAsync((void **)&t->arena, t->arena_bytes, t->stream);
+    const auto h2 = hclock();
     if (ae != cudaSuccess) {
         t->arena = nullptr;
         destroy(t);
@@ -373,12 +423,19 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     t->d_leaf_rows = (int32_t *)(A + o_lrows);
 
     // ---- host-side metadata: level plan, descriptors, walk nodes ----
-    std::vector<char> meta(meta_end - o_meta, 0);
-    CombineDesc *hd = (CombineDesc *)(meta.data() + (o_desc - o_meta));
-    WalkNode *hw = (WalkNode *)(meta.data() + (o_walk - o_meta));
-    int32_t *hids = (int32_t *)(meta.data() + (o_wids - o_meta));
-    int32_t *hln = (int32_t *)(meta.data() + (o_lnodes - o_meta));
-    int32_t *hlr = (int32_t *)(meta.data() + (o_lrows - o_meta));
+    const size_t meta_bytes = meta_end - o_meta;
+    std::vector<char> meta_fallback;
+    char *meta = meta_stage_acquire(t_meta_stage, device, meta_bytes);
+    const bool meta_pinned = meta != nullptr;
+    if (!meta_pinned) {
+        meta_fallback.assign(meta_bytes, 0);
+        meta = meta_fallback.data();
+    }  // no zero-fill: every descriptor / walk-node field is written below
+    CombineDesc *hd = (CombineDesc *)(meta + (o_desc - o_meta));
+    WalkNode *hw = (WalkNode *)(meta + (o_walk - o_meta));
+    int32_t *hids = (int32_t *)(meta + (o_wids - o_meta));
+    int32_t *hln = (int32_t *)(meta + (o_lnodes - o_meta));
+    int32_t *hlr = (int32_t *)(meta + (o_lrows - o_meta));
 
     int32_t maxh = 0;
     for (auto &nd : t->nodes) maxh = std::max(maxh, nd.height);
@@ -481,36 +538,6 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             }
         }
     }
-    // walk nodes + depth lists of internal nodes
-    int32_t maxd = 0, maxku = 0;
-    for (int32_t id = 0; id < nn; ++id) {
-        const NodeH &nd = t->nodes[id];
-        WalkNode &w = hw[id];
-        w.top_row = nd.top_row - t->top_row + 1;  // relative: cols index = top_row - 1
-        w.bottom_row = nd.bottom_row;
-        w.upper = nd.upper;
-        w.lower = nd.lower;
-        w.w1 = nd.w1;
-        w.is_leaf = nd.upper < 0;
-        w.trace = (nd.upper >= 0 && t->with_trace) ? t->d_tables + nd.trace_off : nullptr;
-        if (nd.upper >= 0) {
-            w.U = t->tab(nd.upper);
-            w.L = t->tab(nd.lower);
-            maxku = std::max(maxku, t->nodes[nd.upper].w1 - 1);
-        }
-        maxd = std::max(maxd, nd.depth);
-    }
-    t->walk_shift = bits_for(maxku);
-    t->walk_key64 = vbits + t->walk_shift > 32;
-    int32_t wpos = 0;
-    std::vector<std::vector<int32_t>> by_depth(maxd + 1);
-    for (int32_t id = 0; id < nn; ++id)
-        if (t->nodes[id].upper >= 0) by_depth[t->nodes[id].depth].push_back(id);
-    for (int32_t dd = 0; dd <= maxd; ++dd) {
-        int32_t start = wpos;
-        for (const int32_t id : by_depth[dd]) hids[wpos++] = id;
-        if (wpos > start) t->depth_ranges.push_back({start, wpos - start});
-    }
     int32_t li = 0;
     for (int32_t id = 0; id < nn; ++id)
         if (t->nodes[id].upper < 0) {
@@ -519,6 +546,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             ++li;
         }
 
+    const auto h3 = hclock();
     // ---- enqueue: inputs, metadata, leaf step, levels ----
     const cudaStream_t s = t->stream;
 #define BCK(call)                            \
@@ -551,9 +579,13 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     if (n > 0)
         BCK(cudaMemcpyAsync(t->d_cols, cols, (size_t)n,
                             cols_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
-    BCK(cudaMemcpyAsync(A + o_meta, meta.data(), meta.size(), cudaMemcpyHostToDevice, s));
-    t->h2d_bytes = (int64_t)meta.size() + (rows_dev ? 0 : t->m_slab) + (cols_dev ? 0 : n);
-    // the pageable-host copy above is staged synchronously, so `meta` may die
+    // descriptors and leaf lists now; the walk nodes (extraction only) are
+    // built and uploaded after the level launches, overlapping the combines
+    BCK(cudaMemcpyAsync(A + o_meta, meta, o_walk - o_meta, cudaMemcpyHostToDevice, s));
+    BCK(cudaMemcpyAsync(A + o_lnodes, meta + (o_lnodes - o_meta), meta_end - o_lnodes,
+                        cudaMemcpyHostToDevice, s));
+    t->h2d_bytes = (int64_t)meta_bytes + (rows_dev ? 0 : t->m_slab) + (cols_dev ? 0 : n);
+    // a pageable fallback copy is staged synchronously, so `meta_fallback` may die
     BCK(cudaMemsetAsync(t->d_node_wstar, 0, (size_t)nn * 4, s));
     BCKL(launch_nx(t->d_cols, (int32_t)n, t->d_nx, t->d_sym_wstar, s));
     BCKL(launch_leaf_wstar(t->d_rows, t->d_leaf_nodes, t->d_leaf_rows, t->nleaves,
@@ -587,6 +619,47 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             BCKL(launch_refine(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s));
     }
     if (t->timing && t->ev_ok) BCK(cudaEventRecord(t->ev[2], s));
+    // walk nodes + depth lists of internal nodes
+    int32_t maxd = 0, maxku = 0;
+    for (int32_t id = 0; id < nn; ++id) {
+        const NodeH &nd = t->nodes[id];
+        WalkNode &w = hw[id];
+        w.top_row = nd.top_row - t->top_row + 1;  // relative: cols index = top_row - 1
+        w.bottom_row = nd.bottom_row;
+        w.upper = nd.upper;
+        w.lower = nd.lower;
+        w.w1 = nd.w1;
+        w.is_leaf = nd.upper < 0;
+        w.trace = (nd.upper >= 0 && t->with_trace) ? t->d_tables + nd.trace_off : nullptr;
+        if (nd.upper >= 0) {
+            w.U = t->tab(nd.upper);
+            w.L = t->tab(nd.lower);
+            maxku = std::max(maxku, t->nodes[nd.upper].w1 - 1);
+        } else {
+            w.U = TabDev{};
+            w.L = TabDev{};
+        }
+        maxd = std::max(maxd, nd.depth);
+    }
+    t->walk_shift = bits_for(maxku);
+    t->walk_key64 = vbits + t->walk_shift > 32;
+    int32_t wpos = 0;
+    std::vector<std::vector<int32_t>> by_depth(maxd + 1);
+    for (int32_t id = 0; id < nn; ++id)
+        if (t->nodes[id].upper >= 0) by_depth[t->nodes[id].depth].push_back(id);
+    for (int32_t dd = 0; dd <= maxd; ++dd) {
+        int32_t start = wpos;
+        for (const int32_t id : by_depth[dd]) hids[wpos++] = id;
+        if (wpos > start) t->depth_ranges.push_back({start, wpos - start});
+    }
+    BCK(cudaMemcpyAsync(A + o_walk, meta + (o_walk - o_meta), o_lnodes - o_walk,
+                        cudaMemcpyHostToDevice, s));
+    if (meta_pinned && t_meta_stage.done) BCK(cudaEventRecord(t_meta_stage.done, s));
+    if (hprof) {
+        const auto h4 = hclock();
+        fprintf(stderr, "lcsg_build host ms: tree+layout %.3f  arena %.3f  metadata %.3f  enqueue %.3f\n",
+                hms(h0, h1), hms(h1, h2), hms(h2, h3), hms(h3, h4));
+    }
 #undef BCK
 #undef BCKL
     *out = t;
