@@ -437,6 +437,82 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     int32_t *hln = (int32_t *)(meta + (o_lnodes - o_meta));
     int32_t *hlr = (int32_t *)(meta + (o_lrows - o_meta));
 
+    // ---- enqueue: inputs, leaf step; then the levels as they are planned ----
+    const cudaStream_t s = t->stream;
+#define BCK(call)                            \
+    do {                                     \
+        int r__ = 0;                         \
+        cudaError_t e__ = (call);            \
+        if (e__ != cudaSuccess) {            \
+            r__ = fail(LCSG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e__)); \
+            destroy(t);                      \
+            return r__;                      \
+        }                                    \
+    } while (0)
+#define BCKL(call)                           \
+    do {                                     \
+        int e__ = (call);                    \
+        if (e__ != 0) {                      \
+            int r__ = fail(LCSG_ECUDA, std::string("launch ") + #call + ": " +      \
+                                           cudaGetErrorString((cudaError_t)e__));   \
+            destroy(t);                      \
+            return r__;                      \
+        }                                    \
+        ++t->launches;                       \
+    } while (0)
+
+    int32_t li = 0;
+    for (int32_t id = 0; id < nn; ++id)
+        if (t->nodes[id].upper < 0) {
+            hln[li] = id;
+            hlr[li] = t->nodes[id].leaf_row;
+            ++li;
+        }
+
+    if (t->timing && t->ev_ok) BCK(cudaEventRecord(t->ev[0], s));
+    const uint8_t *rows_slab = rows + (top_row - 1);
+    if (t->m_slab > 0)
+        BCK(cudaMemcpyAsync(t->d_rows, rows_slab, (size_t)t->m_slab,
+                            rows_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    if (n > 0)
+        BCK(cudaMemcpyAsync(t->d_cols, cols, (size_t)n,
+                            cols_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    // leaf lists now; each level's descriptors are uploaded as soon as that
+    // level is planned (its kernels start while the host plans the next), the
+    // walk nodes (extraction only) after the last level
+    BCK(cudaMemcpyAsync(A + o_lnodes, meta + (o_lnodes - o_meta), meta_end - o_lnodes,
+                        cudaMemcpyHostToDevice, s));
+    t->h2d_bytes = (int64_t)meta_bytes + (rows_dev ? 0 : t->m_slab) + (cols_dev ? 0 : n);
+    // a pageable fallback copy is staged synchronously, so `meta_fallback` may die
+    BCK(cudaMemsetAsync(t->d_node_wstar, 0, (size_t)nn * 4, s));
+    BCKL(launch_nx(t->d_cols, (int32_t)n, t->d_nx, t->d_sym_wstar, s));
+    BCKL(launch_leaf_wstar(t->d_rows, t->d_leaf_nodes, t->d_leaf_rows, t->nleaves,
+                           t->d_sym_wstar, t->d_node_wstar, s));
+    bool ev1_done = false;  // ev[1]: just before the first level's descriptors
+    const Ctx c = t->ctx();
+    auto launch_entry = [&](const LaunchH &L) -> int {
+        const CombineDesc *dd = t->d_descs + L.desc_off;
+        if (L.kind <= 1) return launch_combine(L.kind, dd, L.count, c, L.shift, L.key64, s);
+        if (L.kind == 9) return launch_combine_staged(dd, L.count, c, L.shift, L.key64, s);
+        if (L.kind == 10)
+            return launch_narrow(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s);
+        if (L.kind == 11) return launch_narrow_leafpair(dd, L.count, c, L.shift, L.key64, s);
+        if (L.kind == 3)
+            return launch_skeleton(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s);
+        if (L.kind == 6 && L.stride_or_delta > 1 && t->with_trace &&
+            env_int("LCSG_SKEL_WARP_BATCHED", 1))
+            return launch_skeleton_warp(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s);
+        if (L.kind == 5 || L.kind == 6)
+            return launch_combine(L.kind == 5 ? 0 : 1, dd, L.count, c, L.shift, L.key64, s,
+                                  L.stride_or_delta);
+        if (L.kind == 7)
+            return launch_block_refine(dd, L.count, c, L.shift, L.key64, L.stride_or_delta,
+                                       L.wpr_log2, L.ustride, s);
+        if (L.kind == 8) return launch_finalize_rows(dd, L.count, c, L.stride_or_delta, s, L.ustride);
+        if (refine_rows(n1, L.stride_or_delta) > 0)
+            return launch_refine(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s);
+        return -1;  // no launch
+    };
     int32_t maxh = 0;
     for (auto &nd : t->nodes) maxh = std::max(maxh, nd.height);
     const int vbits = bits_for(t->inf);
@@ -445,7 +521,14 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     std::vector<std::vector<int32_t>> by_height(maxh + 1);
     for (int32_t id = 0; id < nn; ++id)
         if (t->nodes[id].upper >= 0) by_height[t->nodes[id].height].push_back(id);
+    // levels are flushed (descriptors copied, kernels launched) in three
+    // groups -- the first level, the next two, the rest -- so the GPU starts
+    // early and runs while the host plans, with only three extra copies in
+    // the stream (one copy per level cost ~0.1 ms of gaps between kernels)
+    int32_t level_di = 0, nplanned = 0;
+    size_t level_plan = 0;
     for (int32_t h = 1; h <= maxh; ++h) {
+        const int32_t h_di = di;
         for (int kind = 0; kind < 3; ++kind) {
             int32_t start = di;
             int32_t maxk = 0, maxw1 = 0, maxkl = 0;
@@ -537,87 +620,31 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
                 t->plan.push_back(P);
             }
         }
-    }
-    int32_t li = 0;
-    for (int32_t id = 0; id < nn; ++id)
-        if (t->nodes[id].upper < 0) {
-            hln[li] = id;
-            hlr[li] = t->nodes[id].leaf_row;
-            ++li;
+        if (di > h_di) ++nplanned;
+        if (!(h == maxh || (di > h_di && (nplanned == 1 || nplanned == 3)))) continue;
+        if (!ev1_done && di > level_di) {
+            if (t->timing && t->ev_ok) BCK(cudaEventRecord(t->ev[1], s));
+            ev1_done = true;
         }
-
-    const auto h3 = hclock();
-    // ---- enqueue: inputs, metadata, leaf step, levels ----
-    const cudaStream_t s = t->stream;
-#define BCK(call)                            \
-    do {                                     \
-        int r__ = 0;                         \
-        cudaError_t e__ = (call);            \
-        if (e__ != cudaSuccess) {            \
-            r__ = fail(LCSG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e__)); \
-            destroy(t);                      \
-            return r__;                      \
-        }                                    \
-    } while (0)
-#define BCKL(call)                           \
-    do {                                     \
-        int e__ = (call);                    \
-        if (e__ != 0) {                      \
-            int r__ = fail(LCSG_ECUDA, std::string("launch ") + #call + ": " +      \
-                                           cudaGetErrorString((cudaError_t)e__));   \
-            destroy(t);                      \
-            return r__;                      \
-        }                                    \
-        ++t->launches;                       \
-    } while (0)
-
-    if (t->timing && t->ev_ok) BCK(cudaEventRecord(t->ev[0], s));
-    const uint8_t *rows_slab = rows + (top_row - 1);
-    if (t->m_slab > 0)
-        BCK(cudaMemcpyAsync(t->d_rows, rows_slab, (size_t)t->m_slab,
-                            rows_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
-    if (n > 0)
-        BCK(cudaMemcpyAsync(t->d_cols, cols, (size_t)n,
-                            cols_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
-    // descriptors and leaf lists now; the walk nodes (extraction only) are
-    // built and uploaded after the level launches, overlapping the combines
-    BCK(cudaMemcpyAsync(A + o_meta, meta, o_walk - o_meta, cudaMemcpyHostToDevice, s));
-    BCK(cudaMemcpyAsync(A + o_lnodes, meta + (o_lnodes - o_meta), meta_end - o_lnodes,
-                        cudaMemcpyHostToDevice, s));
-    t->h2d_bytes = (int64_t)meta_bytes + (rows_dev ? 0 : t->m_slab) + (cols_dev ? 0 : n);
-    // a pageable fallback copy is staged synchronously, so `meta_fallback` may die
-    BCK(cudaMemsetAsync(t->d_node_wstar, 0, (size_t)nn * 4, s));
-    BCKL(launch_nx(t->d_cols, (int32_t)n, t->d_nx, t->d_sym_wstar, s));
-    BCKL(launch_leaf_wstar(t->d_rows, t->d_leaf_nodes, t->d_leaf_rows, t->nleaves,
-                           t->d_sym_wstar, t->d_node_wstar, s));
-    if (t->timing && t->ev_ok) BCK(cudaEventRecord(t->ev[1], s));
-    const Ctx c = t->ctx();
-    for (const LaunchH &L : t->plan) {
-        const CombineDesc *dd = t->d_descs + L.desc_off;
-        if (L.kind <= 1)
-            BCKL(launch_combine(L.kind, dd, L.count, c, L.shift, L.key64, s));
-        else if (L.kind == 9)
-            BCKL(launch_combine_staged(dd, L.count, c, L.shift, L.key64, s));
-        else if (L.kind == 10)
-            BCKL(launch_narrow(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s));
-        else if (L.kind == 11)
-            BCKL(launch_narrow_leafpair(dd, L.count, c, L.shift, L.key64, s));
-        else if (L.kind == 3)
-            BCKL(launch_skeleton(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s));
-        else if (L.kind == 6 && L.stride_or_delta > 1 && t->with_trace &&
-                 env_int("LCSG_SKEL_WARP_BATCHED", 1))
-            BCKL(launch_skeleton_warp(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s));
-        else if (L.kind == 5 || L.kind == 6)
-            BCKL(launch_combine(L.kind == 5 ? 0 : 1, dd, L.count, c, L.shift, L.key64, s,
-                                L.stride_or_delta));
-        else if (L.kind == 7)
-            BCKL(launch_block_refine(dd, L.count, c, L.shift, L.key64, L.stride_or_delta,
-                                     L.wpr_log2, L.ustride, s));
-        else if (L.kind == 8)
-            BCKL(launch_finalize_rows(dd, L.count, c, L.stride_or_delta, s, L.ustride));
-        else if (refine_rows(n1, L.stride_or_delta) > 0)
-            BCKL(launch_refine(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s));
+        if (di > level_di)  // the group's descriptors, then its kernels
+            BCK(cudaMemcpyAsync(t->d_descs + level_di, hd + level_di,
+                                (size_t)(di - level_di) * sizeof(CombineDesc),
+                                cudaMemcpyHostToDevice, s));
+        for (size_t pi = level_plan; pi < t->plan.size(); ++pi) {
+            const int e = launch_entry(t->plan[pi]);
+            if (e > 0) {
+                const int r = fail(LCSG_ECUDA, std::string("launch: ") +
+                                                   cudaGetErrorString((cudaError_t)e));
+                destroy(t);
+                return r;
+            }
+            if (e == 0) ++t->launches;
+        }
+        level_di = di;
+        level_plan = t->plan.size();
     }
+    const auto h3 = hclock();
+    if (!ev1_done && t->timing && t->ev_ok) BCK(cudaEventRecord(t->ev[1], s));  // no combines
     if (t->timing && t->ev_ok) BCK(cudaEventRecord(t->ev[2], s));
     // walk nodes + depth lists of internal nodes
     int32_t maxd = 0, maxku = 0;
