@@ -228,8 +228,8 @@ def assemble_lcs(g: GridModel, path_cols: np.ndarray, *, device=None) -> LcsResu
     _lib.check(rc, "assemble_lcs")
     L = int(length.value)
     return LcsResult(length=L, subsequence=sub[:L].tobytes(),
-                     row_positions=tuple(int(x) for x in rp[:L]),
-                     col_positions=tuple(int(x) for x in cp[:L]))
+                     row_positions=tuple(rp[:L].tolist()),
+                     col_positions=tuple(cp[:L].tolist()))
 
 
 def lcs(
@@ -267,8 +267,8 @@ def lcs(
     _lib.check(rc, "lcs")
     L = int(length.value)
     return LcsResult(length=L, subsequence=sub[:L].tobytes(),
-                     row_positions=tuple(int(v) for v in pa[:L]),
-                     col_positions=tuple(int(v) for v in pb[:L]))
+                     row_positions=tuple(pa[:L].tolist()),
+                     col_positions=tuple(pb[:L].tolist()))
 
 
 def lcs_many(
