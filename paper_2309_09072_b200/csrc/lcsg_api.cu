@@ -477,9 +477,9 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     if (n > 0)
         BCK(cudaMemcpyAsync(t->d_cols, cols, (size_t)n,
                             cols_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
-    // leaf lists now; each level's descriptors are uploaded as soon as that
-    // level is planned (its kernels start while the host plans the next), the
-    // walk nodes (extraction only) after the last level
+    // leaf lists now; the level descriptors are uploaded in groups as they
+    // are planned (their kernels start while the host plans the next
+    // levels), the walk nodes (extraction only) after the last level
     BCK(cudaMemcpyAsync(A + o_lnodes, meta + (o_lnodes - o_meta), meta_end - o_lnodes,
                         cudaMemcpyHostToDevice, s));
     t->h2d_bytes = (int64_t)meta_bytes + (rows_dev ? 0 : t->m_slab) + (cols_dev ? 0 : n);
