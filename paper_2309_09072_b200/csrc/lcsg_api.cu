@@ -495,7 +495,8 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
         if (L.kind <= 1) return launch_combine(L.kind, dd, L.count, c, L.shift, L.key64, s);
         if (L.kind == 9) return launch_combine_staged(dd, L.count, c, L.shift, L.key64, s);
         if (L.kind == 10)
-            return launch_narrow(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s);
+            return launch_narrow(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s,
+                                 L.wpr_log2 != 0);
         if (L.kind == 11) return launch_narrow_leafpair(dd, L.count, c, L.shift, L.key64, s);
         if (L.kind == 3)
             return launch_skeleton(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s);
@@ -531,7 +532,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
         const int32_t h_di = di;
         for (int kind = 0; kind < 3; ++kind) {
             int32_t start = di;
-            int32_t maxk = 0, maxw1 = 0, maxkl = 0;
+            int32_t maxk = 0, maxw1 = 0, maxkl = 0, minw1 = INT32_MAX;
             for (const int32_t id : by_height[h]) {
                 const NodeH &nd = t->nodes[id];
                 if (nd.kind != kind) continue;
@@ -548,6 +549,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
                 maxk = std::max(maxk, t->nodes[nd.upper].w1 - 1);
                 maxkl = std::max(maxkl, t->nodes[nd.lower].w1 - 1);
                 maxw1 = std::max(maxw1, nd.w1);
+                minw1 = std::min(minw1, nd.w1);
             }
             if (di == start) continue;
             LaunchH L;
@@ -562,6 +564,8 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
                 if (kind == 0 && P > 0 && narrow_on) {
                     L.kind = 10;
                     L.stride_or_delta = P;
+                    L.wpr_log2 = (minw1 == maxw1 && maxw1 == 2 * P + 1 &&
+                                  env_int("LCSG_NARROW_FW", 1)) ? 1 : 0;  // full width
                     // height 1: both children are leaves
                     if (h == 1 && env_int("LCSG_LEAFPAIR", 1)) L.kind = 11;
                 }

@@ -123,7 +123,7 @@ int narrow_bucket(int32_t max_weight);  // P, or -1 when too wide
 int launch_narrow_leafpair(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
                            cudaStream_t s);
 int launch_narrow(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
-                  int32_t P, cudaStream_t s);
+                  int32_t P, cudaStream_t s, bool full_width = false);
 // skeleton rows 0, S, 2S, ..., n by exact Alg. 1 (one CTA per row)
 int launch_skeleton(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
                     int32_t stride, cudaStream_t s);

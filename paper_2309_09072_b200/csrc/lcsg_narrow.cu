@@ -157,7 +157,9 @@ __device__ __noinline__ void stage_rows_call(int32_t *dst, const TabAcc &t, int6
 }
 
 // P: bucket >= every U and L weight (w1 - 1) of the launch
-template <int P, typename Key>
+// FW: every combine of the launch has the full output width 2P+1 (each level
+// of a power-of-two tree) -- compile-time row pitch and bounds in the epilogue
+template <int P, typename Key, bool FW = false>
 __global__ void __launch_bounds__(NarrowGeom<P>::NT)
     narrow_combine_kernel(const CombineDesc *__restrict__ descs, Ctx c, int shift, int32_t bpd,
                           int32_t lcap) {
@@ -265,7 +267,7 @@ __global__ void __launch_bounds__(NarrowGeom<P>::NT)
         }
     }
     __syncthreads();  // sU and sL are reused as the output staging area below
-    const int32_t w1 = d.w1, w = w1 - 1;
+    const int32_t w1 = FW ? 2 * P + 1 : d.w1, w = w1 - 1;
     const int32_t wstar_l = *d.L.wstar;
     // descriptor fields in registers (stores below must not force re-loads)
     int32_t *__restrict__ const out_kmax = d.out_kmax;
@@ -580,12 +582,12 @@ int launch_narrow_leafpair(const CombineDesc *descs, int32_t ndesc, Ctx c, int s
     return (int)cudaGetLastError();
 }
 
-template <int P, typename Key>
+template <int P, typename Key, bool FW = false>
 static int launch_narrow_t(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift,
                            cudaStream_t s) {
     using G = NarrowGeom<P>;
     constexpr int PT = G::PITCH, BYTES = G::BYTES;
-    cudaError_t e = cudaFuncSetAttribute(narrow_combine_kernel<P, Key>,
+    cudaError_t e = cudaFuncSetAttribute(narrow_combine_kernel<P, Key, FW>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, BYTES);
     if (e != cudaSuccess) return (int)e;
     const int64_t n1 = (int64_t)c.n + 1;
@@ -595,8 +597,8 @@ static int launch_narrow_t(const CombineDesc *descs, int32_t ndesc, Ctx c, int s
     const int64_t blocks = (int64_t)ndesc * bpd;
     if (blocks == 0) return 0;
     if (blocks >= ((int64_t)1 << 31)) return (int)cudaErrorInvalidConfiguration;
-    narrow_combine_kernel<P, Key><<<(unsigned)blocks, G::NT, BYTES, s>>>(descs, c, shift, bpd,
-                                                                         lcap);
+    narrow_combine_kernel<P, Key, FW><<<(unsigned)blocks, G::NT, BYTES, s>>>(descs, c, shift, bpd,
+                                                                             lcap);
     return (int)cudaGetLastError();
 }
 
@@ -607,9 +609,10 @@ int narrow_bucket(int32_t max_weight) {
 }
 
 int launch_narrow(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
-                  int32_t P, cudaStream_t s) {
+                  int32_t P, cudaStream_t s, bool full_width) {
 #define NARROW_CASE(PP)                                                              \
     case PP:                                                                         \
+        if (full_width && !key64) return launch_narrow_t<PP, uint32_t, true>(descs, ndesc, c, shift, s); \
         return key64 ? launch_narrow_t<PP, uint64_t>(descs, ndesc, c, shift, s)      \
                      : launch_narrow_t<PP, uint32_t>(descs, ndesc, c, shift, s);
     switch (P) {

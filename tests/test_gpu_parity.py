@@ -305,6 +305,7 @@ def test_skeleton_refine_strides(stride, monkeypatch):
     {"LCSG_FINE_SC_MAXW1": "0"},                            # runtime block size in the fine kernel
     {"LCSG_SKELETON_STRIDE": "512", "LCSG_COL_BLOCK": "8"},  # row-step 64 / 8 / 1 stages
     {"LCSG_SKEL_WARP_BATCHED": "0"},                        # per-node warp DFS for w1 <= 257 skeletons
+    {"LCSG_NARROW_FW": "0"},                                # narrow kernels with a runtime row width
 ])
 def test_refinement_variants(env, monkeypatch):
     """Every geometry / schedule of the wide-table combine is bit-exact."""
