@@ -322,6 +322,7 @@ __global__ void __launch_bounds__(NarrowGeom<P>::NT)
 // candidates and first-wins keys, hence the same output.
 constexpr int R32_NT = 128, R32_KC = 8, R32_PT = 33, R32_BYTES = 72 * 1024;
 
+template <bool FW>  // FW: every output row is 65 wide (compile-time epilogue pitch)
 __global__ void __launch_bounds__(R32_NT)
     narrow32_roll_kernel(const CombineDesc *__restrict__ descs, Ctx c, int shift, int32_t bpd,
                          int32_t lcap) {
@@ -422,7 +423,7 @@ __global__ void __launch_bounds__(R32_NT)
     }
     chunk(4, 32, std::integral_constant<int, 1>{});
     __syncthreads();  // folds done; sU keeps the parked columns 0..31
-    const int32_t w1 = d.w1, w = w1 - 1;
+    const int32_t w1 = FW ? 2 * P + 1 : d.w1, w = w1 - 1;
     const int32_t wstar_l = *d.L.wstar;
     int32_t *__restrict__ const out_kmax = d.out_kmax;
     int32_t *__restrict__ const out_reach = d.out_reach;
@@ -466,9 +467,10 @@ __global__ void __launch_bounds__(R32_NT)
     if (tid == 0 && s_wstar >= 0) atomicMax(out_wstar, s_wstar);
 }
 
+template <bool FW>
 static int launch_narrow32_roll(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift,
                                 cudaStream_t s) {
-    cudaError_t e = cudaFuncSetAttribute(narrow32_roll_kernel,
+    cudaError_t e = cudaFuncSetAttribute(narrow32_roll_kernel<FW>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, R32_BYTES);
     if (e != cudaSuccess) return (int)e;
     const int64_t n1 = (int64_t)c.n + 1;
@@ -477,7 +479,7 @@ static int launch_narrow32_roll(const CombineDesc *descs, int32_t ndesc, Ctx c, 
     const int64_t blocks = (int64_t)ndesc * bpd;
     if (blocks == 0) return 0;
     if (blocks >= ((int64_t)1 << 31)) return (int)cudaErrorInvalidConfiguration;
-    narrow32_roll_kernel<<<(unsigned)blocks, R32_NT, R32_BYTES, s>>>(descs, c, shift, bpd, lcap);
+    narrow32_roll_kernel<FW><<<(unsigned)blocks, R32_NT, R32_BYTES, s>>>(descs, c, shift, bpd, lcap);
     return (int)cudaGetLastError();
 }
 
@@ -624,7 +626,8 @@ int launch_narrow(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, boo
         case 32: {
             const char *e = getenv("LCSG_NARROW32_ROLL");
             if (!key64 && (e == nullptr || atoi(e) != 0))
-                return launch_narrow32_roll(descs, ndesc, c, shift, s);
+                return full_width ? launch_narrow32_roll<true>(descs, ndesc, c, shift, s)
+                                  : launch_narrow32_roll<false>(descs, ndesc, c, shift, s);
             return key64 ? launch_narrow_t<32, uint64_t>(descs, ndesc, c, shift, s)
                          : launch_narrow_t<32, uint32_t>(descs, ndesc, c, shift, s);
         }
