@@ -199,6 +199,16 @@ int32_t build_tree(lcsg_tree_s *t, int32_t top, int32_t bottom, int32_t depth) {
 
 thread_local std::vector<NodeH> t_spare_nodes;  // node storage reused across solves
 
+// tree + table layout of the last shape solved on this host thread
+struct LayoutCache {
+    bool valid = false, with_trace = false;
+    int32_t top_row = 0, bottom_row = 0, root = -1, nleaves = 0, ncomb = 0, maxh0 = 0;
+    int64_t n = -1, tab_elems = 0, scratch_elems = 0;
+    int skel_stride = 0, thread_max_w1 = 0;
+    std::vector<NodeH> nodes;
+};
+thread_local LayoutCache t_layout;
+
 void destroy(lcsg_tree_s *t) {
     if (!t) return;
     if (t->nodes.capacity() > t_spare_nodes.capacity()) t->nodes.swap(t_spare_nodes);
@@ -296,10 +306,27 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
         return std::chrono::duration<double, std::milli>(b - a).count();
     };
     const auto h0 = hclock();
+    // skeleton stride: 32 rows for small column counts (the extra skeleton
+    // rows are cheaper than the latency of a coarser refinement stage), 64
+    // above (measured on cfg2/cfg3 vs cfg4/cfg5)
+    const int skel_stride = std::max(1, env_int("LCSG_SKELETON_STRIDE", default_skeleton_stride(n + 1)));
+    const int thread_max_w1 = env_int("LCSG_THREAD_MAX_W1", 65);
+    // the tree and the table layout depend only on the shape and the knobs:
+    // a repeated shape reuses them (saves ~0.5 ms of host work at cfg5 before
+    // the first kernel can be enqueued)
+    LayoutCache &lc = t_layout;
+    const bool layout_hit = lc.valid && lc.top_row == top_row && lc.bottom_row == bottom_row &&
+                            lc.n == n && lc.with_trace == t->with_trace &&
+                            lc.skel_stride == skel_stride && lc.thread_max_w1 == thread_max_w1;
     t->nodes.swap(t_spare_nodes);  // keeps the capacity of an earlier solve
     t->nodes.clear();
-    t->nodes.reserve(2 * t->m_slab);
-    t->root = build_tree(t, top_row, bottom_row, 0);
+    if (layout_hit) {
+        t->nodes.assign(lc.nodes.begin(), lc.nodes.end());
+        t->root = lc.root;
+    } else {
+        t->nodes.reserve(2 * t->m_slab);
+        t->root = build_tree(t, top_row, bottom_row, 0);
+    }
     const int32_t nn = (int32_t)t->nodes.size();
     const int64_t n1 = n + 1;
 
@@ -320,12 +347,6 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     size_t o_path = take((size_t)(t->m_slab + 1) * 4);
     size_t o_out = take((size_t)(1 + 2 * std::max<int64_t>(kmin, 1)) * 4);
     size_t o_sub = take((size_t)std::max<int64_t>(kmin, 1));
-    // int32 tables of every combine node
-    // skeleton stride: 32 rows for small column counts (the extra skeleton
-    // rows are cheaper than the latency of a coarser refinement stage), 64
-    // above (measured on cfg2/cfg3 vs cfg4/cfg5)
-    const int skel_stride = std::max(1, env_int("LCSG_SKELETON_STRIDE", default_skeleton_stride(n + 1)));
-    const int thread_max_w1 = env_int("LCSG_THREAD_MAX_W1", 65);
     const int skel_thread_max = env_int("LCSG_SKEL_THREAD_MAX_W1", 65);
     const int skel_warp_max = env_int("LCSG_SKEL_WARP_MAX_W1", 257);
     // refinement mode: tiled (default) or one launch per pass ("LCSG_REFINE_PASSES=1")
@@ -335,51 +356,73 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     int col_block = 1;
     while (col_block * 2 <= std::min(16, std::max(2, env_int("LCSG_COL_BLOCK", 8)))) col_block *= 2;
     size_t o_tab = off;
-    int64_t tab_elems = 0;
+    // int32 tables of every combine node
+    int64_t tab_elems = 0, scratch_elems = 0;
     int32_t ncomb = 0;
     int32_t maxh0 = 0;
-    for (auto &nd : t->nodes) {
-        if (nd.upper < 0) { t->nleaves++; continue; }
-        ++ncomb;
-        maxh0 = std::max(maxh0, nd.height);
-        const int32_t wu1 = t->nodes[nd.upper].w1;
-        // the refinement kernels read both children as materialised slabs
-        const bool kids_are_slabs =
-            t->nodes[nd.upper].upper >= 0 && t->nodes[nd.lower].upper >= 0;
-        nd.kind = (nd.w1 <= thread_max_w1 || !kids_are_slabs) ? 0 : 2;
-        // the refinement kernels use 32-bit element offsets into each table
-        if (nd.kind == 2 && n1 * (int64_t)nd.w1 >= ((int64_t)1 << 32)) nd.kind = 1;
-        (void)wu1;
-        if (skel_stride == 1 && nd.kind == 2) nd.kind = 1;
-        // every table starts on a 128-byte boundary (vector / async copies)
-        tab_elems = (tab_elems + 31) / 32 * 32;
-        nd.reach_off = tab_elems;
-        tab_elems += n1 * nd.w1;
-        if (t->with_trace) {
+    if (layout_hit) {
+        t->nleaves = lc.nleaves;
+        ncomb = lc.ncomb;
+        maxh0 = lc.maxh0;
+        tab_elems = lc.tab_elems;
+        scratch_elems = lc.scratch_elems;
+    } else {
+        for (auto &nd : t->nodes) {
+            if (nd.upper < 0) { t->nleaves++; continue; }
+            ++ncomb;
+            maxh0 = std::max(maxh0, nd.height);
+            const int32_t wu1 = t->nodes[nd.upper].w1;
+            // the refinement kernels read both children as materialised slabs
+            const bool kids_are_slabs =
+                t->nodes[nd.upper].upper >= 0 && t->nodes[nd.lower].upper >= 0;
+            nd.kind = (nd.w1 <= thread_max_w1 || !kids_are_slabs) ? 0 : 2;
+            // the refinement kernels use 32-bit element offsets into each table
+            if (nd.kind == 2 && n1 * (int64_t)nd.w1 >= ((int64_t)1 << 32)) nd.kind = 1;
+            (void)wu1;
+            if (skel_stride == 1 && nd.kind == 2) nd.kind = 1;
+            // every table starts on a 128-byte boundary (vector / async copies)
             tab_elems = (tab_elems + 31) / 32 * 32;
-            nd.trace_off = tab_elems;
+            nd.reach_off = tab_elems;
             tab_elems += n1 * nd.w1;
-        }
-    }
-    // kmax rows of every combine (written by the kernel that finishes each row:
-    // narrow / skeleton / finalize -- no initialisation needed)
-    for (auto &nd : t->nodes) {
-        if (nd.upper < 0) continue;
-        nd.kmax_off = tab_elems;
-        tab_elems += (n1 + 63) / 64 * 64;
-    }
-    // low-memory mode: the refinement passes still need this level's traces
-    // (they bound neighbouring rows); one scratch region reused level by level
-    int64_t scratch_elems = 0;
-    std::vector<int64_t> level_scratch(maxh0 + 1, 0);
-    if (!t->with_trace) {
-        for (auto &nd : t->nodes)
-            if (nd.upper >= 0 && nd.kind == 2) {
-                level_scratch[nd.height] = (level_scratch[nd.height] + 31) / 32 * 32;
-                nd.trace_off = level_scratch[nd.height];  // relative to the scratch base
-                level_scratch[nd.height] += n1 * nd.w1;
+            if (t->with_trace) {
+                tab_elems = (tab_elems + 31) / 32 * 32;
+                nd.trace_off = tab_elems;
+                tab_elems += n1 * nd.w1;
             }
-        for (int64_t v : level_scratch) scratch_elems = std::max(scratch_elems, v);
+        }
+        // kmax rows of every combine (written by the kernel that finishes each row:
+        // narrow / skeleton / finalize -- no initialisation needed)
+        for (auto &nd : t->nodes) {
+            if (nd.upper < 0) continue;
+            nd.kmax_off = tab_elems;
+            tab_elems += (n1 + 63) / 64 * 64;
+        }
+        // low-memory mode: the refinement passes still need this level's traces
+        // (they bound neighbouring rows); one scratch region reused level by level
+        std::vector<int64_t> level_scratch(maxh0 + 1, 0);
+        if (!t->with_trace) {
+            for (auto &nd : t->nodes)
+                if (nd.upper >= 0 && nd.kind == 2) {
+                    level_scratch[nd.height] = (level_scratch[nd.height] + 31) / 32 * 32;
+                    nd.trace_off = level_scratch[nd.height];  // relative to the scratch base
+                    level_scratch[nd.height] += n1 * nd.w1;
+                }
+            for (int64_t v : level_scratch) scratch_elems = std::max(scratch_elems, v);
+        }
+        lc.valid = true;
+        lc.top_row = top_row;
+        lc.bottom_row = bottom_row;
+        lc.n = n;
+        lc.with_trace = t->with_trace;
+        lc.skel_stride = skel_stride;
+        lc.thread_max_w1 = thread_max_w1;
+        lc.nodes.assign(t->nodes.begin(), t->nodes.end());
+        lc.root = t->root;
+        lc.nleaves = t->nleaves;
+        lc.ncomb = ncomb;
+        lc.maxh0 = maxh0;
+        lc.tab_elems = tab_elems;
+        lc.scratch_elems = scratch_elems;
     }
     tab_elems = (tab_elems + 31) / 32 * 32;
     const int64_t scratch_base = tab_elems;

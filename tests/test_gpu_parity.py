@@ -112,6 +112,32 @@ def test_random_against_oracle_trees():
             np.testing.assert_array_equal(L.recover_cross_vertices(g, tab, j), t.recover(j))
 
 
+def test_layout_reuse_across_solves(monkeypatch):
+    """The host reuses the tree + table layout of the previous solve when the
+    shape and the layout knobs repeat: interleave repeated shapes with new
+    data, the other trace mode, other slabs and another skeleton stride."""
+    rng = np.random.default_rng(13)
+    pairs = [workloads.random_pair(rng, 150, 190, s) for s in (4, 26, 4)]
+    t_full = [O.OracleTree(a, b) for a, b in pairs]
+    for stride in (None, "1", None):
+        if stride is None:
+            monkeypatch.delenv("LCSG_SKELETON_STRIDE", raising=False)
+        else:
+            monkeypatch.setenv("LCSG_SKELETON_STRIDE", stride)
+        for (a, b), t in zip(pairs, t_full):
+            g = L.GridModel(a, b)
+            for with_trace in (True, True, False):
+                tab = L.build_cost_table(g, 1, 151, with_trace=with_trace)
+                np.testing.assert_array_equal(tab.reach, t.node(t.root).reach)
+                length = L.lcs_length(tab)
+                np.testing.assert_array_equal(L.recover_cross_vertices(g, tab, length),
+                                              t.recover(length))
+            sub = L.build_cost_table(g, 40, 101)  # another slab, then the full grid again
+            ref = O.OracleTree(a, b, 40, 101)
+            np.testing.assert_array_equal(sub.reach, ref.node(ref.root).reach)
+            np.testing.assert_array_equal(sub.trace, ref.node(ref.root).trace)
+
+
 def test_low_memory_tables_and_retrace():
     rng = np.random.default_rng(12)
     for _ in range(20):
