@@ -75,6 +75,84 @@ def load_counters(cfg, seed):
     return d.get(f"cfg{cfg}/seed{seed}", {}).get("counters")
 
 
+def load_digest(cfg, seed):
+    with open(os.path.join(ROOT, "tests", "golden", "config_digests.json")) as f:
+        return json.load(f).get(f"cfg{cfg}/seed{seed}")
+
+
+def verify_timed_path(lib, _lib, build, m, n, swapped, digest):
+    """One more solve of the exact timed path (traced build + device
+    extraction), checked against the REFERENCE's digests of this config
+    (tests/golden/config_digests.json, make_golden.py / make_deep_digests.py):
+    LCS length, sha256 of subsequence and positions, of the final D_G and of
+    the final trace table.  Outside the timed region."""
+    import hashlib
+
+    if digest is None:
+        return "no reference digest for this config/seed"
+    h = build()
+    k = min(m, n)
+    sub, rp, cp = np.empty(k, np.uint8), np.empty(k, np.int32), np.empty(k, np.int32)
+    try:
+        length = ctypes.c_int32()
+        _lib.check(lib.lcsg_extract(h, -1, ctypes.byref(length), sub.ctypes.data, rp.ctypes.data,
+                                    cp.ctypes.data), "extract")
+        L = int(length.value)
+        pa, pb = (cp[:L], rp[:L]) if swapped else (rp[:L], cp[:L])
+        bad = []
+        if L != digest["length"]:
+            bad.append("length")
+        if hashlib.sha256(sub[:L].tobytes()).hexdigest() != digest["subsequence_sha256"]:
+            bad.append("subsequence")
+        pos = np.concatenate([pa, pb]).astype(np.int64).tobytes()
+        if hashlib.sha256(pos).hexdigest() != digest["positions_sha256"]:
+            bad.append("positions")
+        root = lib.lcsg_root(h)
+        tab = np.empty((n + 1) * (min(m, n) + 1), np.int32)
+        _lib.check(lib.lcsg_node_reach(h, root, tab.ctypes.data), "reach")
+        if hashlib.sha256(tab.tobytes()).hexdigest() != digest["dg_sha256"]:
+            bad.append("D_G")
+        checked = "length, subsequence, positions, D_G"
+        if "trace_sha256" in digest:
+            _lib.check(lib.lcsg_node_trace(h, root, tab.ctypes.data), "trace")
+            if hashlib.sha256(tab.tobytes()).hexdigest() != digest["trace_sha256"]:
+                bad.append("trace")
+            checked += ", trace"
+    finally:
+        lib.lcsg_free(h)
+    return "ok" if not bad else "MISMATCH: " + ", ".join(bad) + f" (checked {checked})"
+
+
+def load_cpu_full(cfg, seed):
+    """The reference timed once on the WHOLE config (traced / low_memory, T=1 /
+    all threads) on a GPU box's host by tools/cpu_full_baseline.py
+    (profiles/cpu_full_cfgN.json); None if it was not run for this config."""
+    path = os.path.join(ROOT, "profiles", f"cpu_full_cfg{cfg}.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        doc = json.load(f)
+    if doc.get("seed") != seed or not doc.get("best"):
+        return None
+    best = doc["best"]
+    return {"value": best["cells_per_s"], "unit": UNIT, "cores": best["threads"],
+            "kind": "reference", "seconds": best["seconds"], "mode": best["mode"],
+            "cpu_model": doc["cpu_model"], "host_threads": doc["host_threads"],
+            "runs": [{k: r.get(k) for k in ("mode", "threads", "seconds", "peak_rss_gb")}
+                     for r in doc["runs"]],
+            "source": f"profiles/cpu_full_cfg{cfg}.json (measured once, not in this run)"}
+
+
+def load_issue(cfg):
+    """Issue-slot utilisation of the dominant combine kernels from the
+    committed ncu captures (profiles/issue_cfgN.json, tools/ncu_summary.py)."""
+    path = os.path.join(ROOT, "profiles", f"issue_cfg{cfg}.json")
+    if not os.path.exists(path):
+        return None
+    with open(path) as f:
+        return json.load(f)
+
+
 def load_traffic(cfg):
     """DRAM bytes of one solve's combine launches from the committed ncu
     launch list (profiles/traffic_cfgN.json, tools/traffic.py); None if absent."""
@@ -245,10 +323,14 @@ def run_ours(args, rank, world, dist):
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=dev)  # 256 MiB > L2
     flags = _lib.LCSG_WITH_TRACE | _lib.LCSG_TIMING
 
-    def solve():
+    def build():
         h = ctypes.c_void_p()
         _lib.check(lib.lcsg_build_device(d_rows.data_ptr(), m, d_cols.data_ptr(), n, 1, m + 1,
                                          flags, local, sp, ctypes.byref(h)), "build")
+        return h
+
+    def solve():
+        h = build()
         length = ctypes.c_int32()
         _lib.check(lib.lcsg_extract(h, -1, ctypes.byref(length), sub.ctypes.data,
                                     rp.ctypes.data, cp.ctypes.data), "extract")
@@ -300,6 +382,8 @@ def run_ours(args, rank, world, dist):
         if it > 0:  # first call is a warm-up of the host-input path
             e2e_ms.append(e0.elapsed_time(e1))
     assert r.length == length
+    parity = verify_timed_path(lib, _lib, build, m, n, len(a) > len(b),
+                               load_digest(args.config, seed))
     e2e_t = statistics.mean(e2e_ms)
     if dist is not None:
         tt = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
@@ -322,6 +406,22 @@ def run_ours(args, rank, world, dist):
                 "kernel": "combine levels (all heights)", "combine_ms": comb,
                 "algorithmic_bytes": alg, "peak_source": peak_kind,
                 "compulsory_frac": (8 * counters["OUT"] + 4 * counters["IN"]) / (comb / 1e3) / 1e9 / peak}
+        # INT32 term: C reference cell evaluations, one
+        # 32-bit min each, at the IMNMX rate measured live on this GPU
+        rate, sms, pms = ctypes.c_double(), ctypes.c_int32(), ctypes.c_double()
+        if lib.lcsg_probe_int32_rate(local, ctypes.byref(rate), ctypes.byref(sms),
+                                     ctypes.byref(pms)) == 0 and rate.value > 0:
+            t_int = counters["C"] / rate.value * 1e3
+            t_hbm = alg / (peak * 1e9) * 1e3
+            roof["int32"] = {"rate_mins_per_s": rate.value, "sms": sms.value,
+                             "ops": counters["C"], "t_roof_ms": t_int,
+                             "frac": t_int / comb,
+                             "source": "lcsg_probe_int32_rate: IMNMX.U32 chains, best of 5"}
+            roof["t_roof_ms"] = max(t_hbm, t_int)
+            roof["bound"] = "hbm" if t_hbm >= t_int else "int32"
+        issue = load_issue(args.config)
+        if issue:
+            roof["issue_active"] = issue
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t_ms, "higher_is_better": True,
@@ -330,6 +430,7 @@ def run_ours(args, rank, world, dist):
                    "seed": args.seed, "lcs_length": length, "l2": "flushed (256 MiB) between steps",
                    "parallelism": f"replicas x{world}"},
         "roofline": roof,
+        "parity": parity,
         "e2e": {"value": world * m * n / (e2e_t / 1e3), "unit": UNIT,
                 "h2d_bytes_per_step": int(h2d + m + n), "d2h_bytes_per_step": int(d2h)},
         "gpu_launches": launches,
@@ -337,6 +438,9 @@ def run_ours(args, rank, world, dist):
     }
     if not args.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline(args.config, args.seed, 1, args.cpu_budget)
+        full = load_cpu_full(args.config, args.seed)
+        if full is not None:
+            line["cpu_baseline"]["full"] = full
     print(json.dumps(line), flush=True)
 
 

@@ -60,8 +60,13 @@ int lcsg_build_device(const uint8_t *rows_dev, int64_t m, const uint8_t *cols_de
                       int32_t top_row, int32_t bottom_row, uint32_t flags, int device,
                       void *stream, lcsg_handle *out);
 
-/* Release every device buffer of the tree. */
+/* Release every device buffer of the tree (back to the library's private
+ * stream-ordered pool, which keeps them for the next solve). */
 int lcsg_free(lcsg_handle h);
+/* Return the unused blocks of the library's memory pool on `device` to the
+ * driver (after lcsg_free of the trees; no reference counterpart -- the
+ * reference frees numpy arrays with the CostTable, solver.py:52-53). */
+int lcsg_trim(int device);
 /* Wait for all work enqueued on the handle's stream. */
 int lcsg_sync(lcsg_handle h);
 
@@ -148,6 +153,11 @@ int lcsg_recover_from(lcsg_handle h, int32_t i_start, int32_t j, int32_t *cols_o
 #define LCSG_TIMING 2u
 int lcsg_stats(lcsg_handle h, int64_t *launches, double *combine_ms, double *leaf_ms,
                double *total_ms, int64_t *h2d_bytes, int64_t *d2h_bytes);
+
+/* Measured INT32 min issue rate of `device` (R_INT32 of the combine
+ * roofline): independent IMNMX.U32 chains on every SM, best
+ * of 5 timed launches.  *mins_per_s = 32-bit min operations per second. */
+int lcsg_probe_int32_rate(int device, double *mins_per_s, int32_t *sm_count, double *ms);
 
 #ifdef __cplusplus
 }

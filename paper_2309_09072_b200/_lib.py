@@ -18,7 +18,8 @@ _ROOT = os.path.dirname(_PKG)
 LIB_DIR = os.path.join(_PKG, "lib")
 LIB_PATH = os.environ.get("LCSG_LIB_PATH") or os.path.join(LIB_DIR, "liblcsgrid_b200.so")
 CSRC = os.path.join(_PKG, "csrc")
-SOURCES = ["lcsg_api.cu", "lcsg_kernels.cu", "lcsg_refine.cu", "lcsg_tile.cu", "lcsg_narrow.cu"]
+SOURCES = ["lcsg_api.cu", "lcsg_kernels.cu", "lcsg_refine.cu", "lcsg_tile.cu", "lcsg_narrow.cu",
+           "lcsg_probe.cu"]
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
     "-Xcompiler", "-fPIC", "-shared",
@@ -52,6 +53,7 @@ SIGNATURES = {
     "lcsg_build_device": (ctypes.c_int, [_vp, _i64, _vp, _i64, _i32, _i32, ctypes.c_uint32,
                                          ctypes.c_int, _vp, ctypes.POINTER(_vp)]),
     "lcsg_free": (ctypes.c_int, [_vp]),
+    "lcsg_trim": (ctypes.c_int, [ctypes.c_int]),
     "lcsg_sync": (ctypes.c_int, [_vp]),
     "lcsg_num_nodes": (_i32, [_vp]),
     "lcsg_root": (_i32, [_vp]),
@@ -76,6 +78,8 @@ SIGNATURES = {
     "lcsg_combine_rows": (ctypes.c_int, [_vp, _i32, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp,
                                          _vp, _i32, _i32, _i64, _i64, _i64, _vp]),
     "lcsg_recover_from": (ctypes.c_int, [_vp, _i32, _i32, _vp]),
+    "lcsg_probe_int32_rate": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                             _i32p, ctypes.POINTER(ctypes.c_double)]),
     "lcsg_stats": (ctypes.c_int, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_double),
                                   ctypes.POINTER(ctypes.c_double),
                                   ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64),
@@ -84,15 +88,34 @@ SIGNATURES = {
 
 
 def build_library(verbose: bool = False) -> str:
-    """Compile the CUDA sources for sm_100a into the in-tree shared object."""
+    """Compile the CUDA sources for sm_100a into the in-tree shared object
+    (one nvcc per translation unit in parallel, then one link)."""
+    from concurrent.futures import ThreadPoolExecutor
+
     os.makedirs(LIB_DIR, exist_ok=True)
+    obj_dir = os.path.join(LIB_DIR, "obj")
+    os.makedirs(obj_dir, exist_ok=True)
     srcs = [os.path.join(CSRC, s) for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
-    cmd = ["nvcc", *NVCC_FLAGS, "-o", LIB_PATH, *srcs]
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+
+    def compile_one(src):
+        obj = os.path.join(obj_dir, os.path.basename(src)[:-3] + ".o")
+        cmd = ["nvcc", *compile_flags, "-c", "-o", obj, src]
+        return obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    with ThreadPoolExecutor(max_workers=len(srcs)) as ex:
+        results = list(ex.map(compile_one, srcs))
+    log = ""
+    for obj, res in results:
+        log += res.stdout + res.stderr
+        if res.returncode != 0:
+            raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
+    cmd = ["nvcc", *NVCC_FLAGS, "-o", LIB_PATH, *[o for o, _ in results]]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
+        raise RuntimeError("nvcc link failed:\n" + res.stdout + res.stderr)
     if verbose:
-        print(res.stdout + res.stderr)
+        print(log + res.stdout + res.stderr)
     return LIB_PATH
 
 

@@ -57,25 +57,68 @@ int bits_for(int64_t x) {
 }
 
 std::mutex g_pool_mu;
-bool g_pool_ready[64] = {};
+cudaMemPool_t g_pool[64] = {};
 
+// Saves the caller's current device and restores it on scope exit: no entry
+// point leaves the calling thread on another device (torch allocations and
+// kernels of the caller keep going to the device it had selected).
+struct SaveDevice {
+    int prev = -1;
+    SaveDevice() {
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            cudaGetLastError();
+            prev = -1;
+        }
+    }
+    ~SaveDevice() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+// Selects `device` (callers hold a SaveDevice) and makes sure the library's
+// own memory pool exists there.  The pool is private to the library (not the
+// device's default pool, which PyTorch's cudaMallocAsync backend and other
+// libraries share): it keeps freed blocks so repeated solves reuse the same
+// HBM without cudaMalloc/cudaFree round trips, and lcsg_trim() returns them.
 int prepare_device(int device) {
     int count = 0;
-    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0)
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
         return fail(LCSG_ENODEV, "no CUDA device visible");
-    if (device < 0 || device >= count) return fail(LCSG_EINVAL, "device index out of range");
+    }
+    if (device < 0 || device >= count || device >= 64)
+        return fail(LCSG_EINVAL, "device index out of range");
     CK(cudaSetDevice(device));
     std::lock_guard<std::mutex> lk(g_pool_mu);
-    if (device < 64 && !g_pool_ready[device]) {
-        // stream-ordered allocator that keeps freed blocks: repeated solves
-        // reuse the same HBM without cudaMalloc/cudaFree round trips.
+    if (!g_pool[device]) {
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = device;
         cudaMemPool_t pool;
-        CK(cudaDeviceGetDefaultMemPool(&pool, device));
+        CK(cudaMemPoolCreate(&pool, &props));
         uint64_t thr = UINT64_MAX;
         CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-        g_pool_ready[device] = true;
+        g_pool[device] = pool;
     }
     return LCSG_OK;
+}
+
+// stream-ordered allocation from the library pool of `device`
+cudaError_t pool_alloc(void **p, size_t bytes, int device, cudaStream_t s) {
+    cudaMemPool_t pool;
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        pool = (device >= 0 && device < 64) ? g_pool[device] : nullptr;
+    }
+    if (!pool) return cudaMallocAsync(p, bytes, s);
+    return cudaMallocFromPoolAsync(p, bytes, pool, s);
+}
+
+int current_device_prepared(int *dev) {
+    CK(cudaGetDevice(dev));
+    return prepare_device(*dev);
 }
 
 // Kernel choice per combine:
@@ -89,6 +132,13 @@ int prepare_device(int device) {
 int env_int(const char *name, int def) {
     const char *v = getenv(name);
     return v && *v ? atoi(v) : def;
+}
+
+// 64-bit packed (value, k) keys when the value and split bits do not fit in
+// 32; LCSG_FORCE_KEY64=1 selects them everywhere, so the 64-bit
+// instantiation of every kernel is parity-tested at small sizes too.
+bool need_key64(int value_bits, int shift) {
+    return value_bits + shift > 32 || env_int("LCSG_FORCE_KEY64", 0) != 0;
 }
 
 int default_skeleton_stride(int64_t n1) { return n1 <= 8193 ? 32 : 64; }
@@ -227,11 +277,13 @@ void destroy(lcsg_tree_s *t) {
     delete t;
 }
 
-// Host staging of the plan metadata, one pinned buffer per host thread and
-// device, reused across solves: no page faults on a fresh multi-MB vector
-// (they cost 1-3 ms per cfg5 solve) and a truly asynchronous upload.  `done`
-// is recorded after the upload; the next solve on this thread waits on it
-// before rewriting the buffer (it has normally long completed).
+// Host staging of the plan metadata: pinned buffers reused across solves (no
+// page faults on a fresh multi-MB vector -- they cost 1-3 ms per cfg5 solve --
+// and a truly asynchronous upload).  Stages live in a small per-device free
+// list shared by all host threads (bounded by the number of concurrent
+// solves, so short-lived worker threads do not leak pinned memory); `done`
+// is recorded after a solve's uploads and waited on before the buffer is
+// rewritten by the next solve that takes it (normally long completed).
 struct MetaStage {
     char *buf = nullptr;
     size_t cap = 0;
@@ -239,29 +291,66 @@ struct MetaStage {
     int device = -1;
 };
 
-char *meta_stage_acquire(MetaStage &ms, int device, size_t bytes) {
-    if (ms.device != device && ms.buf) {  // another device: start over
-        cudaFreeHost(ms.buf);
-        if (ms.done) cudaEventDestroy(ms.done);
-        ms = MetaStage();
-    }
-    ms.device = device;
-    if (ms.done) cudaEventSynchronize(ms.done);  // previous upload finished
-    if (ms.cap < bytes) {
-        if (ms.buf) cudaFreeHost(ms.buf);
-        ms.cap = std::max(bytes, ms.cap * 2);
-        if (cudaMallocHost((void **)&ms.buf, ms.cap) != cudaSuccess) {
-            ms.buf = nullptr;
-            ms.cap = 0;
-            return nullptr;
-        }
-    }
-    if (!ms.done && cudaEventCreateWithFlags(&ms.done, cudaEventDisableTiming) != cudaSuccess)
-        ms.done = nullptr;
-    return ms.buf;
-}
+std::mutex g_meta_mu;
+std::vector<MetaStage *> g_meta_free[64];
 
-thread_local MetaStage t_meta_stage;
+// RAII lease of one stage: returned to the device's free list on scope exit
+// (after recording `done` on the solve stream, so a later user waits for
+// this solve's uploads even on an error path).
+struct MetaLease {
+    MetaStage *ms = nullptr;
+    cudaStream_t stream = nullptr;
+    MetaLease() = default;
+    MetaLease(const MetaLease &) = delete;
+    MetaLease &operator=(const MetaLease &) = delete;
+    ~MetaLease() { finish(); }
+    // record `done` after everything enqueued so far and hand the stage back
+    // (call while the stream is still alive)
+    void finish() {
+        if (!ms) return;
+        if (ms->done && stream && cudaEventRecord(ms->done, stream) != cudaSuccess) {
+            cudaGetLastError();
+            cudaStreamSynchronize(stream);
+            cudaGetLastError();
+        }
+        std::lock_guard<std::mutex> lk(g_meta_mu);
+        g_meta_free[ms->device].push_back(ms);
+        ms = nullptr;
+    }
+    // buffer of >= bytes on `device` (current device), or nullptr
+    char *acquire(int device, size_t bytes, cudaStream_t s) {
+        stream = s;
+        {
+            std::lock_guard<std::mutex> lk(g_meta_mu);
+            auto &fl = g_meta_free[device];
+            if (!fl.empty()) {
+                ms = fl.back();
+                fl.pop_back();
+            }
+        }
+        if (!ms) {
+            ms = new MetaStage();
+            ms->device = device;
+        }
+        if (ms->done) cudaEventSynchronize(ms->done);  // previous upload finished
+        if (ms->cap < bytes) {
+            if (ms->buf) cudaFreeHost(ms->buf);
+            ms->cap = std::max(bytes, ms->cap * 2);
+            if (cudaMallocHost((void **)&ms->buf, ms->cap) != cudaSuccess) {
+                cudaGetLastError();
+                ms->buf = nullptr;
+                ms->cap = 0;
+                return nullptr;
+            }
+        }
+        if (!ms->done && cudaEventCreateWithFlags(&ms->done, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            ms->done = nullptr;
+        }
+        return ms->buf;
+    }
+};
+
 int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *cols, bool cols_dev,
                int64_t n, int32_t top_row, int32_t bottom_row, uint32_t flags, int device,
                void *stream, lcsg_handle *out) {
@@ -271,6 +360,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     if (!(1 <= top_row && top_row < bottom_row && (int64_t)bottom_row <= m + 1))
         return fail(LCSG_EINVAL, "1 <= top_row < bottom_row <= m + 1");
     if (n > (int64_t)INT32_MAX - 4) return fail(LCSG_EINVAL, "column string too long for int32 tables");
+    SaveDevice keep_caller_device;
     int rc = prepare_device(device);
     if (rc) return rc;
 
@@ -439,7 +529,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     t->arena_bytes = off;
 
     const auto h1 = hclock();
-    cudaError_t ae = cudaMallocAsync((void **)&t->arena, t->arena_bytes, t->stream);
+    cudaError_t ae = pool_alloc((void **)&t->arena, t->arena_bytes, device, t->stream);
     const auto h2 = hclock();
     if (ae != cudaSuccess) {
         t->arena = nullptr;
@@ -468,7 +558,8 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     // ---- host-side metadata: level plan, descriptors, walk nodes ----
     const size_t meta_bytes = meta_end - o_meta;
     std::vector<char> meta_fallback;
-    char *meta = meta_stage_acquire(t_meta_stage, device, meta_bytes);
+    MetaLease lease;
+    char *meta = lease.acquire(device, meta_bytes, t->stream);
     const bool meta_pinned = meta != nullptr;
     if (!meta_pinned) {
         meta_fallback.assign(meta_bytes, 0);
@@ -488,7 +579,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
         cudaError_t e__ = (call);            \
         if (e__ != cudaSuccess) {            \
             r__ = fail(LCSG_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e__)); \
-            destroy(t);                      \
+            lease.finish(); destroy(t);                      \
             return r__;                      \
         }                                    \
     } while (0)
@@ -498,7 +589,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
         if (e__ != 0) {                      \
             int r__ = fail(LCSG_ECUDA, std::string("launch ") + #call + ": " +      \
                                            cudaGetErrorString((cudaError_t)e__));   \
-            destroy(t);                      \
+            lease.finish(); destroy(t);                      \
             return r__;                      \
         }                                    \
         ++t->launches;                       \
@@ -599,7 +690,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             L.desc_off = start;
             L.count = di - start;
             L.shift = bits_for(maxk);
-            L.key64 = vbits + L.shift > 32;
+            L.key64 = need_key64(vbits, L.shift);
             if (kind < 2) {
                 // narrow thread-per-row tables: shared-memory staged row writes
                 L.kind = (kind == 0 && maxw1 <= 33 && env_int("LCSG_STAGED_ROWS", 0)) ? 9 : kind;
@@ -682,7 +773,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             if (e > 0) {
                 const int r = fail(LCSG_ECUDA, std::string("launch: ") +
                                                    cudaGetErrorString((cudaError_t)e));
-                destroy(t);
+                lease.finish(); destroy(t);
                 return r;
             }
             if (e == 0) ++t->launches;
@@ -716,7 +807,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
         maxd = std::max(maxd, nd.depth);
     }
     t->walk_shift = bits_for(maxku);
-    t->walk_key64 = vbits + t->walk_shift > 32;
+    t->walk_key64 = need_key64(vbits, t->walk_shift);
     int32_t wpos = 0;
     std::vector<std::vector<int32_t>> by_depth(maxd + 1);
     for (int32_t id = 0; id < nn; ++id)
@@ -728,7 +819,6 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     }
     BCK(cudaMemcpyAsync(A + o_walk, meta + (o_walk - o_meta), o_lnodes - o_walk,
                         cudaMemcpyHostToDevice, s));
-    if (meta_pinned && t_meta_stage.done) BCK(cudaEventRecord(t_meta_stage.done, s));
     if (hprof) {
         const auto h4 = hclock();
         fprintf(stderr, "lcsg_build host ms: tree+layout %.3f  arena %.3f  metadata %.3f  enqueue %.3f\n",
@@ -736,6 +826,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     }
 #undef BCK
 #undef BCKL
+    lease.finish();
     *out = t;
     return LCSG_OK;
 }
@@ -850,6 +941,18 @@ int lcsg_free(lcsg_handle h) {
     return LCSG_OK;
 }
 
+int lcsg_trim(int device) {
+    cudaMemPool_t pool;
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        if (device < 0 || device >= 64) return fail(LCSG_EINVAL, "device index out of range");
+        pool = g_pool[device];
+    }
+    if (!pool) return LCSG_OK;  // nothing allocated on that device yet
+    CK(cudaMemPoolTrimTo(pool, 0));
+    return LCSG_OK;
+}
+
 int lcsg_sync(lcsg_handle h) {
     if (!h) return fail(LCSG_EINVAL, "null handle");
     DeviceGuard g(h->device);
@@ -891,7 +994,7 @@ static int leaf_device(lcsg_handle h, int32_t node, int32_t **reach) {
     const NodeH &nd = h->nodes[node];
     const int64_t n1 = h->n + 1;
     int32_t *buf = nullptr;
-    CK(cudaMallocAsync((void **)&buf, (size_t)(n1 * nd.w1 + n1) * 4, h->stream));
+    CK(pool_alloc((void **)&buf, (size_t)(n1 * nd.w1 + n1) * 4, h->device, h->stream));
     h->leaf_cache[node] = buf;
     CKL(launch_leaf_table(h->ctx(), nd.leaf_row, nd.w1, buf, buf + n1 * nd.w1, h->stream));
     ++h->launches;
@@ -1021,15 +1124,15 @@ int lcsg_assemble(const uint8_t *rows, int64_t m, const uint8_t *cols, int64_t n
     if (!length) return fail(LCSG_EINVAL, "null length pointer");
     *length = 0;
     if (m == 0 || n == 0) return LCSG_OK;  // solver.py:219-220
+    SaveDevice keep_caller_device;
     int rc = prepare_device(device);
     if (rc) return rc;
-    DeviceGuard g(device);
     const int64_t k = std::min(m, n);
     size_t bytes = align_up(m) + align_up(n) + align_up((m + 1) * 4) + align_up((1 + 2 * k) * 4) + align_up(k);
     char *buf = nullptr;
     cudaStream_t s = nullptr;
     CK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
-    cudaError_t e = cudaMallocAsync((void **)&buf, bytes, s);
+    cudaError_t e = pool_alloc((void **)&buf, bytes, device, s);
     if (e != cudaSuccess) {
         cudaStreamDestroy(s);
         return fail(LCSG_ENOMEM, cudaGetErrorString(e));
@@ -1082,8 +1185,7 @@ int lcsg_combine_level(const int32_t *upper_reach, int32_t wu1, const int32_t *u
     if (i_lo < 0 || i_hi > n1 || i_lo > i_hi) return fail(LCSG_EINVAL, "bad row range");
     if (i_hi == i_lo) return LCSG_OK;
     int dev = 0;
-    CK(cudaGetDevice(&dev));
-    int rc = prepare_device(dev);
+    int rc = current_device_prepared(&dev);
     if (rc) return rc;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t rows = i_hi - i_lo;
@@ -1092,7 +1194,7 @@ int lcsg_combine_level(const int32_t *upper_reach, int32_t wu1, const int32_t *u
         int32_t wstar_l, wstar_out;
     };
     char *buf = nullptr;
-    CK(cudaMallocAsync((void **)&buf, sizeof(Scratch) + 256 + (size_t)rows * 4, s));
+    CK(pool_alloc((void **)&buf, sizeof(Scratch) + 256 + (size_t)rows * 4, dev, s));
     Scratch *sc = (Scratch *)buf;
     int32_t *kmax_scratch = (int32_t *)(buf + align_up(sizeof(Scratch)));
     Scratch hs;
@@ -1112,7 +1214,7 @@ int lcsg_combine_level(const int32_t *upper_reach, int32_t wu1, const int32_t *u
     c.n = (int32_t)(rows - 1);
     c.inf = inf;
     const int shift = bits_for(wu1 - 1);
-    const bool key64 = bits_for(inf) + shift > 32;
+    const bool key64 = need_key64(bits_for(inf), shift);
     CKL(launch_combine(w1 <= 65 ? 0 : 1, &sc->d, 1, c, shift, key64, s));
     CK(cudaFreeAsync(buf, s));
     CK(cudaStreamSynchronize(s));
@@ -1187,8 +1289,7 @@ int lcsg_combine_rows(const int32_t *upper_reach, int32_t wu1, const int32_t *up
     const int64_t rows = i_hi - i_lo;
     if (rows == 0) return LCSG_OK;
     int dev = 0;
-    CK(cudaGetDevice(&dev));
-    int rc = prepare_device(dev);
+    int rc = current_device_prepared(&dev);
     if (rc) return rc;
     cudaStream_t s = (cudaStream_t)stream;
     struct Scratch {
@@ -1196,7 +1297,7 @@ int lcsg_combine_rows(const int32_t *upper_reach, int32_t wu1, const int32_t *up
         int32_t wstar_l;
     };
     Scratch *sc = nullptr;
-    CK(cudaMallocAsync((void **)&sc, sizeof(Scratch), s));
+    CK(pool_alloc((void **)&sc, sizeof(Scratch), dev, s));
     Scratch hs;
     std::memset(&hs, 0, sizeof(hs));
     // the row window [i_lo, i_hi) is addressed as a table of `rows` rows; L
@@ -1216,7 +1317,7 @@ int lcsg_combine_rows(const int32_t *upper_reach, int32_t wu1, const int32_t *up
     c.n = (int32_t)(rows - 1);
     c.inf = inf;
     const int shift = bits_for(wu1 - 1);
-    const bool key64 = bits_for(inf) + shift > 32;
+    const bool key64 = need_key64(bits_for(inf), shift);
     const int thread_max_w1 = env_int("LCSG_THREAD_MAX_W1", 65);
     int S = 1;
     while (S * 2 <= std::max(1, env_int("LCSG_SKELETON_STRIDE", default_skeleton_stride(n1)))) S *= 2;

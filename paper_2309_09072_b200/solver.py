@@ -251,9 +251,9 @@ def lcs(
     ``stream`` (a cudaStream_t handle as int, e.g. torch's current stream)."""
     aa = as_bytes(a)
     bb = as_bytes(b)
-    _backend.resolve(backend)
-    if len(aa) == 0 or len(bb) == 0:
+    if len(aa) == 0 or len(bb) == 0:  # before any backend resolution (solver.py:255-256)
         return LcsResult(0, b"", (), ())
+    _backend.resolve(backend)
     k = min(len(aa), len(bb))
     x = np.frombuffer(aa, dtype=np.uint8)
     y = np.frombuffer(bb, dtype=np.uint8)

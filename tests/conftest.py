@@ -15,7 +15,7 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 GOLDEN = os.path.join(ROOT, "tests", "golden")
-for p in (ROOT, os.path.join(ROOT, "oracle")):
+for p in (ROOT, os.path.join(ROOT, "oracle"), GOLDEN):
     if p not in sys.path:
         sys.path.insert(0, p)
 REF_DIR = os.path.join(ROOT, "oracle", "_ref")

@@ -81,7 +81,9 @@ def test_reference_cfg1_tree_every_node(ref_trees):
     compare_nodes(gpu_tree_nodes(L.build_cost_table(g, 1, g.m + 1)), trees["cfg1"])
 
 
-def test_reference_lcs_pairs(ref_lcs_pairs):
+@pytest.mark.parametrize("key64", ["0", "1"])
+def test_reference_lcs_pairs(ref_lcs_pairs, key64, monkeypatch):
+    monkeypatch.setenv("LCSG_FORCE_KEY64", key64)
     for p in ref_lcs_pairs:
         a, b = bytes.fromhex(p["a"]), bytes.fromhex(p["b"])
         for low in (False, True):
@@ -232,27 +234,91 @@ def test_assemble_and_device_view():
         np.testing.assert_array_equal(tab.reach_device.cpu().numpy(), tab.reach)
 
 
-def _check_digest(exp, a, b, low_memory=False):
+def gpu_tree_digest(table) -> str:
+    """tree_digest() of tests/golden/make_deep_digests.py over a device tree:
+    node ids are the reference's post-order creation ids, so records are
+    hashed in id order; buffers are reused (one node on the host at a time)."""
+    from make_deep_digests import node_record
+
+    lib = _lib.load()
+    h = table._tree.handle
+    acc = hashlib.sha256()
+    info = (ctypes.c_int32 * 8)()
+    buf = np.empty(0, np.int32)
+    for node in range(lib.lcsg_num_nodes(h)):
+        _lib.check(lib.lcsg_node_info(h, node, info))
+        w1, upper, n = info[2], info[3], info[6]
+        cells = (n + 1) * w1
+        if buf.size < 2 * cells + n + 1:
+            buf = np.empty(2 * cells + n + 1, np.int32)
+        reach = buf[:cells]
+        kmax = buf[2 * cells:2 * cells + n + 1]
+        _lib.check(lib.lcsg_node_reach(h, node, reach.ctypes.data))
+        _lib.check(lib.lcsg_node_kmax(h, node, kmax.ctypes.data))
+        trace = None
+        if upper >= 0:
+            trace = buf[cells:2 * cells]
+            _lib.check(lib.lcsg_node_trace(h, node, trace.ctypes.data))
+        w = ctypes.c_int32()
+        _lib.check(lib.lcsg_node_wstar(h, node, ctypes.byref(w)))
+        acc.update(node_record(reach, trace, kmax, w.value))
+    return acc.hexdigest()
+
+
+def _check_lcs_digest(exp, a, b, low_memory):
     r = L.lcs(a, b, low_memory=low_memory)
-    assert r.length == exp["length"]
-    assert hashlib.sha256(r.subsequence).hexdigest() == exp["subsequence_sha256"]
+    assert r.length == exp["length"], low_memory
+    assert hashlib.sha256(r.subsequence).hexdigest() == exp["subsequence_sha256"], low_memory
     pos = np.array(r.row_positions + r.col_positions, dtype=np.int64).tobytes()
-    assert hashlib.sha256(pos).hexdigest() == exp["positions_sha256"]
+    assert hashlib.sha256(pos).hexdigest() == exp["positions_sha256"], low_memory
+
+
+def _check_digest(exp, a, b, low_memory_too=False, deep=True):
+    """lcs() in TRACED mode (the path bench.py times) and, optionally,
+    low-memory mode; the final D_G built with and without traces; the final
+    trace table and every node of the traced tree when the reference digests
+    hold them (tests/golden/make_deep_digests.py)."""
+    _check_lcs_digest(exp, a, b, low_memory=False)
+    if low_memory_too:
+        _check_lcs_digest(exp, a, b, low_memory=True)
     rows, cols = (b, a) if len(a) > len(b) else (a, b)
     g = L.GridModel(rows, cols)
     tab = L.build_cost_table(g, 1, g.m + 1, with_trace=False)
     assert hashlib.sha256(tab.reach.tobytes()).hexdigest() == exp["dg_sha256"]
+    del tab
+    tab = L.build_cost_table(g, 1, g.m + 1, with_trace=True)
+    assert hashlib.sha256(tab.reach.tobytes()).hexdigest() == exp["dg_sha256"]
+    if "trace_sha256" in exp:
+        assert hashlib.sha256(tab.trace.tobytes()).hexdigest() == exp["trace_sha256"]
+    if deep and "tree_sha256" in exp:
+        assert gpu_tree_digest(tab) == exp["tree_sha256"]
 
 
-@pytest.mark.parametrize("key", ["cfg1/seed0", "cfg1/seed1", "cfg1/seed2", "cfg2/seed0",
-                                 "cfg2/seed1", "cfg2/seed2", "cfg3/seed0", "cfg3/seed1",
-                                 "cfg3/seed2", "cfg4/seed0", "cfg5/seed0"])
+DIGEST_KEYS = [f"cfg{c}/seed{s}" for c in (1, 2, 3, 4, 5) for s in (0, 1, 2)]
+
+
+@pytest.mark.parametrize("key", DIGEST_KEYS)
 def test_config_digests(config_digests, key):
+    """Every config, seeds 0-2, against the reference's own digests: traced
+    lcs() (what bench.py times), low-memory lcs() on cfg4/cfg5, D_G in both
+    trace modes, the final trace table and a digest of every node of the
+    traced tree (reach, trace, kmax, wstar)."""
     if key not in config_digests:
         pytest.skip(f"{key} digest not generated")
     cfg, seed = int(key[3]), int(key.split("seed")[1])
     a, b = workloads.generate(cfg, seed)
-    _check_digest(config_digests[key], a, b, low_memory=(cfg == 5))
+    _check_digest(config_digests[key], a, b, low_memory_too=(cfg >= 4))
+
+
+@pytest.mark.parametrize("key", ["cfg1/seed0", "cfg2/seed1", "cfg3/seed2", "cfg4/seed0"])
+def test_config_digests_key64(config_digests, key, monkeypatch):
+    """The 64-bit packed-key instantiation of every kernel (selected at
+    bits(n+2) + bits(max k) > 32, e.g. 100k x 100k inputs) forced on at
+    config scale: same digests, every node of the tree included."""
+    monkeypatch.setenv("LCSG_FORCE_KEY64", "1")
+    cfg, seed = int(key[3]), int(key.split("seed")[1])
+    a, b = workloads.generate(cfg, seed)
+    _check_digest(config_digests[key], a, b, low_memory_too=True)
 
 
 def _dg_row_by_definition(rows: bytes, cols: bytes, i: int, w1: int) -> np.ndarray:
@@ -315,6 +381,7 @@ def test_skeleton_refine_strides(stride, monkeypatch):
                                           t.recover(length))
 
 
+@pytest.mark.parametrize("key64", ["0", "1"])
 @pytest.mark.parametrize("env", [
     {"LCSG_SKELETON_STRIDE": "64", "LCSG_COL_BLOCK": "8"},   # two stages: step 8, step 1
     {"LCSG_SKELETON_STRIDE": "32", "LCSG_COL_BLOCK": "4"},   # stages: step 8, 2, 1 (B=4,4,2)
@@ -333,10 +400,12 @@ def test_skeleton_refine_strides(stride, monkeypatch):
     {"LCSG_SKEL_WARP_BATCHED": "0"},                        # per-node warp DFS for w1 <= 257 skeletons
     {"LCSG_NARROW_FW": "0"},                                # narrow kernels with a runtime row width
 ])
-def test_refinement_variants(env, monkeypatch):
-    """Every geometry / schedule of the wide-table combine is bit-exact."""
+def test_refinement_variants(env, key64, monkeypatch):
+    """Every geometry / schedule of the wide-table combine is bit-exact, with
+    32-bit and (forced) 64-bit packed keys."""
     for k, v in env.items():
         monkeypatch.setenv(k, v)
+    monkeypatch.setenv("LCSG_FORCE_KEY64", key64)
     import zlib
 
     rng = np.random.default_rng(zlib.crc32(repr(sorted(env.items())).encode()))

@@ -58,11 +58,25 @@ def test_empty_short_circuit_needs_no_device():
     assert L.assemble_lcs(g, np.array([1], dtype=np.int32)) == L.LcsResult(0, b"", (), ())
 
 
+def test_backend_env_aliases(monkeypatch):
+    for name in ("cython", "python", "cuda"):
+        monkeypatch.setenv("LCSGRID_BACKEND", name)
+        assert _backend.default_backend() == "cuda"
+    monkeypatch.setenv("LCSGRID_BACKEND", "numba")
+    with pytest.raises(ValueError, match="LCSGRID_BACKEND='numba' not available"):
+        _backend.resolve(None)
+
+
 def test_type_and_backend_errors():
     with pytest.raises(TypeError, match="expected str or bytes, got int"):
         L.lcs(5, "abc")
-    with pytest.raises(ValueError, match="unknown backend 'cython'"):
-        L.lcs("abc", "abc", backend="cython")
+    with pytest.raises(ValueError, match="unknown backend 'numba'"):
+        L.lcs("abc", "abc", backend="numba")
+    # the reference's own backend names are aliases of the CUDA path (drop-in)
+    assert _backend.resolve("cython") == "cuda"
+    assert _backend.resolve("python") == "cuda"
+    # an empty input returns before the backend is resolved (solver.py:255-256)
+    assert L.lcs("", "abc", backend="numba") == L.LcsResult(0, b"", (), ())
     assert _backend.resolve(None) == "cuda"
     assert _backend.resolve("auto") == "cuda"
     assert L.active_backend() == "cuda"
