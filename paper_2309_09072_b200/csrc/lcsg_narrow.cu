@@ -287,9 +287,13 @@ __global__ void __launch_bounds__(NarrowGeom<P>::NT)
 #pragma unroll
         for (int j = 0; j <= 2 * P; ++j) {
             if (j <= w) {
-                const int32_t v = (int32_t)(best[q][j] >> shift);
+                // compare in the key domain: an untouched slot (~0, no
+                // candidate) must read as INF also for 64-bit keys, whose
+                // shifted value does not fit an int32
+                const Key vk = best[q][j] >> shift;
+                const int32_t v = vk < (Key)(uint32_t)inf ? (int32_t)vk : inf;
                 if (v < inf) kfin = j;
-                rr[j] = v < inf ? v : inf;
+                rr[j] = v;
                 tr[j] = (int32_t)(best[q][j] & (((Key)1 << shift) - 1));
             }
         }
@@ -448,9 +452,10 @@ __global__ void __launch_bounds__(R32_NT)
 #pragma unroll
         for (int j = 0; j <= 2 * P; ++j) {
             if (j <= w) {
-                const int32_t v = (int32_t)(best[j] >> shift);
+                const uint32_t vk = best[j] >> shift;
+                const int32_t v = vk < (uint32_t)inf ? (int32_t)vk : inf;
                 if (v < inf) kfin = j;
-                rr[j] = v < inf ? v : inf;
+                rr[j] = v;
                 tr[j] = (int32_t)(best[j] & ((1u << shift) - 1));
             }
         }
@@ -536,9 +541,10 @@ __global__ void __launch_bounds__(LP_NT)
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
             if (j <= w) {
-                const int32_t v = (int32_t)(best[j] >> shift);
+                const Key vk = best[j] >> shift;
+                const int32_t v = vk < (Key)(uint32_t)inf ? (int32_t)vk : inf;
                 if (v < inf) kfin = j;
-                rr[j] = v < inf ? v : inf;
+                rr[j] = v;
                 tr[j] = (int32_t)(best[j] & (((Key)1 << shift) - 1));
             }
         }
