@@ -16,7 +16,8 @@ import threading
 _PKG = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_PKG)
 LIB_DIR = os.path.join(_PKG, "lib")
-LIB_PATH = os.environ.get("LCSG_LIB_PATH") or os.path.join(LIB_DIR, "liblcsgrid_b200.so")
+_DEFAULT_LIB = os.path.join(LIB_DIR, "liblcsgrid_b200.so")
+LIB_PATH = os.environ.get("LCSG_LIB_PATH") or _DEFAULT_LIB
 CSRC = os.path.join(_PKG, "csrc")
 SOURCES = ["lcsg_api.cu", "lcsg_kernels.cu", "lcsg_refine.cu", "lcsg_tile.cu", "lcsg_narrow.cu",
            "lcsg_probe.cu"]
@@ -87,16 +88,19 @@ SIGNATURES = {
 }
 
 
-def build_library(verbose: bool = False) -> str:
+def build_library(verbose: bool = False, out: str | None = None, defines=()) -> str:
     """Compile the CUDA sources for sm_100a into the in-tree shared object
-    (one nvcc per translation unit in parallel, then one link)."""
+    (one nvcc per translation unit in parallel, then one link).  ``out`` /
+    ``defines`` build an experiment variant elsewhere (tools/ab_build.py)."""
     from concurrent.futures import ThreadPoolExecutor
 
-    os.makedirs(LIB_DIR, exist_ok=True)
-    obj_dir = os.path.join(LIB_DIR, "obj")
+    out = out or LIB_PATH
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    obj_dir = os.path.join(os.path.dirname(out), "obj" if out == LIB_PATH else
+                           "obj_" + os.path.basename(out)[:-3])
     os.makedirs(obj_dir, exist_ok=True)
     srcs = [os.path.join(CSRC, s) for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
-    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"] + [f"-D{d}" for d in defines]
 
     def compile_one(src):
         obj = os.path.join(obj_dir, os.path.basename(src)[:-3] + ".o")
@@ -110,13 +114,13 @@ def build_library(verbose: bool = False) -> str:
         log += res.stdout + res.stderr
         if res.returncode != 0:
             raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
-    cmd = ["nvcc", *NVCC_FLAGS, "-o", LIB_PATH, *[o for o, _ in results]]
+    cmd = ["nvcc", *NVCC_FLAGS, "-o", out, *[o for o, _ in results]]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc link failed:\n" + res.stdout + res.stderr)
     if verbose:
         print(log + res.stdout + res.stderr)
-    return LIB_PATH
+    return out
 
 
 def load():
@@ -132,6 +136,8 @@ def load():
                     "(the CUDA path has no CPU fallback)")
             lib = ctypes.CDLL(LIB_PATH)
             for name, (res, args) in SIGNATURES.items():
+                if LIB_PATH != _DEFAULT_LIB and not hasattr(lib, name):
+                    continue  # an older A/B build (tools/ab_commit.py)
                 fn = getattr(lib, name)
                 fn.restype = res
                 fn.argtypes = args
