@@ -147,6 +147,7 @@ struct NodeH {
     int32_t top_row, bottom_row, w1, upper, lower, height, depth, leaf_row;
     int64_t reach_off = -1, trace_off = -1, kmax_off = -1;  // int32 element offsets
     int kind = 0;
+    bool virt = false;  // virtual height-1 node: no table (TabDev closed form of its leaves)
 };
 
 struct LaunchH {
@@ -188,7 +189,9 @@ struct lcsg_tree_s {
     int32_t *d_walk_ids = nullptr, *d_leaf_nodes = nullptr, *d_leaf_rows = nullptr;
     int32_t *d_wi = nullptr, *d_wj = nullptr, *d_path = nullptr, *d_out = nullptr;
     int32_t nleaves = 0;
-    std::map<int32_t, int32_t *> leaf_cache;
+    std::map<int32_t, int32_t *> leaf_cache;  // materialised leaves / virtual nodes (API only)
+    int32_t nvirt = 0;
+    int32_t *d_vnodes = nullptr;
     int64_t launches = 0, h2d_bytes = 0, d2h_bytes = 0;
     cudaEvent_t ev[5] = {};
     bool ev_ok = false;
@@ -206,10 +209,16 @@ struct lcsg_tree_s {
         TabDev t;
         t.w1 = nd.w1;
         t.wstar = d_node_wstar + id;
+        t.leaf2 = 0;
         if (nd.upper < 0) {
             t.reach = nullptr;
             t.kmax = nullptr;
             t.leaf_row = nd.leaf_row;
+        } else if (nd.virt) {
+            t.reach = nullptr;
+            t.kmax = nullptr;
+            t.leaf_row = nodes[nd.upper].leaf_row;
+            t.leaf2 = nodes[nd.lower].leaf_row + 1;
         } else {
             t.reach = d_tables + nd.reach_off;
             t.kmax = d_tables + nd.kmax_off;
@@ -254,7 +263,8 @@ struct LayoutCache {
     bool valid = false, with_trace = false;
     int32_t top_row = 0, bottom_row = 0, root = -1, nleaves = 0, ncomb = 0, maxh0 = 0;
     int64_t n = -1, tab_elems = 0, scratch_elems = 0;
-    int skel_stride = 0, thread_max_w1 = 0;
+    int skel_stride = 0, thread_max_w1 = 0, virt_on = -1;
+    int32_t nvirt = 0;
     std::vector<NodeH> nodes;
 };
 thread_local LayoutCache t_layout;
@@ -401,13 +411,16 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     // above (measured on cfg2/cfg3 vs cfg4/cfg5)
     const int skel_stride = std::max(1, env_int("LCSG_SKELETON_STRIDE", default_skeleton_stride(n + 1)));
     const int thread_max_w1 = env_int("LCSG_THREAD_MAX_W1", 65);
+    // virtual height-1 nodes (LCSG_VIRTUAL_H1=0 materialises them)
+    const int virt_on = (env_int("LCSG_VIRTUAL_H1", 1) != 0 && n >= 2) ? 1 : 0;
     // the tree and the table layout depend only on the shape and the knobs:
     // a repeated shape reuses them (saves ~0.5 ms of host work at cfg5 before
     // the first kernel can be enqueued)
     LayoutCache &lc = t_layout;
     const bool layout_hit = lc.valid && lc.top_row == top_row && lc.bottom_row == bottom_row &&
                             lc.n == n && lc.with_trace == t->with_trace &&
-                            lc.skel_stride == skel_stride && lc.thread_max_w1 == thread_max_w1;
+                            lc.skel_stride == skel_stride && lc.thread_max_w1 == thread_max_w1 &&
+                            lc.virt_on == virt_on;
     t->nodes.swap(t_spare_nodes);  // keeps the capacity of an earlier solve
     t->nodes.clear();
     if (layout_hit) {
@@ -452,6 +465,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     int32_t maxh0 = 0;
     if (layout_hit) {
         t->nleaves = lc.nleaves;
+        t->nvirt = lc.nvirt;
         ncomb = lc.ncomb;
         maxh0 = lc.maxh0;
         tab_elems = lc.tab_elems;
@@ -461,15 +475,30 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             if (nd.upper < 0) { t->nleaves++; continue; }
             ++ncomb;
             maxh0 = std::max(maxh0, nd.height);
-            const int32_t wu1 = t->nodes[nd.upper].w1;
             // the refinement kernels read both children as materialised slabs
             const bool kids_are_slabs =
                 t->nodes[nd.upper].upper >= 0 && t->nodes[nd.lower].upper >= 0;
             nd.kind = (nd.w1 <= thread_max_w1 || !kids_are_slabs) ? 0 : 2;
             // the refinement kernels use 32-bit element offsets into each table
             if (nd.kind == 2 && n1 * (int64_t)nd.w1 >= ((int64_t)1 << 32)) nd.kind = 1;
-            (void)wu1;
             if (skel_stride == 1 && nd.kind == 2) nd.kind = 1;
+        }
+        // height-1 children of narrow (kind 0) combines are virtual: those
+        // kernels read them through TabAcc / stage_rows, which evaluate the
+        // closed form from NX (the wide kernels need materialised slabs)
+        if (virt_on)
+            for (auto &nd : t->nodes) {
+                if (nd.upper < 0 || nd.kind != 0) continue;
+                for (int32_t ch : {nd.upper, nd.lower}) {
+                    NodeH &cn = t->nodes[ch];
+                    if (cn.upper >= 0 && cn.height == 1 && !cn.virt) {
+                        cn.virt = true;
+                        ++t->nvirt;
+                    }
+                }
+            }
+        for (auto &nd : t->nodes) {
+            if (nd.upper < 0 || nd.virt) continue;
             // every table starts on a 128-byte boundary (vector / async copies)
             tab_elems = (tab_elems + 31) / 32 * 32;
             nd.reach_off = tab_elems;
@@ -483,7 +512,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
         // kmax rows of every combine (written by the kernel that finishes each row:
         // narrow / skeleton / finalize -- no initialisation needed)
         for (auto &nd : t->nodes) {
-            if (nd.upper < 0) continue;
+            if (nd.upper < 0 || nd.virt) continue;
             nd.kmax_off = tab_elems;
             tab_elems += (n1 + 63) / 64 * 64;
         }
@@ -506,6 +535,8 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
         lc.with_trace = t->with_trace;
         lc.skel_stride = skel_stride;
         lc.thread_max_w1 = thread_max_w1;
+        lc.virt_on = virt_on;
+        lc.nvirt = t->nvirt;
         lc.nodes.assign(t->nodes.begin(), t->nodes.end());
         lc.root = t->root;
         lc.nleaves = t->nleaves;
@@ -525,6 +556,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     size_t o_wids = take((size_t)std::max(ncomb, 1) * 4);
     size_t o_lnodes = take((size_t)std::max(t->nleaves, 1) * 4);
     size_t o_lrows = take((size_t)std::max(t->nleaves, 1) * 4);
+    size_t o_vnodes = take((size_t)std::max(t->nvirt, 1) * 12);
     size_t meta_end = off;
     t->arena_bytes = off;
 
@@ -554,6 +586,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     t->d_walk_ids = (int32_t *)(A + o_wids);
     t->d_leaf_nodes = (int32_t *)(A + o_lnodes);
     t->d_leaf_rows = (int32_t *)(A + o_lrows);
+    t->d_vnodes = (int32_t *)(A + o_vnodes);
 
     // ---- host-side metadata: level plan, descriptors, walk nodes ----
     const size_t meta_bytes = meta_end - o_meta;
@@ -570,6 +603,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     int32_t *hids = (int32_t *)(meta + (o_wids - o_meta));
     int32_t *hln = (int32_t *)(meta + (o_lnodes - o_meta));
     int32_t *hlr = (int32_t *)(meta + (o_lrows - o_meta));
+    int32_t *hvn = (int32_t *)(meta + (o_vnodes - o_meta));
 
     // ---- enqueue: inputs, leaf step; then the levels as they are planned ----
     const cudaStream_t s = t->stream;
@@ -595,13 +629,20 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
         ++t->launches;                       \
     } while (0)
 
-    int32_t li = 0;
-    for (int32_t id = 0; id < nn; ++id)
-        if (t->nodes[id].upper < 0) {
+    int32_t li = 0, vi = 0;
+    for (int32_t id = 0; id < nn; ++id) {
+        const NodeH &nd = t->nodes[id];
+        if (nd.upper < 0) {
             hln[li] = id;
-            hlr[li] = t->nodes[id].leaf_row;
+            hlr[li] = nd.leaf_row;
             ++li;
+        } else if (nd.virt) {
+            hvn[3 * vi] = id;
+            hvn[3 * vi + 1] = t->nodes[nd.upper].leaf_row;
+            hvn[3 * vi + 2] = t->nodes[nd.lower].leaf_row;
+            ++vi;
         }
+    }
 
     if (t->timing && t->ev_ok) BCK(cudaEventRecord(t->ev[0], s));
     const uint8_t *rows_slab = rows + (top_row - 1);
@@ -622,8 +663,9 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     BCKL(launch_nx(t->d_cols, (int32_t)n, t->d_nx, t->d_sym_wstar, s));
     BCKL(launch_leaf_wstar(t->d_rows, t->d_leaf_nodes, t->d_leaf_rows, t->nleaves,
                            t->d_sym_wstar, t->d_node_wstar, s));
-    bool ev1_done = false;  // ev[1]: just before the first level's descriptors
     const Ctx c = t->ctx();
+    if (t->nvirt > 0) BCKL(launch_virtual_wstar(c, t->d_vnodes, t->nvirt, t->d_node_wstar, s));
+    bool ev1_done = false;  // ev[1]: just before the first level's descriptors
     auto launch_entry = [&](const LaunchH &L) -> int {
         const CombineDesc *dd = t->d_descs + L.desc_off;
         if (L.kind <= 1) return launch_combine(L.kind, dd, L.count, c, L.shift, L.key64, s);
@@ -655,7 +697,8 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     // node ids bucketed by height (ascending id order kept): O(nodes) planning
     std::vector<std::vector<int32_t>> by_height(maxh + 1);
     for (int32_t id = 0; id < nn; ++id)
-        if (t->nodes[id].upper >= 0) by_height[t->nodes[id].height].push_back(id);
+        if (t->nodes[id].upper >= 0 && !t->nodes[id].virt)
+            by_height[t->nodes[id].height].push_back(id);
     // levels are flushed (descriptors copied, kernels launched) in three
     // groups -- the first level, the next two, the rest -- so the GPU starts
     // early and runs while the host plans, with only three extra copies in
@@ -795,7 +838,8 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
         w.lower = nd.lower;
         w.w1 = nd.w1;
         w.is_leaf = nd.upper < 0;
-        w.trace = (nd.upper >= 0 && t->with_trace) ? t->d_tables + nd.trace_off : nullptr;
+        w.trace = (nd.upper >= 0 && !nd.virt && t->with_trace) ? t->d_tables + nd.trace_off
+                                                                : nullptr;
         if (nd.upper >= 0) {
             w.U = t->tab(nd.upper);
             w.L = t->tab(nd.lower);
@@ -985,6 +1029,11 @@ int lcsg_node_wstar(lcsg_handle h, int32_t node, int32_t *wstar) {
     return LCSG_OK;
 }
 
+// Leaves and virtual height-1 nodes have no table in the arena; the API
+// materialises one on first access (reach [+ trace] + kmax, cached per node):
+// leaves by leaf_table_kernel, virtual nodes by the leaf-pair combine kernel
+// (the same kernel that computes a stored height-1 node, INF-cell traces
+// included).
 static int leaf_device(lcsg_handle h, int32_t node, int32_t **reach) {
     auto it = h->leaf_cache.find(node);
     if (it != h->leaf_cache.end()) {
@@ -994,19 +1043,44 @@ static int leaf_device(lcsg_handle h, int32_t node, int32_t **reach) {
     const NodeH &nd = h->nodes[node];
     const int64_t n1 = h->n + 1;
     int32_t *buf = nullptr;
-    CK(pool_alloc((void **)&buf, (size_t)(n1 * nd.w1 + n1) * 4, h->device, h->stream));
-    h->leaf_cache[node] = buf;
-    CKL(launch_leaf_table(h->ctx(), nd.leaf_row, nd.w1, buf, buf + n1 * nd.w1, h->stream));
+    if (nd.virt) {
+        // reach | trace | kmax | wstar, then the combine descriptor
+        const size_t tab = (size_t)(n1 * nd.w1);
+        const size_t desc_off = align_up((2 * tab + n1 + 1) * 4);
+        CK(pool_alloc((void **)&buf, desc_off + sizeof(CombineDesc), h->device, h->stream));
+        h->leaf_cache[node] = buf;
+        CombineDesc d;
+        std::memset(&d, 0, sizeof(d));
+        d.U = h->tab(nd.upper);
+        d.L = h->tab(nd.lower);
+        d.out_reach = buf;
+        d.out_trace = buf + tab;
+        d.out_kmax = buf + 2 * tab;
+        d.out_wstar = buf + 2 * tab + n1;
+        d.w1 = nd.w1;
+        d.node = node;
+        CombineDesc *dd = (CombineDesc *)((char *)buf + desc_off);
+        CK(cudaMemcpyAsync(dd, &d, sizeof(d), cudaMemcpyHostToDevice, h->stream));
+        const int shift = bits_for(std::max(h->nodes[nd.upper].w1 - 1, 1));
+        CKL(launch_narrow_leafpair(dd, 1, h->ctx(), shift, need_key64(bits_for(h->inf), shift),
+                                   h->stream));
+    } else {
+        CK(pool_alloc((void **)&buf, (size_t)(n1 * nd.w1 + n1) * 4, h->device, h->stream));
+        h->leaf_cache[node] = buf;
+        CKL(launch_leaf_table(h->ctx(), nd.leaf_row, nd.w1, buf, buf + n1 * nd.w1, h->stream));
+    }
     ++h->launches;
     *reach = buf;
     return LCSG_OK;
 }
 
+static bool materialised_on_demand(const NodeH &nd) { return nd.upper < 0 || nd.virt; }
+
 int lcsg_node_reach_device(lcsg_handle h, int32_t node, void **dev_ptr) {
     if (!h || node < 0 || node >= (int32_t)h->nodes.size()) return fail(LCSG_EINVAL, "bad node");
     DeviceGuard g(h->device);
     const NodeH &nd = h->nodes[node];
-    if (nd.upper < 0) {
+    if (materialised_on_demand(nd)) {
         int32_t *p = nullptr;
         int rc = leaf_device(h, node, &p);
         if (rc) return rc;
@@ -1031,6 +1105,14 @@ static int copy_node(lcsg_handle h, int32_t node, int which, int32_t *host_out) 
         if (rc) return rc;
         src = which == 0 ? p : p + n1 * nd.w1;
         elems = which == 0 ? (size_t)(n1 * nd.w1) : (size_t)n1;
+    } else if (nd.virt) {
+        if (which == 1 && !h->with_trace) return fail(LCSG_EINVAL, "table was built without traces");
+        int32_t *p = nullptr;
+        int rc = leaf_device(h, node, &p);
+        if (rc) return rc;
+        const size_t tab = (size_t)(n1 * nd.w1);
+        src = p + which * tab;  // reach | trace | kmax
+        elems = which == 2 ? (size_t)n1 : tab;
     } else if (which == 0) {
         src = h->d_tables + nd.reach_off;
         elems = (size_t)(n1 * nd.w1);

@@ -11,12 +11,20 @@ namespace lcsg {
 // (single string row, solver.py:72-88) are never materialised on the hot
 // path: their weight-1 column is the next-occurrence row NX[sym] (built once
 // per solve by the leaf kernel) and their weight-0 column is r+1.
+//
+// A VIRTUAL height-1 node (a 2-row slab whose parent is a narrow combine, n
+// >= 2) is never materialised either: its (n+1) x 3 table is a closed form
+// of its two leaves' NX rows (virtual_get below), read wherever the table
+// would have been read -- the leaf-pair level costs no launch and no HBM
+// round trip.
 struct TabDev {
-    const int32_t *reach;  // nullptr for a leaf
-    const int32_t *kmax;   // nullptr for a leaf
+    const int32_t *reach;  // nullptr for a leaf / virtual node
+    const int32_t *kmax;   // nullptr for a leaf / virtual node
     const int32_t *wstar;  // device scalar (node_wstar[node])
     int32_t w1;            // table width = min(slab rows, n) + 1
-    int32_t leaf_row;      // leaf: 0-based index into the slab's row string; else -1
+    int32_t leaf_row;      // leaf: 0-based index into the slab's row string; virtual
+                           // node: its upper leaf's row; else -1
+    int32_t leaf2;         // virtual node: its lower leaf's row + 1; else 0
 };
 
 // Per-solve constants, passed by value to every kernel.
@@ -42,8 +50,10 @@ struct CombineDesc {
 struct TabAcc {
     const int32_t *reach;
     const int32_t *kmax;
-    const int32_t *nx;  // leaf only
+    const int32_t *nx;   // leaf, or a virtual node's upper leaf
+    const int32_t *nx2;  // virtual node's lower leaf (nullptr otherwise)
     int32_t w1;
+    int32_t inf;
 };
 
 __device__ __forceinline__ TabAcc resolve(const TabDev &t, const Ctx &c) {
@@ -51,18 +61,38 @@ __device__ __forceinline__ TabAcc resolve(const TabDev &t, const Ctx &c) {
     a.reach = t.reach;
     a.kmax = t.kmax;
     a.w1 = t.w1;
+    a.inf = c.inf;
     a.nx = t.leaf_row >= 0 ? c.nx + (size_t)c.rows[t.leaf_row] * (size_t)(c.n + 1) : nullptr;
+    a.nx2 = t.leaf2 > 0 ? c.nx + (size_t)c.rows[t.leaf2 - 1] * (size_t)(c.n + 1) : nullptr;
     return a;
+}
+
+// Row r of a virtual height-1 node = combine of leaf a (upper) and leaf b
+// (lower) (solver.py:91-110 on two _base_table leaves): U = (r+1, A), A =
+// NX_a[r]; L row x-1 = (x, NX_b[x-1]).  Weight 0: r+1.  Weight 1: min over
+// k = 0 (L[r][1] = NX_b[r]) and k = 1 (L[A-1][0] = A).  Weight 2: only k = 1
+// (L[A-1][1] = NX_b[A-1]).
+__device__ __forceinline__ int32_t virtual_get(const TabAcc &t, int64_t r, int32_t d) {
+    if (d == 0) return (int32_t)(r + 1);
+    const int32_t xa = __ldg(t.nx + r);
+    if (d == 1) return min(__ldg(t.nx2 + r), xa);
+    return xa < t.inf ? __ldg(t.nx2 + (xa - 1)) : t.inf;
 }
 
 // Entry (r, d) of a table, d <= w1-1 (breakout.py:37-55 for leaves).
 __device__ __forceinline__ int32_t tab_get(const TabAcc &t, int64_t r, int32_t d) {
+    if (t.nx2) return virtual_get(t, r, d);
     if (t.nx) return d == 0 ? (int32_t)(r + 1) : __ldg(t.nx + r);
     return __ldg(t.reach + r * (int64_t)t.w1 + d);
 }
 
 // kmax of row r (solver.py:84,104: (reach < inf).sum - 1).
 __device__ __forceinline__ int32_t tab_kmax(const TabAcc &t, int64_t r, int32_t inf) {
+    if (t.nx2) {
+        const int32_t xa = __ldg(t.nx + r);
+        if (xa < inf && __ldg(t.nx2 + (xa - 1)) < inf) return 2;
+        return min(__ldg(t.nx2 + r), xa) < inf ? 1 : 0;
+    }
     if (t.nx) return (t.w1 == 2 && __ldg(t.nx + r) < inf) ? 1 : 0;
     return __ldg(t.kmax + r);
 }
@@ -104,6 +134,10 @@ int launch_nx(const uint8_t *cols, int32_t n, int32_t *nx, int32_t *sym_wstar, c
 int launch_leaf_wstar(const uint8_t *rows, const int32_t *leaf_nodes, const int32_t *leaf_rows,
                       int32_t nleaves, const int32_t *sym_wstar, int32_t *node_wstar,
                       cudaStream_t s);
+// wstar of the virtual height-1 nodes: vnodes[3t..3t+2] = (node, upper leaf
+// row, lower leaf row)
+int launch_virtual_wstar(Ctx c, const int32_t *vnodes, int32_t nvirt, int32_t *node_wstar,
+                         cudaStream_t s);
 int launch_leaf_table(Ctx c, int32_t leaf_row, int32_t w1, int32_t *reach, int32_t *kmax,
                       cudaStream_t s);
 int launch_base_case_row(const uint8_t *cols, int32_t n, uint8_t sym, int32_t *out,

@@ -106,6 +106,31 @@ int launch_leaf_wstar(const uint8_t *rows, const int32_t *leaf_nodes, const int3
     return 0;
 }
 
+// wstar of the virtual height-1 nodes (solver.py:108, max over rows of kmax):
+// kmax of row r is 2 iff a occurs at some q >= r and b after it, 1 iff a or b
+// occurs at or after r -- both are largest at r = 0.
+__global__ void virtual_wstar_kernel(Ctx c, const int32_t *__restrict__ vnodes, int32_t nvirt,
+                                     int32_t *__restrict__ node_wstar) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nvirt) return;
+    TabDev d;
+    d.reach = nullptr;
+    d.kmax = nullptr;
+    d.wstar = nullptr;
+    d.w1 = 3;
+    d.leaf_row = vnodes[3 * t + 1];
+    d.leaf2 = vnodes[3 * t + 2] + 1;
+    node_wstar[vnodes[3 * t]] = tab_kmax(resolve(d, c), 0, c.inf);
+}
+
+int launch_virtual_wstar(Ctx c, const int32_t *vnodes, int32_t nvirt, int32_t *node_wstar,
+                         cudaStream_t s) {
+    if (nvirt <= 0) return 0;
+    virtual_wstar_kernel<<<(nvirt + 255) / 256, 256, 0, s>>>(c, vnodes, nvirt, node_wstar);
+    LCSG_LAUNCH_CHECK();
+    return 0;
+}
+
 // Materialise one leaf table (solver.py:72-88) -- only for API copy-out.
 __global__ void leaf_table_kernel(Ctx c, int32_t leaf_row, int32_t w1, int32_t *reach,
                                   int32_t *kmax) {
@@ -535,7 +560,25 @@ __global__ void walk_trace_kernel(const WalkNode *__restrict__ nodes, const int3
     const int32_t id = ids[t];
     const WalkNode nd = nodes[id];
     const int32_t i = wi[id], jj = wj[id];
-    const int32_t k = nd.trace[((int64_t)i - 1) * nd.w1 + jj];
+    int32_t k = 0;
+    if (nd.trace) {
+        k = nd.trace[((int64_t)i - 1) * nd.w1 + jj];
+    } else {
+        // a virtual node keeps no trace: first-wins retrace over its (at most
+        // 3) splits (solver.py:165-177)
+        const TabAcc U = resolve(nd.U, c), L = resolve(nd.L, c);
+        const int32_t inf = c.inf;
+        const int32_t hi = min(jj, tab_kmax(U, (int64_t)i - 1, inf));
+        int32_t best = INT32_MAX;
+        for (int32_t kk = 0; kk <= hi; ++kk) {
+            const int32_t x = tab_get(U, (int64_t)i - 1, kk);
+            const int32_t v = (x < inf && jj - kk < L.w1) ? tab_get(L, (int64_t)x - 1, jj - kk) : inf;
+            if (v < best) {
+                best = v;
+                k = kk;
+            }
+        }
+    }
     walk_children(nd, nodes, c, i, jj, k, wi, wj, cols_out);
 }
 

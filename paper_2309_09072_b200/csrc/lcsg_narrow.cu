@@ -93,7 +93,18 @@ template <int PT, int NT>
 __device__ __forceinline__ void stage_rows(int32_t *dst, const TabAcc &t, int64_t row0,
                                            int32_t nrows, int32_t inf) {
     const int tid = threadIdx.x;
-    if (t.nx) {  // leaf: (r + 1, NX[sym][r]) (breakout.py:37-55)
+    if (t.nx2) {  // virtual height-1 node: closed form of its two leaves
+        for (int r = tid; r < nrows; r += NT) {
+            int32_t *d = dst + r * PT;
+            const int64_t row = row0 + r;
+            const int32_t xa = __ldg(t.nx + row);
+            d[0] = (int32_t)(row + 1);
+            d[1] = min(__ldg(t.nx2 + row), xa);
+            d[2] = xa < inf ? __ldg(t.nx2 + (xa - 1)) : inf;
+#pragma unroll
+            for (int k = 3; k < PT; ++k) d[k] = inf;
+        }
+    } else if (t.nx) {  // leaf: (r + 1, NX[sym][r]) (breakout.py:37-55)
         const int32_t *nx = t.nx + row0;
         const bool w2 = t.w1 > 1;
         for (int r = tid; r < nrows; r += NT) {

@@ -399,6 +399,8 @@ def test_skeleton_refine_strides(stride, monkeypatch):
     {"LCSG_SKELETON_STRIDE": "512", "LCSG_COL_BLOCK": "8"},  # row-step 64 / 8 / 1 stages
     {"LCSG_SKEL_WARP_BATCHED": "0"},                        # per-node warp DFS for w1 <= 257 skeletons
     {"LCSG_NARROW_FW": "0"},                                # narrow kernels with a runtime row width
+    {"LCSG_VIRTUAL_H1": "0"},                               # height-1 tables materialised (leaf-pair kernel)
+    {"LCSG_VIRTUAL_H1": "0", "LCSG_LEAFPAIR": "0"},         # ... and computed by the staged narrow kernel
 ])
 def test_refinement_variants(env, key64, monkeypatch):
     """Every geometry / schedule of the wide-table combine is bit-exact, with
