@@ -141,7 +141,16 @@ bool need_key64(int value_bits, int shift) {
     return value_bits + shift > 32 || env_int("LCSG_FORCE_KEY64", 0) != 0;
 }
 
-int default_skeleton_stride(int64_t n1) { return n1 <= 8193 ? 32 : 64; }
+// Skeleton stride (rows computed by the exact bisection) and column-refinement
+// block size by column count: short strings have few CTAs per level, so a
+// denser skeleton and shallower refinement stages (fewer dependent passes)
+// win; long strings amortise the refinement (measured with tools/sweep.py on
+// cfg1 256^2: 8/4 0.24 ms vs 32/8 0.32; cfg2 2048^2: 8/4 0.96 vs 1.25; cfg3
+// 4096^2: 16/4 2.20 vs 2.30; cfg4/cfg5 keep 64/8).
+int default_skeleton_stride(int64_t n1) {
+    return n1 <= 2049 ? 8 : n1 <= 4097 ? 16 : n1 <= 8193 ? 32 : 64;
+}
+int default_col_block(int64_t n1) { return n1 <= 4097 ? 4 : 8; }
 
 struct NodeH {
     int32_t top_row, bottom_row, w1, upper, lower, height, depth, leaf_row;
@@ -457,7 +466,8 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     const bool narrow_on = env_int("LCSG_NARROW", 1) != 0;
     // block size (local rows) of each column-refinement stage, power of two
     int col_block = 1;
-    while (col_block * 2 <= std::min(16, std::max(2, env_int("LCSG_COL_BLOCK", 8)))) col_block *= 2;
+    while (col_block * 2 <= std::min(16, std::max(2, env_int("LCSG_COL_BLOCK", default_col_block(n1)))))
+        col_block *= 2;
     size_t o_tab = off;
     // int32 tables of every combine node
     int64_t tab_elems = 0, scratch_elems = 0;
@@ -1404,7 +1414,8 @@ int lcsg_combine_rows(const int32_t *upper_reach, int32_t wu1, const int32_t *up
     int S = 1;
     while (S * 2 <= std::max(1, env_int("LCSG_SKELETON_STRIDE", default_skeleton_stride(n1)))) S *= 2;
     int col_block = 1;
-    while (col_block * 2 <= std::min(16, std::max(2, env_int("LCSG_COL_BLOCK", 8)))) col_block *= 2;
+    while (col_block * 2 <= std::min(16, std::max(2, env_int("LCSG_COL_BLOCK", default_col_block(n1)))))
+        col_block *= 2;
     const int P = narrow_bucket(std::max(wu1, wl1) - 1);
     if (w1 <= thread_max_w1 && P > 0 && env_int("LCSG_NARROW", 1) != 0) {
         CKL(launch_narrow(&sc->d, 1, c, shift, key64, P, s));

@@ -84,6 +84,9 @@ def census(node, U, L, inf, S=8):
             out["long"] += int(longr.sum())
             out["long_cands"] += int(ln[longr].sum())
             out["pinned"] += int(pinned.sum())
+            out["pin_eqT"] += int((fb & (Xa == Xb) & (Ta == Tb)).sum())
+            out["pin_Tdiff1"] += int((fb & (Xa == Xb) & (Ta == Tb + 1)).sum())
+            out["xa_eq_xb"] += int((fb & (Xa == Xb)).sum())
             out["inline"] += int(inl.sum())
             out["inline_cands"] += int(ln[inl].sum())
             out[f"dl{dl}_fin"] += int(fb.sum())
@@ -117,7 +120,9 @@ def main():
               f"a-INF {out['a_inf'] / tot:.2f}  tail {out['tail'] / tot:.3f} "
               f"(cands/cell {out['tail_cands'] / max(1, out['tail']):.1f})  "
               f"long {out['long'] / tot:.3f} (cands {out['long_cands'] / max(1, out['long']):.1f})  "
-              f"pinned {out['pinned'] / tot:.2f}  inline {out['inline'] / tot:.2f} "
+              f"pinned {out['pinned'] / tot:.2f} (Xa=Xb {out['xa_eq_xb'] / tot:.3f}, T equal "
+              f"{out['pin_eqT'] / tot:.3f}, T diff 1 {out['pin_Tdiff1'] / tot:.3f})  "
+              f"inline {out['inline'] / tot:.2f} "
               f"(cands {out['inline_cands'] / max(1, out['inline']):.2f})")
         print("   inline range lengths:", dict(sorted(lens.items())))
 

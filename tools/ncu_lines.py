@@ -5,8 +5,11 @@ import csv, io, subprocess, sys
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
-                     capture_output=True, text=True).stdout
+kfilter = sys.argv[3] if len(sys.argv) > 3 else None  # e.g. regex:narrow_combine_kernel<8
+cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"]
+if kfilter:
+    cmd += ["--kernel-id", kfilter] if kfilter.startswith(":") else ["-k", kfilter]
+out = subprocess.run(cmd, capture_output=True, text=True).stdout
 rows = []
 fname = "?"
 for r in csv.reader(io.StringIO(out)):
