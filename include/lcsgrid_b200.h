@@ -117,6 +117,20 @@ int lcsg_lcs_device(const uint8_t *a_dev, int64_t la, const uint8_t *b_dev, int6
                     uint32_t flags, int device, void *stream, int32_t *length, uint8_t *subseq,
                     int32_t *pos_a, int32_t *pos_b);
 
+/* Batched lcs() of `npairs` pairs of EQUAL shape (many
+ * small pairs, e.g. cfg4's planted queries): a / b hold the pairs back to back
+ * (la / lb bytes each, HOST; _device: DEVICE).  All pairs' recursion trees are
+ * built together -- one launch per tree height for the whole batch -- then one
+ * walk and one assembly.  Pair p's results: lengths[p], subseq / pos_a / pos_b
+ * + p * min(la, lb) (buffers hold npairs * min(la, lb) entries).  Each pair's
+ * result is exactly lcs(a_p, b_p) (solver.py:237-273). */
+int lcsg_lcs_batch(const uint8_t *a, int64_t la, const uint8_t *b, int64_t lb, int32_t npairs,
+                   uint32_t flags, int device, void *stream, int32_t *lengths, uint8_t *subseq,
+                   int32_t *pos_a, int32_t *pos_b);
+int lcsg_lcs_batch_device(const uint8_t *a_dev, int64_t la, const uint8_t *b_dev, int64_t lb,
+                          int32_t npairs, uint32_t flags, int device, void *stream,
+                          int32_t *lengths, uint8_t *subseq, int32_t *pos_a, int32_t *pos_b);
+
 /* ---- kernel-level mirrors, for fixture parity ---------------------------- */
 /* combine_level (_kernel.pyx:63-82) on DEVICE buffers: start columns
  * [i_lo, i_hi) of one slab pair; tables row-major with widths wu1/wl1/w1 and

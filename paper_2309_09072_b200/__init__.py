@@ -21,6 +21,7 @@ from .solver import (
     combine_row,
     lcs,
     lcs_length,
+    lcs_batch,
     lcs_many,
     recover_cross_vertices,
 )
@@ -39,6 +40,7 @@ __all__ = [
     "inf_value",
     "lcs",
     "lcs_length",
+    "lcs_batch",
     "lcs_many",
     "match_positions",
     "recover_cross_vertices",

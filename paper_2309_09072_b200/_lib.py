@@ -73,6 +73,10 @@ SIGNATURES = {
                                 _vp, _vp, _vp]),
     "lcsg_lcs_device": (ctypes.c_int, [_vp, _i64, _vp, _i64, ctypes.c_uint32, ctypes.c_int, _vp,
                                        _i32p, _vp, _vp, _vp]),
+    "lcsg_lcs_batch": (ctypes.c_int, [_vp, _i64, _vp, _i64, _i32, ctypes.c_uint32, ctypes.c_int,
+                                      _vp, _vp, _vp, _vp, _vp]),
+    "lcsg_lcs_batch_device": (ctypes.c_int, [_vp, _i64, _vp, _i64, _i32, ctypes.c_uint32,
+                                             ctypes.c_int, _vp, _vp, _vp, _vp, _vp]),
     "lcsg_combine_level": (ctypes.c_int, [_vp, _i32, _vp, _vp, _i32, _i32, _vp, _vp, _i32,
                                           ctypes.c_int, _i32, _i64, _i64, _i64, _vp]),
     "lcsg_base_case_row": (ctypes.c_int, [_vp, _i64, ctypes.c_uint8, _vp, _vp]),

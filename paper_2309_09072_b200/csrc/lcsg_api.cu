@@ -154,6 +154,7 @@ int default_col_block(int64_t n1) { return n1 <= 4097 ? 4 : 8; }
 
 struct NodeH {
     int32_t top_row, bottom_row, w1, upper, lower, height, depth, leaf_row;
+    int32_t pair = 0;  // batched solves: the pair this node belongs to
     int64_t reach_off = -1, trace_off = -1, kmax_off = -1;  // int32 element offsets
     int kind = 0;
     bool virt = false;  // virtual height-1 node: no table (TabDev closed form of its leaves)
@@ -181,6 +182,11 @@ struct lcsg_tree_s {
     bool own_stream = false;
     int64_t m_grid = 0, m_slab = 0, n = 0;
     int32_t inf = 0, top_row = 1, bottom_row = 2;
+    // batched solves (lcsg_lcs_batch): npairs independent trees of the same
+    // shape side by side -- pair p's nodes are ids [p*pair_nodes, (p+1)*pair_nodes),
+    // its tables pair_tab ints after pair p-1's; every level is one launch
+    int32_t npairs = 1, pair_nodes = 0;
+    int64_t pair_tab = 0;
     bool with_trace = true, timing = false;
     std::vector<NodeH> nodes;
     int32_t root = -1;
@@ -209,9 +215,18 @@ struct lcsg_tree_s {
         Ctx c;
         c.rows = d_rows;
         c.nx = d_nx;
+        c.nx_stride = (int64_t)256 * (n + 1);
         c.n = (int32_t)n;
         c.inf = inf;
         return c;
+    }
+    RootBatch root_batch() const {
+        RootBatch rb;
+        rb.npairs = npairs;
+        rb.pair_nodes = pair_nodes;
+        rb.pair_rows = (int32_t)m_slab;
+        rb.tab_stride = pair_tab;
+        return rb;
     }
     TabDev tab(int32_t id) const {
         const NodeH &nd = nodes[id];
@@ -219,6 +234,7 @@ struct lcsg_tree_s {
         t.w1 = nd.w1;
         t.wstar = d_node_wstar + id;
         t.leaf2 = 0;
+        t.pair = nd.pair;
         if (nd.upper < 0) {
             t.reach = nullptr;
             t.kmax = nullptr;
@@ -372,10 +388,13 @@ struct MetaLease {
 
 int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *cols, bool cols_dev,
                int64_t n, int32_t top_row, int32_t bottom_row, uint32_t flags, int device,
-               void *stream, lcsg_handle *out) {
+               void *stream, lcsg_handle *out, int32_t npairs = 1) {
     if (!out) return fail(LCSG_EINVAL, "null output handle");
     *out = nullptr;
     if (m < 0 || n < 0) return fail(LCSG_EINVAL, "negative length");
+    if (npairs < 1) return fail(LCSG_EINVAL, "npairs < 1");
+    if (npairs > 1 && !(top_row == 1 && bottom_row == m + 1))
+        return fail(LCSG_EINVAL, "batched builds cover the full grid");
     if (!(1 <= top_row && top_row < bottom_row && (int64_t)bottom_row <= m + 1))
         return fail(LCSG_EINVAL, "1 <= top_row < bottom_row <= m + 1");
     if (n > (int64_t)INT32_MAX - 4) return fail(LCSG_EINVAL, "column string too long for int32 tables");
@@ -393,6 +412,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     t->bottom_row = bottom_row;
     t->with_trace = (flags & LCSG_WITH_TRACE) != 0;
     t->timing = (flags & LCSG_TIMING) != 0;
+    t->npairs = npairs;
     if (stream) {
         t->stream = (cudaStream_t)stream;
     } else {
@@ -439,7 +459,10 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
         t->nodes.reserve(2 * t->m_slab);
         t->root = build_tree(t, top_row, bottom_row, 0);
     }
-    const int32_t nn = (int32_t)t->nodes.size();
+    const int32_t nn1 = (int32_t)t->nodes.size();  // nodes of one pair
+    const int32_t nn = nn1 * npairs;
+    const int64_t B = npairs;
+    t->pair_nodes = nn1;
     const int64_t n1 = n + 1;
 
     // ---- arena layout ----
@@ -450,15 +473,15 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
         return o;
     };
     const int64_t kmin = std::min<int64_t>(t->m_slab, n);
-    size_t o_rows = take((size_t)t->m_slab);
-    size_t o_cols = take((size_t)std::max<int64_t>(n, 1));
-    size_t o_nx = take((size_t)256 * n1 * 4);
-    size_t o_symw = take(256 * 4);
+    size_t o_rows = take((size_t)(B * t->m_slab));
+    size_t o_cols = take((size_t)std::max<int64_t>(B * n, 1));
+    size_t o_nx = take((size_t)(B * 256 * n1 * 4));
+    size_t o_symw = take((size_t)B * 256 * 4);
     size_t o_nodew = take((size_t)nn * 4);
     size_t o_wi = take((size_t)nn * 4), o_wj = take((size_t)nn * 4);
-    size_t o_path = take((size_t)(t->m_slab + 1) * 4);
-    size_t o_out = take((size_t)(1 + 2 * std::max<int64_t>(kmin, 1)) * 4);
-    size_t o_sub = take((size_t)std::max<int64_t>(kmin, 1));
+    size_t o_path = take((size_t)(B * (t->m_slab + 1)) * 4);
+    size_t o_out = take((size_t)(B * (1 + 2 * std::max<int64_t>(kmin, 1))) * 4);
+    size_t o_sub = take((size_t)(B * std::max<int64_t>(kmin, 1)));
     const int skel_thread_max = env_int("LCSG_SKEL_THREAD_MAX_W1", 65);
     const int skel_warp_max = env_int("LCSG_SKEL_WARP_MAX_W1", 257);
     // refinement mode: tiled (default) or one launch per pass ("LCSG_REFINE_PASSES=1")
@@ -555,9 +578,32 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
         lc.tab_elems = tab_elems;
         lc.scratch_elems = scratch_elems;
     }
-    tab_elems = (tab_elems + 31) / 32 * 32;
-    const int64_t scratch_base = tab_elems;
-    tab_elems += scratch_elems;
+    // pair p's tables occupy [p * pair_tab, (p+1) * pair_tab); the low-memory
+    // level scratch of every pair follows all of them
+    const int64_t pair_tab = (tab_elems + 31) / 32 * 32;
+    t->pair_tab = pair_tab;
+    const int64_t scratch_base = B * pair_tab;
+    tab_elems = scratch_base + B * scratch_elems;
+    if (B > 1) {  // replicate the tree of pair 0 for the other pairs
+        t->nodes.resize((size_t)nn);
+        for (int32_t p = 1; p < npairs; ++p)
+            for (int32_t id = 0; id < nn1; ++id) {
+                NodeH nd = t->nodes[id];
+                nd.pair = p;
+                if (nd.upper >= 0) {
+                    nd.upper += p * nn1;
+                    nd.lower += p * nn1;
+                }
+                if (nd.leaf_row >= 0) nd.leaf_row += (int32_t)(p * t->m_slab);
+                if (nd.reach_off >= 0) nd.reach_off += p * pair_tab;
+                if (nd.kmax_off >= 0) nd.kmax_off += p * pair_tab;
+                if (nd.trace_off >= 0) nd.trace_off += t->with_trace ? p * pair_tab : p * scratch_elems;
+                t->nodes[(size_t)p * nn1 + id] = nd;
+            }
+        ncomb *= npairs;
+        t->nleaves *= npairs;
+        t->nvirt *= npairs;
+    }
     off = align_up(o_tab + (size_t)tab_elems * 4);
     // metadata region (uploaded with one copy)
     size_t o_meta = off;
@@ -566,7 +612,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     size_t o_wids = take((size_t)std::max(ncomb, 1) * 4);
     size_t o_lnodes = take((size_t)std::max(t->nleaves, 1) * 4);
     size_t o_lrows = take((size_t)std::max(t->nleaves, 1) * 4);
-    size_t o_vnodes = take((size_t)std::max(t->nvirt, 1) * 12);
+    size_t o_vnodes = take((size_t)std::max(t->nvirt, 1) * 16);
     size_t meta_end = off;
     t->arena_bytes = off;
 
@@ -647,32 +693,34 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             hlr[li] = nd.leaf_row;
             ++li;
         } else if (nd.virt) {
-            hvn[3 * vi] = id;
-            hvn[3 * vi + 1] = t->nodes[nd.upper].leaf_row;
-            hvn[3 * vi + 2] = t->nodes[nd.lower].leaf_row;
+            hvn[4 * vi] = id;
+            hvn[4 * vi + 1] = t->nodes[nd.upper].leaf_row;
+            hvn[4 * vi + 2] = t->nodes[nd.lower].leaf_row;
+            hvn[4 * vi + 3] = nd.pair;
             ++vi;
         }
     }
 
     if (t->timing && t->ev_ok) BCK(cudaEventRecord(t->ev[0], s));
     const uint8_t *rows_slab = rows + (top_row - 1);
-    if (t->m_slab > 0)
-        BCK(cudaMemcpyAsync(t->d_rows, rows_slab, (size_t)t->m_slab,
+    if (t->m_slab > 0)  // batched: full grids, so the pairs' slabs are contiguous
+        BCK(cudaMemcpyAsync(t->d_rows, rows_slab, (size_t)(B * t->m_slab),
                             rows_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
     if (n > 0)
-        BCK(cudaMemcpyAsync(t->d_cols, cols, (size_t)n,
+        BCK(cudaMemcpyAsync(t->d_cols, cols, (size_t)(B * n),
                             cols_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
     // leaf lists now; the level descriptors are uploaded in groups as they
     // are planned (their kernels start while the host plans the next
     // levels), the walk nodes (extraction only) after the last level
     BCK(cudaMemcpyAsync(A + o_lnodes, meta + (o_lnodes - o_meta), meta_end - o_lnodes,
                         cudaMemcpyHostToDevice, s));
-    t->h2d_bytes = (int64_t)meta_bytes + (rows_dev ? 0 : t->m_slab) + (cols_dev ? 0 : n);
+    t->h2d_bytes = (int64_t)meta_bytes + (rows_dev ? 0 : B * t->m_slab) + (cols_dev ? 0 : B * n);
     // a pageable fallback copy is staged synchronously, so `meta_fallback` may die
     BCK(cudaMemsetAsync(t->d_node_wstar, 0, (size_t)nn * 4, s));
-    BCKL(launch_nx(t->d_cols, (int32_t)n, t->d_nx, t->d_sym_wstar, s));
+    BCKL(launch_nx(t->d_cols, (int32_t)n, npairs, t->d_nx, t->d_sym_wstar, s));
     BCKL(launch_leaf_wstar(t->d_rows, t->d_leaf_nodes, t->d_leaf_rows, t->nleaves,
-                           t->d_sym_wstar, t->d_node_wstar, s));
+                           (int32_t)std::max<int64_t>(t->m_slab, 1), t->d_sym_wstar,
+                           t->d_node_wstar, s));
     const Ctx c = t->ctx();
     if (t->nvirt > 0) BCKL(launch_virtual_wstar(c, t->d_vnodes, t->nvirt, t->d_node_wstar, s));
     bool ev1_done = false;  // ev[1]: just before the first level's descriptors
@@ -842,7 +890,8 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     for (int32_t id = 0; id < nn; ++id) {
         const NodeH &nd = t->nodes[id];
         WalkNode &w = hw[id];
-        w.top_row = nd.top_row - t->top_row + 1;  // relative: cols index = top_row - 1
+        // relative: path index = top_row - 1 (pair p's path after the others')
+        w.top_row = nd.top_row - t->top_row + 1 + (int32_t)(nd.pair * (t->m_slab + 1));
         w.bottom_row = nd.bottom_row;
         w.upper = nd.upper;
         w.lower = nd.lower;
@@ -893,7 +942,8 @@ int run_walk(lcsg_tree_s *t, int32_t j, int32_t i_start = 1) {
     const cudaStream_t s = t->stream;
     const Ctx c = t->ctx();
     const TabDev rt = t->tab(t->root);
-    CKL(launch_walk_root(t->d_walk, t->root, c, rt, j, i_start, t->d_wi, t->d_wj, t->d_path, s));
+    CKL(launch_walk_root(t->d_walk, t->root, c, rt, j, i_start, t->d_wi, t->d_wj, t->d_path,
+                         t->root_batch(), s));
     ++t->launches;
     const bool retrace = !t->with_trace;
     for (auto &dr : t->depth_ranges) {
@@ -901,7 +951,8 @@ int run_walk(lcsg_tree_s *t, int32_t j, int32_t i_start = 1) {
                               t->d_path, retrace, t->walk_shift, t->walk_key64, s));
         ++t->launches;
     }
-    CKL(launch_walk_final(c, rt, i_start, (int32_t)t->m_slab, t->d_wj + t->root, t->d_path, s));
+    CKL(launch_walk_final(c, rt, i_start, (int32_t)t->m_slab, t->root, t->d_wj, t->d_path,
+                          t->root_batch(), s));
     ++t->launches;
     return LCSG_OK;
 }
@@ -917,45 +968,55 @@ struct DeviceGuard {
     }
 };
 
+// lcs() (solver.py:237-273) of `npairs` pairs of equal shape: a / b hold the
+// pairs back to back (la / lb bytes each); pair p's outputs land at
+// length[p], subseq / pos_a / pos_b + p * min(la, lb).  One build of all the
+// pairs' trees (one launch per height), one walk, one assembly.
 int lcs_impl(const uint8_t *a, int64_t la, const uint8_t *b, int64_t lb, bool dev, uint32_t flags,
              int device, void *stream, int32_t *length, uint8_t *subseq, int32_t *pos_a,
-             int32_t *pos_b) {
+             int32_t *pos_b, int32_t npairs = 1) {
     if (!length) return fail(LCSG_EINVAL, "null length pointer");
-    *length = 0;
+    if (npairs < 1) return fail(LCSG_EINVAL, "npairs < 1");
+    for (int32_t p = 0; p < npairs; ++p) length[p] = 0;
     if (la == 0 || lb == 0) return LCSG_OK;  // solver.py:255-256
     const bool swapped = la > lb;             // solver.py:257-258
     const uint8_t *rows = swapped ? b : a, *cols = swapped ? a : b;
     const int64_t m = swapped ? lb : la, n = swapped ? la : lb;
     lcsg_handle h = nullptr;
-    int rc = build_impl(rows, dev, m, cols, dev, n, 1, (int32_t)(m + 1), flags, device, stream, &h);
+    int rc = build_impl(rows, dev, m, cols, dev, n, 1, (int32_t)(m + 1), flags, device, stream, &h,
+                        npairs);
     if (rc) return rc;
     DeviceGuard g(h->device);
+    const int64_t k = std::min(m, n), ostride = 1 + 2 * k;
     rc = run_walk(h, -1);
     if (rc == 0) {
         int r2 = launch_assemble(h->d_rows, (int32_t)m, h->d_cols, (int32_t)n, h->d_path, h->d_out,
-                                 h->d_out + 1, h->d_out + 1 + std::min(m, n), h->d_subseq,
-                                 h->stream);
+                                 h->d_out + 1, h->d_out + 1 + k, h->d_subseq, h->stream, npairs,
+                                 ostride, k);
         if (r2) rc = fail(LCSG_ECUDA, std::string("assemble: ") + cudaGetErrorString((cudaError_t)r2));
         ++h->launches;
     }
     if (rc == 0) {
-        const int64_t k = std::min(m, n);
-        std::vector<int32_t> hb((size_t)(1 + 2 * k));
-        std::vector<uint8_t> hs((size_t)k);
+        std::vector<int32_t> hb((size_t)(npairs * ostride));
+        std::vector<uint8_t> hs((size_t)(npairs * k));
         cudaError_t e = cudaMemcpyAsync(hb.data(), h->d_out, hb.size() * 4, cudaMemcpyDeviceToHost, h->stream);
         if (e == cudaSuccess)
-            e = cudaMemcpyAsync(hs.data(), h->d_subseq, (size_t)k, cudaMemcpyDeviceToHost, h->stream);
+            e = cudaMemcpyAsync(hs.data(), h->d_subseq, hs.size(), cudaMemcpyDeviceToHost, h->stream);
         if (e == cudaSuccess && h->timing && h->ev_ok) e = cudaEventRecord(h->ev[3], h->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
         if (e != cudaSuccess) {
             rc = fail(LCSG_ECUDA, std::string("lcs result copy: ") + cudaGetErrorString(e));
         } else {
-            const int32_t len = hb[0];
-            *length = len;
-            int32_t *rp = swapped ? pos_b : pos_a, *cp = swapped ? pos_a : pos_b;
-            if (subseq) std::memcpy(subseq, hs.data(), (size_t)len);
-            if (rp) std::memcpy(rp, hb.data() + 1, (size_t)len * 4);
-            if (cp) std::memcpy(cp, hb.data() + 1 + k, (size_t)len * 4);
+            h->d2h_bytes += (int64_t)(hb.size() * 4 + hs.size());
+            for (int32_t p = 0; p < npairs; ++p) {
+                const int32_t *ob = hb.data() + p * ostride;
+                const int32_t len = ob[0];
+                length[p] = len;
+                int32_t *rp = swapped ? pos_b : pos_a, *cp = swapped ? pos_a : pos_b;
+                if (subseq) std::memcpy(subseq + p * k, hs.data() + p * k, (size_t)len);
+                if (rp) std::memcpy(rp + p * k, ob + 1, (size_t)len * 4);
+                if (cp) std::memcpy(cp + p * k, ob + 1 + k, (size_t)len * 4);
+            }
         }
     }
     destroy(h);
@@ -1268,6 +1329,20 @@ int lcsg_lcs_device(const uint8_t *a_dev, int64_t la, const uint8_t *b_dev, int6
                     uint32_t flags, int device, void *stream, int32_t *length, uint8_t *subseq,
                     int32_t *pos_a, int32_t *pos_b) {
     return lcs_impl(a_dev, la, b_dev, lb, true, flags, device, stream, length, subseq, pos_a, pos_b);
+}
+
+int lcsg_lcs_batch(const uint8_t *a, int64_t la, const uint8_t *b, int64_t lb, int32_t npairs,
+                   uint32_t flags, int device, void *stream, int32_t *lengths, uint8_t *subseq,
+                   int32_t *pos_a, int32_t *pos_b) {
+    return lcs_impl(a, la, b, lb, false, flags, device, stream, lengths, subseq, pos_a, pos_b,
+                    npairs);
+}
+
+int lcsg_lcs_batch_device(const uint8_t *a_dev, int64_t la, const uint8_t *b_dev, int64_t lb,
+                          int32_t npairs, uint32_t flags, int device, void *stream,
+                          int32_t *lengths, uint8_t *subseq, int32_t *pos_a, int32_t *pos_b) {
+    return lcs_impl(a_dev, la, b_dev, lb, true, flags, device, stream, lengths, subseq, pos_a,
+                    pos_b, npairs);
 }
 
 int lcsg_combine_level(const int32_t *upper_reach, int32_t wu1, const int32_t *upper_kmax,

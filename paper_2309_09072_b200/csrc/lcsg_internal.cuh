@@ -25,12 +25,15 @@ struct TabDev {
     int32_t leaf_row;      // leaf: 0-based index into the slab's row string; virtual
                            // node: its upper leaf's row; else -1
     int32_t leaf2;         // virtual node: its lower leaf's row + 1; else 0
+    int32_t pair;          // batched solves: the pair whose NX block a leaf reads (0 otherwise)
 };
 
 // Per-solve constants, passed by value to every kernel.
 struct Ctx {
-    const uint8_t *rows;  // slab row string (device)
+    const uint8_t *rows;  // slab row string (device; batched: the pairs' slabs back to back)
     const int32_t *nx;    // 256 x (n+1): NX[s][r] = (first q >= r with cols[q]==s) + 2, else n+2
+                          // (batched: one such block per pair, nx_stride ints apart)
+    int64_t nx_stride;    // 256 * (n+1)
     int32_t n;
     int32_t inf;  // n + 2 (seqcore.py:37-39)
 };
@@ -62,8 +65,9 @@ __device__ __forceinline__ TabAcc resolve(const TabDev &t, const Ctx &c) {
     a.kmax = t.kmax;
     a.w1 = t.w1;
     a.inf = c.inf;
-    a.nx = t.leaf_row >= 0 ? c.nx + (size_t)c.rows[t.leaf_row] * (size_t)(c.n + 1) : nullptr;
-    a.nx2 = t.leaf2 > 0 ? c.nx + (size_t)c.rows[t.leaf2 - 1] * (size_t)(c.n + 1) : nullptr;
+    const int32_t *nxp = c.nx + (size_t)t.pair * (size_t)c.nx_stride;
+    a.nx = t.leaf_row >= 0 ? nxp + (size_t)c.rows[t.leaf_row] * (size_t)(c.n + 1) : nullptr;
+    a.nx2 = t.leaf2 > 0 ? nxp + (size_t)c.rows[t.leaf2 - 1] * (size_t)(c.n + 1) : nullptr;
     return a;
 }
 
@@ -130,12 +134,15 @@ struct WalkNode {
 
 // ---- launchers implemented in lcsg_kernels.cu ------------------------------
 namespace lcsg {
-int launch_nx(const uint8_t *cols, int32_t n, int32_t *nx, int32_t *sym_wstar, cudaStream_t s);
+// NX of `npairs` column strings of length n (back to back) -> npairs blocks
+int launch_nx(const uint8_t *cols, int32_t n, int32_t npairs, int32_t *nx, int32_t *sym_wstar,
+              cudaStream_t s);
+// leaf_rows are rows of the concatenated slabs (pair = row / pair_rows)
 int launch_leaf_wstar(const uint8_t *rows, const int32_t *leaf_nodes, const int32_t *leaf_rows,
-                      int32_t nleaves, const int32_t *sym_wstar, int32_t *node_wstar,
-                      cudaStream_t s);
-// wstar of the virtual height-1 nodes: vnodes[3t..3t+2] = (node, upper leaf
-// row, lower leaf row)
+                      int32_t nleaves, int32_t pair_rows, const int32_t *sym_wstar,
+                      int32_t *node_wstar, cudaStream_t s);
+// wstar of the virtual height-1 nodes: vnodes[4t..4t+3] = (node, upper leaf
+// row, lower leaf row, pair)
 int launch_virtual_wstar(Ctx c, const int32_t *vnodes, int32_t nvirt, int32_t *node_wstar,
                          cudaStream_t s);
 int launch_leaf_table(Ctx c, int32_t leaf_row, int32_t w1, int32_t *reach, int32_t *kmax,
@@ -178,12 +185,23 @@ int launch_finalize_rows(const CombineDesc *descs, int32_t ndesc, Ctx c, int32_t
 int launch_walk_level(const WalkNode *nodes, const int32_t *ids, int32_t count, Ctx c,
                       int32_t *wi, int32_t *wj, int32_t *cols_out, bool retrace, int key_shift,
                       bool key64, cudaStream_t s);
+// Batched walks: pair p's root is root + p * pair_nodes, its table is
+// root_tab with table pointers advanced by p * tab_stride ints (a leaf root:
+// leaf_row advanced by p * pair_rows), its path lands at cols_out + p * (m+1).
+struct RootBatch {
+    int32_t npairs = 1, pair_nodes = 0, pair_rows = 0;
+    int64_t tab_stride = 0;
+};
 int launch_walk_root(const WalkNode *nodes, int32_t root, Ctx c, TabDev root_tab, int32_t j,
-                     int32_t i_start, int32_t *wi, int32_t *wj, int32_t *cols_out,
+                     int32_t i_start, int32_t *wi, int32_t *wj, int32_t *cols_out, RootBatch rb,
                      cudaStream_t s);
-int launch_walk_final(Ctx c, TabDev root_tab, int32_t i_start, int32_t m, const int32_t *wj_root,
-                      int32_t *cols_out, cudaStream_t s);
+int launch_walk_final(Ctx c, TabDev root_tab, int32_t i_start, int32_t m, int32_t root,
+                      const int32_t *wj, int32_t *cols_out, RootBatch rb, cudaStream_t s);
+// assemble_lcs of `npairs` pairs: pair p reads rows + p*m, cols + p*n, path +
+// p*(m+1) and writes out_len[p * out_stride], row_pos / col_pos + p * out_stride,
+// subseq + p * sub_stride
 int launch_assemble(const uint8_t *rows, int32_t m, const uint8_t *cols, int32_t n,
                     const int32_t *path, int32_t *out_len, int32_t *row_pos, int32_t *col_pos,
-                    uint8_t *subseq, cudaStream_t s);
+                    uint8_t *subseq, cudaStream_t s, int32_t npairs = 1, int64_t out_stride = 0,
+                    int64_t sub_stride = 0);
 }  // namespace lcsg

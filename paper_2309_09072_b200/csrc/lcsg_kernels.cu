@@ -32,12 +32,15 @@ constexpr int NX_THREADS = 1024;
 constexpr int NX_PER_THREAD = 4;
 constexpr int NX_CHUNK = NX_THREADS * NX_PER_THREAD;
 
-__global__ void __launch_bounds__(NX_THREADS) nx_kernel(const uint8_t *__restrict__ cols,
+__global__ void __launch_bounds__(NX_THREADS) nx_kernel(const uint8_t *__restrict__ cols_all,
                                                         int32_t n, int32_t *__restrict__ nx,
-                                                        int32_t *__restrict__ sym_wstar) {
+                                                        int32_t *__restrict__ sym_wstar_all) {
     const int s = blockIdx.x;
+    const int32_t pair = blockIdx.y;  // batched solves: one NX block per pair
+    const uint8_t *__restrict__ cols = cols_all + (size_t)pair * (size_t)n;
+    int32_t *sym_wstar = sym_wstar_all + 256 * pair;
     const int32_t inf = n + 2;
-    int32_t *row = nx + (size_t)s * (size_t)(n + 1);
+    int32_t *row = nx + ((size_t)pair * 256 + s) * (size_t)(n + 1);
     __shared__ int32_t warp_min[NX_THREADS / 32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     int32_t carry = inf;  // min over everything right of the current chunk
@@ -80,8 +83,9 @@ __global__ void __launch_bounds__(NX_THREADS) nx_kernel(const uint8_t *__restric
     if (threadIdx.x == 0) sym_wstar[s] = (n >= 1 && carry < inf) ? 1 : 0;
 }
 
-int launch_nx(const uint8_t *cols, int32_t n, int32_t *nx, int32_t *sym_wstar, cudaStream_t s) {
-    nx_kernel<<<256, NX_THREADS, 0, s>>>(cols, n, nx, sym_wstar);
+int launch_nx(const uint8_t *cols, int32_t n, int32_t npairs, int32_t *nx, int32_t *sym_wstar,
+              cudaStream_t s) {
+    nx_kernel<<<dim3(256, npairs), NX_THREADS, 0, s>>>(cols, n, nx, sym_wstar);
     LCSG_LAUNCH_CHECK();
     return 0;
 }
@@ -90,18 +94,21 @@ int launch_nx(const uint8_t *cols, int32_t n, int32_t *nx, int32_t *sym_wstar, c
 __global__ void leaf_wstar_kernel(const uint8_t *__restrict__ rows,
                                   const int32_t *__restrict__ leaf_nodes,
                                   const int32_t *__restrict__ leaf_rows, int32_t nleaves,
-                                  const int32_t *__restrict__ sym_wstar,
+                                  int32_t pair_rows, const int32_t *__restrict__ sym_wstar,
                                   int32_t *__restrict__ node_wstar) {
     int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t < nleaves) node_wstar[leaf_nodes[t]] = sym_wstar[rows[leaf_rows[t]]];
+    if (t < nleaves) {
+        const int32_t r = leaf_rows[t];
+        node_wstar[leaf_nodes[t]] = sym_wstar[256 * (r / pair_rows) + rows[r]];
+    }
 }
 
 int launch_leaf_wstar(const uint8_t *rows, const int32_t *leaf_nodes, const int32_t *leaf_rows,
-                      int32_t nleaves, const int32_t *sym_wstar, int32_t *node_wstar,
-                      cudaStream_t s) {
+                      int32_t nleaves, int32_t pair_rows, const int32_t *sym_wstar,
+                      int32_t *node_wstar, cudaStream_t s) {
     if (nleaves <= 0) return 0;
     leaf_wstar_kernel<<<(nleaves + 255) / 256, 256, 0, s>>>(rows, leaf_nodes, leaf_rows, nleaves,
-                                                            sym_wstar, node_wstar);
+                                                            pair_rows, sym_wstar, node_wstar);
     LCSG_LAUNCH_CHECK();
     return 0;
 }
@@ -118,9 +125,10 @@ __global__ void virtual_wstar_kernel(Ctx c, const int32_t *__restrict__ vnodes, 
     d.kmax = nullptr;
     d.wstar = nullptr;
     d.w1 = 3;
-    d.leaf_row = vnodes[3 * t + 1];
-    d.leaf2 = vnodes[3 * t + 2] + 1;
-    node_wstar[vnodes[3 * t]] = tab_kmax(resolve(d, c), 0, c.inf);
+    d.leaf_row = vnodes[4 * t + 1];
+    d.leaf2 = vnodes[4 * t + 2] + 1;
+    d.pair = vnodes[4 * t + 3];
+    node_wstar[vnodes[4 * t]] = tab_kmax(resolve(d, c), 0, c.inf);
 }
 
 int launch_virtual_wstar(Ctx c, const int32_t *vnodes, int32_t nvirt, int32_t *node_wstar,
@@ -136,7 +144,7 @@ __global__ void leaf_table_kernel(Ctx c, int32_t leaf_row, int32_t w1, int32_t *
                                   int32_t *kmax) {
     int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (r > c.n) return;
-    const int32_t *nx = c.nx + (size_t)c.rows[leaf_row] * (size_t)(c.n + 1);
+    const int32_t *nx = c.nx + (size_t)c.rows[leaf_row] * (size_t)(c.n + 1);  // single solves
     reach[r * w1] = (int32_t)r + 1;
     int32_t k = 0;
     if (w1 == 2) {
@@ -630,10 +638,24 @@ int launch_walk_level(const WalkNode *nodes, const int32_t *ids, int32_t count, 
 // (solver.py:160-162), read on the device so no host round trip is needed.
 // (i_start = 1 for lcs(); other start columns walk a band sub-tree for the
 // multi-GPU schedule; WalkNode.top_row is relative to the slab's first row.)
-__global__ void walk_root_kernel(const WalkNode *nodes, int32_t root, Ctx c, TabDev root_tab,
+__device__ __forceinline__ TabDev pair_root(TabDev t, int32_t p, const RootBatch &rb) {
+    if (t.reach) {
+        t.reach += p * rb.tab_stride;
+        t.kmax += p * rb.tab_stride;
+    } else {
+        t.leaf_row += p * rb.pair_rows;
+        t.pair = p;
+    }
+    return t;
+}
+
+__global__ void walk_root_kernel(const WalkNode *nodes, int32_t root0, Ctx c, TabDev root_tab,
                                  int32_t j, int32_t i_start, int32_t *wi, int32_t *wj,
-                                 int32_t *cols_out) {
-    const TabAcc R = resolve(root_tab, c);
+                                 int32_t *cols_out, RootBatch rb) {
+    const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;  // pair
+    if (p >= rb.npairs) return;
+    const int32_t root = root0 + p * rb.pair_nodes;
+    const TabAcc R = resolve(pair_root(root_tab, p, rb), c);
     const int32_t jj = j >= 0 ? j : tab_kmax(R, i_start - 1, c.inf);
     wi[root] = i_start;
     wj[root] = jj;
@@ -641,23 +663,28 @@ __global__ void walk_root_kernel(const WalkNode *nodes, int32_t root, Ctx c, Tab
 }
 
 int launch_walk_root(const WalkNode *nodes, int32_t root, Ctx c, TabDev root_tab, int32_t j,
-                     int32_t i_start, int32_t *wi, int32_t *wj, int32_t *cols_out,
+                     int32_t i_start, int32_t *wi, int32_t *wj, int32_t *cols_out, RootBatch rb,
                      cudaStream_t s) {
-    walk_root_kernel<<<1, 1, 0, s>>>(nodes, root, c, root_tab, j, i_start, wi, wj, cols_out);
+    walk_root_kernel<<<(rb.npairs + 127) / 128, 128, 0, s>>>(nodes, root, c, root_tab, j, i_start,
+                                                             wi, wj, cols_out, rb);
     LCSG_LAUNCH_CHECK();
     return 0;
 }
 
 // cols[m] = table.reach[i_start-1, j] (solver.py:206)
 __global__ void walk_final_kernel(Ctx c, TabDev root_tab, int32_t m, int32_t i_start,
-                                  const int32_t *wj_root, int32_t *cols_out) {
-    const TabAcc R = resolve(root_tab, c);
-    cols_out[m] = tab_get(R, i_start - 1, *wj_root);
+                                  int32_t root0, const int32_t *wj, int32_t *cols_out,
+                                  RootBatch rb) {
+    const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= rb.npairs) return;
+    const TabAcc R = resolve(pair_root(root_tab, p, rb), c);
+    cols_out[(int64_t)p * (m + 1) + m] = tab_get(R, i_start - 1, wj[root0 + p * rb.pair_nodes]);
 }
 
-int launch_walk_final(Ctx c, TabDev root_tab, int32_t i_start, int32_t m, const int32_t *wj_root,
-                      int32_t *cols_out, cudaStream_t s) {
-    walk_final_kernel<<<1, 1, 0, s>>>(c, root_tab, m, i_start, wj_root, cols_out);
+int launch_walk_final(Ctx c, TabDev root_tab, int32_t i_start, int32_t m, int32_t root,
+                      const int32_t *wj, int32_t *cols_out, RootBatch rb, cudaStream_t s) {
+    walk_final_kernel<<<(rb.npairs + 127) / 128, 128, 0, s>>>(c, root_tab, m, i_start, root, wj,
+                                                              cols_out, rb);
     LCSG_LAUNCH_CHECK();
     return 0;
 }
@@ -667,7 +694,17 @@ constexpr int ASM_THREADS = 1024;
 __global__ void __launch_bounds__(ASM_THREADS)
     assemble_kernel(const uint8_t *__restrict__ rows, int32_t m, const uint8_t *__restrict__ cols,
                     int32_t n, const int32_t *__restrict__ path, int32_t *out_len,
-                    int32_t *row_pos, int32_t *col_pos, uint8_t *subseq) {
+                    int32_t *row_pos, int32_t *col_pos, uint8_t *subseq, int64_t out_stride,
+                    int64_t sub_stride) {
+    // one CTA per pair of a batch
+    const int64_t p = blockIdx.x;
+    rows += p * m;
+    cols += p * n;
+    path += p * (m + 1);
+    out_len += p * out_stride;
+    row_pos += p * out_stride;
+    col_pos += p * out_stride;
+    subseq += p * sub_stride;
     using Scan = cub::BlockScan<int32_t, ASM_THREADS>;
     __shared__ typename Scan::TempStorage tmp;
     int32_t carry = 0;
@@ -698,8 +735,10 @@ __global__ void __launch_bounds__(ASM_THREADS)
 
 int launch_assemble(const uint8_t *rows, int32_t m, const uint8_t *cols, int32_t n,
                     const int32_t *path, int32_t *out_len, int32_t *row_pos, int32_t *col_pos,
-                    uint8_t *subseq, cudaStream_t s) {
-    assemble_kernel<<<1, ASM_THREADS, 0, s>>>(rows, m, cols, n, path, out_len, row_pos, col_pos, subseq);
+                    uint8_t *subseq, cudaStream_t s, int32_t npairs, int64_t out_stride,
+                    int64_t sub_stride) {
+    assemble_kernel<<<npairs, ASM_THREADS, 0, s>>>(rows, m, cols, n, path, out_len, row_pos,
+                                                   col_pos, subseq, out_stride, sub_stride);
     LCSG_LAUNCH_CHECK();
     return 0;
 }

@@ -10,6 +10,7 @@ pool); ``backend`` accepts only None / "auto" / "cuda".
 from __future__ import annotations
 
 import ctypes
+from concurrent.futures import ThreadPoolExecutor
 from typing import Optional
 
 import numpy as np
@@ -271,6 +272,61 @@ def lcs(
                      col_positions=tuple(pb[:L].tolist()))
 
 
+# cells (m * n * pairs) per batched launch: bounds the batch's HBM arena
+# (~125 B per cell-equivalent with traces at cfg5-like shapes)
+_BATCH_CELLS = 1 << 28
+
+
+def lcs_batch(
+    a_list,
+    b_list,
+    *,
+    threads: int = 1,
+    backend=None,
+    low_memory: bool = False,
+    device=None,
+    stream=None,
+) -> list:
+    """``[lcs(a, b) for a, b in zip(a_list, b_list)]`` for pairs of EQUAL
+    shape (every a the same length, every b the same length), solved as ONE
+    batch on the GPU: the recursion trees of all pairs are built together,
+    one launch per tree height for the whole batch (SURVEY.md 8(f) rank 4;
+    reference row-range contract _kernel.pyx:63-82), then one walk and one
+    assembly.  Results are identical to the per-pair calls."""
+    A = [as_bytes(x) for x in a_list]
+    Bs = [as_bytes(x) for x in b_list]
+    if len(A) != len(Bs):
+        raise ValueError("a_list and b_list differ in length")
+    if not A:
+        return []
+    la, lb = len(A[0]), len(Bs[0])
+    if any(len(x) != la for x in A) or any(len(x) != lb for x in Bs):
+        raise ValueError("lcs_batch needs pairs of equal shape")
+    if la == 0 or lb == 0:  # solver.py:255-256
+        return [LcsResult(0, b"", (), ()) for _ in A]
+    _backend.resolve(backend)
+    npairs = len(A)
+    k = min(la, lb)
+    aa = np.frombuffer(b"".join(A), dtype=np.uint8)
+    bb = np.frombuffer(b"".join(Bs), dtype=np.uint8)
+    lengths = np.empty(npairs, dtype=np.int32)
+    sub = np.empty(npairs * k, dtype=np.uint8)
+    pa = np.empty(npairs * k, dtype=np.int32)
+    pb = np.empty(npairs * k, dtype=np.int32)
+    flags = 0 if low_memory else _lib.LCSG_WITH_TRACE
+    rc = _lib.load().lcsg_lcs_batch(_ptr(aa), la, _ptr(bb), lb, npairs, flags, _device(device),
+                                    stream, _ptr(lengths), _ptr(sub), _ptr(pa), _ptr(pb))
+    _lib.check(rc, "lcs_batch")
+    out = []
+    for p in range(npairs):
+        L = int(lengths[p])
+        o = p * k
+        out.append(LcsResult(length=L, subsequence=sub[o:o + L].tobytes(),
+                             row_positions=tuple(pa[o:o + L].tolist()),
+                             col_positions=tuple(pb[o:o + L].tolist())))
+    return out
+
+
 def lcs_many(
     pairs,
     *,
@@ -279,20 +335,50 @@ def lcs_many(
     low_memory: bool = False,
     device=None,
     concurrency: int = 8,
+    batch: bool = True,
 ) -> list:
-    """``[lcs(a, b) for a, b in pairs]`` with independent solves overlapped
-    on the GPU (many small pairs, e.g. the planted
-    queries of cfg4).  Each solve runs on its own CUDA stream from one of
-    ``concurrency`` host worker threads (the C-ABI call releases the GIL), so
-    small latency-bound solves share the device instead of queueing behind
-    each other.  Results are identical to the sequential calls, in order."""
+    """``[lcs(a, b) for a, b in pairs]`` with the GPU shared across pairs
+    (many small pairs, e.g. the planted queries of
+    cfg4).  Pairs of equal shape are solved together by :func:`lcs_batch`
+    (one launch per tree height for the group, chunked to bound memory);
+    the remaining pairs run as independent solves on separate CUDA streams
+    from ``concurrency`` host worker threads (the C-ABI call releases the
+    GIL).  Results are identical to the sequential calls, in order."""
     _backend.resolve(backend)
-    items = list(pairs)
-    if concurrency <= 1 or len(items) <= 1:
-        return [lcs(a, b, threads=threads, low_memory=low_memory, device=device) for a, b in items]
-    from concurrent.futures import ThreadPoolExecutor
+    items = [(as_bytes(a), as_bytes(b)) for a, b in pairs]
+    out = [None] * len(items)
+    single = []
+    if batch:
+        groups = {}
+        for idx, (a, b) in enumerate(items):
+            groups.setdefault((len(a), len(b)), []).append(idx)
+        for (la, lb), idxs in groups.items():
+            if len(idxs) < 2 or la == 0 or lb == 0:
+                single.extend(idxs)
+                continue
+            per = max(1, _BATCH_CELLS // max(1, la * lb))
+            for c0 in range(0, len(idxs), per):
+                chunk = idxs[c0:c0 + per]
+                if len(chunk) == 1:
+                    single.extend(chunk)
+                    continue
+                res = lcs_batch([items[i][0] for i in chunk], [items[i][1] for i in chunk],
+                                low_memory=low_memory, device=device)
+                for i, r in zip(chunk, res):
+                    out[i] = r
+    else:
+        single = list(range(len(items)))
+    single.sort()
 
-    with ThreadPoolExecutor(max_workers=min(concurrency, len(items))) as ex:
-        futs = [ex.submit(lcs, a, b, threads=threads, low_memory=low_memory, device=device)
-                for a, b in items]
-        return [f.result() for f in futs]
+    def one(i):
+        a, b = items[i]
+        return lcs(a, b, threads=threads, low_memory=low_memory, device=device)
+
+    if concurrency <= 1 or len(single) <= 1:
+        for i in single:
+            out[i] = one(i)
+        return out
+    with ThreadPoolExecutor(max_workers=min(concurrency, len(single))) as ex:
+        for i, r in zip(single, ex.map(one, single)):
+            out[i] = r
+    return out

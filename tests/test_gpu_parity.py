@@ -486,3 +486,40 @@ def test_lcs_many_matches_sequential():
     for (a, b), r in zip(pairs[:10], got[:10]):
         assert (r.length, r.subsequence, r.row_positions, r.col_positions) == O.lcs(a, b)
     assert L.lcs_many(pairs[:5], concurrency=1, low_memory=True) == got[:5]
+
+
+@pytest.mark.parametrize("low", [False, True])
+def test_lcs_batch_equal_shapes(low):
+    """Batched solve (one launch per tree height for all pairs, SURVEY.md
+    8(f) rank 4) == the per-pair solves == the oracle, for equal-shape groups
+    incl. swapped orientation, m = 1 (leaf roots), n = 1, sparse alphabets and
+    identical / disjoint pairs."""
+    rng = np.random.default_rng(4040)
+    shapes = [(37, 120, 4), (120, 37, 26), (1, 50, 2), (50, 1, 2), (64, 64, 4), (300, 420, 20),
+              (2, 2, 2), (3, 9, 3)]
+    for la, lb, sigma in shapes:
+        pairs = [workloads.random_pair(rng, la, lb, sigma) for _ in range(5)]
+        if la == lb:
+            pairs.append((pairs[0][0], pairs[0][0]))
+        got = L.lcs_batch([a for a, _ in pairs], [b for _, b in pairs], low_memory=low)
+        for (a, b), r in zip(pairs, got):
+            assert r == L.lcs(a, b, low_memory=low), (la, lb)
+            assert (r.length, r.subsequence, r.row_positions, r.col_positions) == O.lcs(a, b)
+
+
+def test_lcs_batch_cfg4_windows(config_digests):
+    """cfg4's query against a window around each of its 8 planted copies, as
+    one batched solve: bit-exact against the sequential solves and the oracle."""
+    pairs = workloads.cfg4_planted_windows(0, width=4096)
+    got = L.lcs_batch([a for a, _ in pairs], [b for _, b in pairs])
+    for (a, b), r in zip(pairs, got):
+        assert r == L.lcs(a, b)
+        assert (r.length, r.subsequence, r.row_positions, r.col_positions) == O.lcs(a, b, threads=8)
+    assert L.lcs_many(pairs + [(b"ab", b"b")]) == got + [L.lcs(b"ab", b"b")]
+
+
+def test_lcs_batch_errors():
+    with pytest.raises(ValueError, match="equal shape"):
+        L.lcs_batch([b"ab", b"abc"], [b"x", b"y"])
+    assert L.lcs_batch([], []) == []
+    assert L.lcs_batch([b"", b""], [b"a", b"b"]) == [L.LcsResult(0, b"", (), ())] * 2

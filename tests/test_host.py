@@ -20,7 +20,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def header_symbols():
     text = open(os.path.join(ROOT, "include", "lcsgrid_b200.h")).read()
-    return sorted(set(re.findall(r"\b(lcsg_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(lcsg_[a-z0-9_]+)\s*\(", text)))
 
 
 def test_library_exports_every_header_symbol():

@@ -62,6 +62,23 @@ def generate(cfg: int, seed: int = 0):
     raise ValueError(f"unknown config {cfg}")
 
 
+def cfg4_planted_windows(seed: int = 0, width: int = 8192):
+    """Batched-solve workload: cfg4's query against a
+    text window of ``width`` columns around each of its 8 planted copies --
+    8 equal-shape pairs (1024 x width).  The planted offsets are re-drawn
+    exactly as generate(4, seed) draws them."""
+    a, b = generate(4, seed)
+    rng = np.random.default_rng(seed)
+    rng.integers(0, 4, 1024)
+    rng.integers(0, 4, 65536)
+    offs = sorted(int(x) for x in rng.choice(65536 - 1024, 8, replace=False))
+    pairs = []
+    for o in offs:
+        lo = min(max(0, o + 512 - width // 2), len(b) - width)
+        pairs.append((a, b[lo:lo + width]))
+    return pairs
+
+
 def random_pair(rng, m: int, n: int, sigma: int, base: int = 97):
     """Small i.i.d. uniform test pair (used by the parity sweeps)."""
     a = (rng.integers(0, sigma, m) + base).astype(np.uint8).tobytes()
