@@ -462,6 +462,7 @@ def run_sharded(args, rank, world, dist):
     r = None
     for _ in range(args.warmup):
         r = D.lcs_sharded(a, b, device=local)
+    stats = D.CommStats()
     times = []
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
@@ -471,7 +472,7 @@ def run_sharded(args, rank, world, dist):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            r = D.lcs_sharded(a, b, device=local)
+            r = D.lcs_sharded(a, b, device=local, stats=stats)
             e1.record(stream)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
@@ -479,6 +480,11 @@ def run_sharded(args, rank, world, dist):
     tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     t_ms = float(tt.item())
+    # bytes each rank received through the schedule's collectives, per solve
+    rb = torch.tensor([stats.received / max(1, args.steps)], dtype=torch.float64, device=dev)
+    rb_all = [torch.zeros_like(rb) for _ in range(world)]
+    dist.all_gather(rb_all, rb)
+    received = [float(x.item()) for x in rb_all]
     _, bands, upper = D.build_plan(m, world)
     # kernels per solve on the busiest rank: its band build (~levels x 4) +
     # every upper combine (skeleton, 2 refinement stages, finalize)
@@ -496,6 +502,10 @@ def run_sharded(args, rank, world, dist):
                    "parallelism": f"{len(bands)} band subtrees + {len(upper)} upper combines "
                                   f"sharded over start columns across {world} GPUs (NCCL)"},
         "roofline": None,
+        "comm": {"received_bytes_per_rank_per_solve": received,
+                 "collectives": "2 all-gathers per upper combine (spans + kmax + wstar, then "
+                                "finite-prefix reach rows) within each subtree's group; one "
+                                "max all-reduce of the path"},
         "e2e": {"value": m * n / (t_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": m + n,
                 "d2h_bytes_per_step": 4 * (m + 1)},
         "gpu_launches": launches,

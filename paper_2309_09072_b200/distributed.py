@@ -179,11 +179,15 @@ class CudaBackend:
         self.handles = []
 
 
+def _is_gloo(dist, group):
+    return dist.get_backend(group) == "gloo"
+
+
 def _bcast(dist, group, t, src):
     """Broadcast a (possibly CUDA) tensor; gloo is staged through host memory."""
     if t.numel() == 0:
         return
-    if t.is_cuda and dist.get_backend(group) == "gloo":
+    if t.is_cuda and _is_gloo(dist, group):
         tmp = t.cpu()
         dist.broadcast(tmp, src=src, group=group)
         t.copy_(tmp)
@@ -191,34 +195,20 @@ def _bcast(dist, group, t, src):
         dist.broadcast(t, src=src, group=group)
 
 
-def _bcast_finite_rows(dist, group, table, kmax_rows, src, inf):
-    """Broadcast rows of a reach table by their finite prefixes only.
-
-    Row i holds finite values in columns 0..kmax[i] and INF beyond, so only
-    those prefixes travel (about a third of a sigma=26 top-level table,
-    SURVEY.md 8(e)); every rank already has ``kmax_rows``, so payload sizes
-    need no exchange.  Receivers rebuild the rows with INF fill."""
-    import torch
-
-    if table.numel() == 0:
-        return
-    cols = torch.arange(table.shape[1], device=table.device, dtype=kmax_rows.dtype)
-    mask = cols[None, :] <= kmax_rows[:, None]
-    me = dist.get_rank()  # global rank: src is a global rank (subgroups too)
-    if me == src:
-        payload = table[mask]
+def _all_gather(dist, group, out, inp):
+    """all_gather_into_tensor (equal shards; gloo staged through host memory)."""
+    if inp.is_cuda and _is_gloo(dist, group):
+        tmp = out.cpu()
+        dist.all_gather_into_tensor(tmp, inp.cpu(), group=group)
+        out.copy_(tmp)
     else:
-        payload = torch.empty(int(mask.sum().item()), dtype=table.dtype, device=table.device)
-    _bcast(dist, group, payload, src)
-    if me != src:
-        table.fill_(inf)
-        table[mask] = payload
+        dist.all_gather_into_tensor(out, inp, group=group)
 
 
-def _allreduce_max(dist, group, t):
+def _all_reduce_max(dist, group, t):
     from torch.distributed import ReduceOp
 
-    if t.is_cuda and dist.get_backend(group) == "gloo":
+    if t.is_cuda and _is_gloo(dist, group):
         tmp = t.cpu()
         dist.all_reduce(tmp, op=ReduceOp.MAX, group=group)
         t.copy_(tmp)
@@ -231,12 +221,13 @@ _SUBGROUPS: Dict[Tuple[int, Tuple[int, ...]], object] = {}
 
 def _subgroup(dist, parent, ranks: Tuple[int, ...]):
     """Process group of a subtree's (global) ranks, created once per parent
-    group and rank set: every rank asks for the same sets in the same order,
-    so creation stays collective while repeated solves reuse communicators."""
+    group and rank set and reused by later solves.  Only the members call
+    ``new_group`` (local synchronisation), so a ``group=`` that is a proper
+    subgroup of the world does not hang the ranks outside it."""
     key = (id(parent), ranks)
     g = _SUBGROUPS.get(key)
     if g is None:
-        g = dist.new_group(list(ranks))
+        g = dist.new_group(list(ranks), use_local_synchronization=True)
         _SUBGROUPS[key] = g
     return g
 
@@ -258,74 +249,170 @@ def _rank_sets(root: Node, P: int) -> Dict[int, Tuple[int, ...]]:
     return rs
 
 
-def _replicate(dist, G, rank, ch: Node, ch_ranks, backend, n, inf):
-    """Make child table ``ch`` (reach, kmax, wstar) complete on every rank of
-    the parent's group ``G``: a band from its owner, an upper node from the
-    owners of its row ranges (spans first, so that every member knows them);
-    rows travel as finite prefixes."""
+def _finite_index(kmax_rows, lo: int, total: int):
+    """(row, column) of every finite cell of rows lo.. of a reach table --
+    row i holds finite values in columns 0..kmax[i] (solver.py:84,104) -- in
+    row-major order: the device-side pack / unpack index of a finite-prefix
+    transfer (a prefix sum of the row lengths; ``total`` is known on the host,
+    so nothing waits on the device)."""
+    import torch
+
+    counts = kmax_rows.long() + 1
+    dev = kmax_rows.device
+    rows = torch.repeat_interleave(torch.arange(lo, lo + len(counts), device=dev), counts,
+                                   output_size=total)
+    starts = torch.cumsum(counts, 0) - counts
+    cols = torch.arange(total, device=dev) - starts[rows - lo]
+    return rows, cols
+
+
+class CommStats:
+    """Bytes this rank received through the schedule's collectives."""
+
+    def __init__(self):
+        self.received = 0
+        self.collectives = 0
+
+    def add(self, gathered_bytes: int, own_bytes: int):
+        self.received += gathered_bytes - own_bytes
+        self.collectives += 1
+
+
+def _replicate_children(dist, G, grank, members, nd: Node, rs, glob, backend, n, inf, stats):
+    """Make both children tables of upper node ``nd`` (reach, kmax, wstar)
+    complete on every member of its group ``G``, with two collectives and
+    one host synchronisation:
+
+    1. one all-gather of a fixed-size record per member -- for each child the
+       row span it computed (a band owner: all rows), its partial wstar and
+       its kmax rows -- from which every member knows both children's spans,
+       full kmax rows and wstar (one device-to-host copy);
+    2. one all-gather of the reach rows as finite prefixes (kmax[i] + 1
+       entries; receivers refill the INF tail -- about a third of a sigma=26
+       top-level table), padded to the largest member's
+       payload, packed and unpacked on the device (``_finite_index``)."""
     import torch
 
     n1 = n + 1
-    w1 = min(ch.rows, n) + 1
-    if ch.band >= 0:
-        spans = [(ch_ranks[0], 0, n1)]  # a band's rank set is its owner
-    else:
-        meta = backend.empty((3 * len(ch_ranks),))
-        if ch.table is not None and "spans" in ch.table:
-            meta.copy_(torch.tensor([v for sp in ch.table["spans"] for v in sp], dtype=meta.dtype))
-        _bcast(dist, G, meta, ch_ranks[0])
-        mh = meta.cpu().tolist()
-        spans = [tuple(int(v) for v in mh[3 * t: 3 * t + 3]) for t in range(len(ch_ranks))]
-    if ch.table is None:
-        ch.table = {"handle": None}
-    T = ch.table
-    if "reach" not in T or T["reach"] is None:
-        T["reach"] = backend.empty((n1, w1))
-        T["kmax"] = backend.empty((n1,))
-    # every member takes part (each child is replicated once, for its parent);
-    # the owners of row ranges send, the others receive
-    for owner, lo, hi in spans:
-        _bcast(dist, G, T["kmax"][lo:hi], owner)
-        _bcast_finite_rows(dist, G, T["reach"][lo:hi], T["kmax"][lo:hi], owner, inf)
-    ws = torch.tensor([int(T.get("wstar", 0))], dtype=torch.int32, device=T["reach"].device)
-    _bcast(dist, G, ws, spans[0][0])
-    T["wstar"] = int(ws.item())
-    T["reach_full"] = True
-    T["spans"] = spans
+    kids = (nd.upper, nd.lower)
+    M = len(members)
+    rec = 4 + n1  # per child: lo, hi, wstar part, has-rows, then kmax (n1)
+    mine = backend.empty((2 * rec,))
+    mine.zero_()
+    for c, ch in enumerate(kids):
+        T = ch.table
+        if T is not None and "my_span" in T:
+            lo, hi = T["my_span"]
+            head = torch.tensor([lo, hi, 0, 1], dtype=mine.dtype)
+            mine[c * rec: c * rec + 4].copy_(head)
+            mine[c * rec + 2: c * rec + 3].copy_(T["wstar_part"].reshape(1))
+            mine[c * rec + 4 + lo: c * rec + 4 + hi].copy_(T["kmax"][lo:hi])
+    gathered = backend.empty((M * 2 * rec,))
+    _all_gather(dist, G, gathered, mine)
+    stats.add(gathered.numel() * 4, mine.numel() * 4)
+    gd = gathered.view(M, 2, rec)
+    gh = gd.cpu().numpy()  # the schedule's one host synchronisation per combine
+    for c, ch in enumerate(kids):
+        w1 = min(ch.rows, n) + 1
+        if ch.table is None:
+            ch.table = {"handle": None}
+        T = ch.table
+        spans, kmax_dev, wstar = [], backend.empty((n1,)), 0
+        for t in range(M):
+            lo, hi, ws, has = (int(v) for v in gh[t, c, :4])
+            if not has:
+                continue
+            spans.append((members[t], lo, hi))
+            kmax_dev[lo:hi].copy_(gd[t, c, 4 + lo: 4 + hi])
+            wstar = max(wstar, ws)
+        spans.sort(key=lambda sp: sp[1])
+        kmax_h = np.zeros(n1, dtype=np.int64)
+        for r, lo, hi in spans:
+            kmax_h[lo:hi] = gh[members.index(r), c, 4 + lo: 4 + hi]
+        if "reach" not in T or T["reach"] is None:
+            T["reach"] = backend.empty((n1, w1))
+        T["kmax"] = kmax_dev
+        T["kmax_host"] = kmax_h
+        T["wstar"] = wstar
+        T["spans"] = spans
+    # 2. finite prefixes of the reach rows, packed per member
+    sizes = np.zeros((M, 2), dtype=np.int64)
+    for c, ch in enumerate(kids):
+        kh = ch.table["kmax_host"]
+        for r, lo, hi in ch.table["spans"]:
+            sizes[members.index(r), c] = int(kh[lo:hi].sum()) + (hi - lo)
+    pad = int(sizes.sum(1).max()) if M else 0
+    me = members.index(grank)
+    payload = backend.empty((max(pad, 1),))
+    off = 0
+    for c, ch in enumerate(kids):
+        T = ch.table
+        if "my_span" in T:
+            lo, hi = T["my_span"]
+            tot = int(sizes[me, c])
+            if tot:
+                rows, cols = _finite_index(T["kmax"][lo:hi], lo, tot)
+                payload[off: off + tot].copy_(T["reach"][rows, cols])
+            off += tot
+    allp = backend.empty((M * max(pad, 1),))
+    _all_gather(dist, G, allp, payload)
+    stats.add(allp.numel() * 4, payload.numel() * 4)
+    allp = allp.view(M, max(pad, 1))
+    for c, ch in enumerate(kids):
+        T = ch.table
+        pieces = []
+        for r, lo, hi in T["spans"]:
+            t = members.index(r)
+            o = int(sizes[t, :c].sum())
+            pieces.append(allp[t, o: o + int(sizes[t, c])])
+        flat = torch.cat(pieces) if pieces else allp.new_empty((0,))
+        total = int(flat.numel())
+        reach = T["reach"]
+        reach.fill_(inf)
+        if total:
+            rows, cols = _finite_index(T["kmax"], 0, total)
+            reach[rows, cols] = flat
+        T["reach_full"] = True
 
 
-def solve_sharded(rows: bytes, cols: bytes, dist, group=None, backend=None, with_trace=True):
+def solve_sharded(rows: bytes, cols: bytes, dist, group=None, backend=None, with_trace=True,
+                  stats: Optional[CommStats] = None):
     """Sharded build of the full-grid tree: returns (root, bands, upper, ctx).
 
     Bands are built by their owners with no communication.  Each upper
     combine is computed by the ranks of its own subtree (pairs, quads, ...,
     all ranks at the root), sharded over start columns; before it, the two
     children tables are replicated within that subtree's process group only
-    (finite row prefixes), so a rank receives its sibling subtrees' tables,
-    not every table of the level.  Traces and the root's rows stay with
-    their row owners (``table["spans"]`` = (rank, lo, hi))."""
+    (``_replicate_children``: two all-gathers, one host synchronisation), so
+    a rank receives its sibling subtrees' tables, not every table of the
+    level.  Traces and the root's rows stay with their row owners
+    (``table["spans"]`` = (global rank, lo, hi)).  Nothing else waits on the
+    device: the row split of a combine is a pure function of the gathered
+    kmax rows, and partial wstar values travel in the next gather."""
     import torch
 
+    stats = stats if stats is not None else CommStats()
     rank, P = dist.get_rank(group), dist.get_world_size(group)
     m, n = len(rows), len(cols)
     n1, inf = n + 1, n + 2
     root, bands, upper = build_plan(m, P)
     rs = _rank_sets(root, P)
     glob = (lambda r: r) if group is None else (lambda r: dist.get_global_rank(group, r))
+    grank = glob(rank)
     groups: Dict[Tuple[int, ...], object] = {}
-    for nd in upper:  # collective: same order on every rank
+    for nd in upper:  # members create their subtree's group (same order everywhere)
         key = rs[id(nd)]
-        if key not in groups:
+        if key not in groups and rank in key:
             groups[key] = group if len(key) == P else _subgroup(dist, group, tuple(glob(r) for r in key))
     # 1. bands: independent subtrees, zero communication
     for b in bands:
         if b.band % P == rank:
             h, reach, kmax, ws = backend.build_band(rows, cols, b.top, b.bottom, with_trace)
             b.table = {"handle": h, "reach": reach, "kmax": kmax, "wstar": ws,
-                       "reach_full": True, "handle_owner": rank}
+                       "wstar_part": torch.tensor([ws], dtype=torch.int32, device=reach.device),
+                       "my_span": (0, n1), "reach_full": True, "handle_owner": rank}
         else:
             b.table = None
-    backend.synchronize()
     # 2. upper combines, bottom-up, each within its subtree's group
     for nd in upper:
         key = rs[id(nd)]
@@ -333,23 +420,21 @@ def solve_sharded(rows: bytes, cols: bytes, dist, group=None, backend=None, with
             nd.table = None
             continue
         G = groups[key]
-        for ch in (nd.upper, nd.lower):
-            _replicate(dist, G, rank, ch, [glob(r) for r in rs[id(ch)]], backend, n, inf)
+        members = [glob(r) for r in key]
+        _replicate_children(dist, G, grank, members, nd, rs, glob, backend, n, inf, stats)
         U, L = nd.upper.table, nd.lower.table
         w1 = min(nd.rows, n) + 1
         out = {"reach": backend.empty((n1, w1)), "trace": backend.empty((n1, w1)),
                "kmax": backend.empty((n1,)), "wstar_dev": backend.empty((1,))}
         out["wstar_dev"].zero_()
-        weights = U["kmax"].cpu().numpy().astype(np.int64) + 1
-        spans = split_rows(weights, len(key))
+        spans = split_rows(U["kmax_host"] + 1, len(key))  # identical on every member
         lo, hi = spans[key.index(rank)]
         backend.combine_rows(U, L, out, lo, hi, inf)
-        backend.synchronize()
-        _allreduce_max(dist, G, out["wstar_dev"])
-        out["wstar"] = int(out["wstar_dev"].item())
-        out["spans"] = [(glob(key[t]), a, b) for t, (a, b) in enumerate(spans)]
+        out["wstar_part"] = out["wstar_dev"]
+        out["my_span"] = (lo, hi)
+        out["spans"] = [(members[t], a, b) for t, (a, b) in enumerate(spans)]
         nd.table = out
-    ctx = {"rs": rs, "groups": groups, "glob": glob, "group": group}
+    ctx = {"rs": rs, "groups": groups, "glob": glob, "group": group, "stats": stats}
     return root, bands, upper, ctx
 
 
@@ -359,7 +444,8 @@ def recover_sharded(root: Node, bands: List[Node], m: int, dist, group=None, bac
     the upper-level walk and the band walks.  Each rank walks only the path
     towards its own band: at a node, the owner of the trace row broadcasts
     (k, x) within the node's group; then every member follows the child
-    whose subtree holds it."""
+    whose subtree holds it.  The band pieces and the path's end column are
+    merged with one max all-reduce of an (m+1) int32 vector (columns >= 1)."""
     import torch
 
     rank, P = dist.get_rank(group), dist.get_world_size(group)
@@ -389,11 +475,11 @@ def recover_sharded(root: Node, bands: List[Node], m: int, dist, group=None, bac
         dev = nd.table["reach"].device
         kx = torch.zeros(2, dtype=torch.int32, device=dev)
         if grank == owner:
-            k = int(nd.table["trace"][i - 1, jj].item())
+            k = nd.table["trace"][i - 1, jj]
             kx[0] = k
-            kx[1] = int(nd.upper.table["reach"][i - 1, k].item())
+            kx[1] = nd.upper.table["reach"][i - 1, k]
         _bcast(dist, G, kx, owner)
-        k, x = int(kx[0].item()), int(kx[1].item())
+        k, x = (int(v) for v in kx.cpu().tolist())
         if rank in rs[id(nd.upper)]:
             walk(nd.upper, i, k)
         if rank in rs[id(nd.lower)]:
@@ -401,29 +487,23 @@ def recover_sharded(root: Node, bands: List[Node], m: int, dist, group=None, bac
 
     if rank in rs[id(root)]:
         walk(root, 1, length)
-    cols = np.zeros(m + 1, dtype=np.int32)
-    pieces = []
+    path = backend.empty((m + 1,))
+    path.zero_()
     for b in bands:
         if b.band % P == rank:
             i, jj = start[b.band]
-            pieces.append((b.top, backend.recover_band(b.table["handle"], i, jj, b.rows)))
-    gathered = [None] * P
-    dist.all_gather_object(gathered, pieces, group=group)
-    for plist in gathered:
-        for top, seg in plist:
-            cols[top - 1: top - 1 + len(seg)] = seg
+            seg = backend.recover_band(b.table["handle"], i, jj, b.rows)
+            path[b.top - 1: b.top - 1 + len(seg)].copy_(torch.from_numpy(seg))
     # the path's end column: root cell (start column 1, weight length), held by
     # the owner of row 0 (root rows are not replicated)
-    end_owner = r0
-    end = backend.empty((1,))
     if R is not None and grank == r0:
-        end.copy_(R["reach"][0, length].reshape(1))
-    _bcast(dist, group, end, end_owner)
-    cols[m] = int(end.item())
-    return length, cols
+        path[m: m + 1].copy_(R["reach"][0, length].reshape(1))
+    _all_reduce_max(dist, group, path)
+    return length, path.cpu().numpy().astype(np.int32)
 
 
-def lcs_sharded(a, b, *, group=None, device=None, low_memory=False, backend=None) -> LcsResult:
+def lcs_sharded(a, b, *, group=None, device=None, low_memory=False, backend=None,
+                stats: Optional[CommStats] = None) -> LcsResult:
     """``lcs(a, b)`` (solver.py:237-273) across the ranks of ``group``; every
     rank returns the same LcsResult, bit-identical to the single-GPU solve."""
     import torch.distributed as dist
@@ -438,7 +518,7 @@ def lcs_sharded(a, b, *, group=None, device=None, low_memory=False, backend=None
         backend = CudaBackend(0 if device is None else int(device))
     try:
         root, bands, upper, ctx = solve_sharded(rows, cols, dist, group, backend,
-                                                with_trace=not low_memory)
+                                                with_trace=not low_memory, stats=stats)
         length, path = recover_sharded(root, bands, len(rows), dist, group, backend, ctx)
     finally:
         if own:
