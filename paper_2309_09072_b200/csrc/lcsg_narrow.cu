@@ -64,6 +64,53 @@ __device__ __forceinline__ void cp_async_wait_all() {
     asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
+// ---- TMA bulk copies (cp.async.bulk, sm_90+): the 16-byte-aligned body of a
+// contiguous block of table rows moves global -> shared as ONE asynchronous
+// bulk transfer issued by a single thread, completing on an mbarrier (the
+// Blackwell-native replacement of per-thread cp.async; no register staging,
+// no per-thread address arithmetic).  LCSG_TMA_STAGE=0 builds the cp.async path.
+#ifndef LCSG_TMA_STAGE
+#define LCSG_TMA_STAGE 1
+#endif
+struct StageBar {
+    uint64_t *bar;    // mbarrier in shared memory (initialised by stage_bar_init)
+    uint32_t phase;   // parity of the next completion (identical in every thread)
+};
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void stage_bar_init(uint64_t *bar) {
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    // order earlier generic-proxy accesses of this shared memory (made visible
+    // to this thread by the preceding barrier) before the async-proxy writes
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void stage_bar_wait(StageBar &sb) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(sb.bar)), "r"(sb.phase)
+            : "memory");
+    } while (!done);
+    sb.phase ^= 1u;
+}
+
 // Traces of the INF cells (kfin, w] of one output row whose finite prefix
 // [0, kfin] (reach and trace) is already in `tr`: Alg. 1 (_kernel.pyx:28-60)
 // visits the INF cells as nodes whose mid is INF; such a node fills
@@ -91,7 +138,7 @@ __device__ __forceinline__ void inf_traces(int32_t *tr, int32_t kfin, int32_t co
 // the table, copied flat when w1 == PT (every power-of-two tree level).
 template <int PT, int NT>
 __device__ __forceinline__ void stage_rows(int32_t *dst, const TabAcc &t, int64_t row0,
-                                           int32_t nrows, int32_t inf) {
+                                           int32_t nrows, int32_t inf, StageBar &sb) {
     const int tid = threadIdx.x;
     if (t.nx2) {  // virtual height-1 node: closed form of its two leaves
         for (int r = tid; r < nrows; r += NT) {
@@ -128,9 +175,18 @@ __device__ __forceinline__ void stage_rows(int32_t *dst, const TabAcc &t, int64_
             const int h = min(tot, (int)(((16 - ((uintptr_t)src & 15)) & 15) >> 2));
             const int nb = (tot - h) >> 2;
             if (tid < h) cp_async4(dst + tid, src + tid);
+#if LCSG_TMA_STAGE
+            if (nb > 0 && tid == 0) bulk_g2s(dst + h, src + h, (uint32_t)nb * 16u, sb.bar);
+#else
             for (int c2 = tid; c2 < nb; c2 += NT) cp_async16(dst + h + 4 * c2, src + h + 4 * c2);
+#endif
             const int t0 = h + 4 * nb;
             if (t0 + tid < tot) cp_async4(dst + t0 + tid, src + t0 + tid);
+            cp_async_wait_all();
+#if LCSG_TMA_STAGE
+            if (nb > 0) stage_bar_wait(sb);  // CTA-uniform
+#endif
+            return;
         } else {
             for (int g = tid; g < tot; g += NT) cp_async4(dst + g, src + g);
         }
@@ -163,8 +219,8 @@ __device__ __forceinline__ void copy_out(int32_t *g, const int32_t *sm, int tot)
 // unrolled: one shared body instead of one inlined copy per chunk
 template <int PT, int NT>
 __device__ __noinline__ void stage_rows_call(int32_t *dst, const TabAcc &t, int64_t row0,
-                                             int32_t nrows, int32_t inf) {
-    stage_rows<PT, NT>(dst, t, row0, nrows, inf);
+                                             int32_t nrows, int32_t inf, StageBar &sb) {
+    stage_rows<PT, NT>(dst, t, row0, nrows, inf, sb);
 }
 
 // P: bucket >= every U and L weight (w1 - 1) of the launch
@@ -181,6 +237,7 @@ __global__ void __launch_bounds__(NarrowGeom<P>::NT)
     int32_t *sU = nsm;               // ROWS x PT
     int32_t *sL = nsm + ROWS * PT;   // lcap x PT
     __shared__ int32_t s_xmax[NCH], s_wstar;
+    __shared__ uint64_t s_bar;
     const int32_t di = blockIdx.x / bpd;
     const int64_t i0 = (int64_t)(blockIdx.x - di * bpd) * ROWS;
     const CombineDesc &d = descs[di];
@@ -192,8 +249,11 @@ __global__ void __launch_bounds__(NarrowGeom<P>::NT)
     const uint32_t mul = 1u << (shift & 31);
     if (tid < NCH) s_xmax[tid] = 0;
     if (tid == 0) s_wstar = -1;
+    stage_bar_init(&s_bar);
+    __syncthreads();
+    StageBar sb{&s_bar, 0u};
     // 1. U rows of the block (columns beyond w_U are INF: no candidate)
-    stage_rows<PT, NT>(sU, U, i0, nr, inf);
+    stage_rows<PT, NT>(sU, U, i0, nr, inf, sb);
     __syncthreads();
     // kmax_U of each row (finite prefix of the U row) and, per chunk of split
     // weights, the largest finite x of the block
@@ -249,9 +309,9 @@ __global__ void __launch_bounds__(NarrowGeom<P>::NT)
             const int sh = L.nx ? 0 : (int)(((uintptr_t)(L.reach + (base + w0) * PT) >> 2) & 3);
             int32_t *sLw = sL + sh;
             if (NCH > 1)
-                stage_rows_call<PT, NT>(sLw, L, base + w0, nL, inf);
+                stage_rows_call<PT, NT>(sLw, L, base + w0, nL, inf, sb);
             else
-                stage_rows<PT, NT>(sLw, L, base + w0, nL, inf);
+                stage_rows<PT, NT>(sLw, L, base + w0, nL, inf, sb);
             __syncthreads();
 #pragma unroll
             for (int q = 0; q < RPT; ++q) {
@@ -347,6 +407,7 @@ __global__ void __launch_bounds__(R32_NT)
     int32_t *sU = nsm;
     int32_t *sL = nsm + ROWS * PT;
     __shared__ int32_t s_xmax[NCH], s_wstar;
+    __shared__ uint64_t s_bar;
     const int32_t di = blockIdx.x / bpd;
     const int64_t i0 = (int64_t)(blockIdx.x - di * bpd) * ROWS;
     const CombineDesc &d = descs[di];
@@ -359,7 +420,10 @@ __global__ void __launch_bounds__(R32_NT)
     const uint32_t mul = 1u << (shift & 31);
     if (tid < NCH) s_xmax[tid] = 0;
     if (tid == 0) s_wstar = -1;
-    stage_rows<PT, NT>(sU, U, i0, nr, inf);
+    stage_bar_init(&s_bar);
+    __syncthreads();
+    StageBar sb{&s_bar, 0u};
+    stage_rows<PT, NT>(sU, U, i0, nr, inf, sb);
     __syncthreads();
     int32_t ku = -1;
     int32_t xlast[NCH];
@@ -396,7 +460,7 @@ __global__ void __launch_bounds__(R32_NT)
             if (w0 > 0) __syncthreads();
             const int sh = L.nx ? 0 : (int)(((uintptr_t)(L.reach + (base + w0) * PT) >> 2) & 3);
             int32_t *sLw = sL + sh;
-            stage_rows_call<PT, NT>(sLw, L, base + w0, nL, inf);
+            stage_rows_call<PT, NT>(sLw, L, base + w0, nL, inf, sb);
             __syncthreads();
             if (r < nr) {
 #pragma unroll
