@@ -215,6 +215,47 @@ __device__ __forceinline__ void copy_out(int32_t *g, const int32_t *sm, int tot)
     }
 }
 
+// shared -> global of the block's output rows with TMA bulk stores
+// (cp.async.bulk.global.shared::cta): one thread moves the 16-byte body of
+// both tables, the other threads write the < 4-int tails.  The caller has
+// synchronised the block after filling `sr` / `st`; the issuing thread waits
+// for the bulk reads of shared memory before it exits (bulk_store_drain).
+template <int NT>
+__device__ __forceinline__ void copy_out_rows(int32_t *gr, int32_t *gt, const int32_t *sr,
+                                              const int32_t *st, int tot) {
+#if LCSG_TMA_STAGE
+    const bool al = (((uintptr_t)gr | (gt ? (uintptr_t)gt : 0)) & 15) == 0 &&
+                    (((uintptr_t)sr | (uintptr_t)st) & 15) == 0;
+    if (al) {
+        const int body = tot & ~3;
+        if (threadIdx.x == 0 && body > 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gr),
+                         "r"(smem_u32(sr)), "r"((uint32_t)body * 4u)
+                         : "memory");
+            if (gt)
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gt),
+                             "r"(smem_u32(st)), "r"((uint32_t)body * 4u)
+                             : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        const int idx = body + (int)threadIdx.x;
+        if (idx < tot) {
+            gr[idx] = sr[idx];
+            if (gt) gt[idx] = st[idx];
+        }
+        return;
+    }
+#endif
+    copy_out<NT>(gr, sr, tot);
+    if (gt) copy_out<NT>(gt, st, tot);
+}
+__device__ __forceinline__ void bulk_store_drain() {
+#if LCSG_TMA_STAGE
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+#endif
+}
+
 // out-of-line copy for the chunked (widest) bucket, whose k-chunk loop is
 // unrolled: one shared body instead of one inlined copy per chunk
 template <int PT, int NT>
@@ -378,9 +419,9 @@ __global__ void __launch_bounds__(NarrowGeom<P>::NT)
     __syncthreads();
     // 4. the block's rows are one contiguous range of the output
     const int tot = nr * w1;
-    copy_out<NT>(out_reach + i0 * w1, sR, tot);
-    if (out_trace) copy_out<NT>(out_trace + i0 * w1, sT, tot);
+    copy_out_rows<NT>(out_reach + i0 * w1, out_trace ? out_trace + i0 * w1 : nullptr, sR, sT, tot);
     if (tid == 0 && s_wstar >= 0) atomicMax(out_wstar, s_wstar);
+    bulk_store_drain();
 }
 
 // narrow<32> with a ROLLED k-chunk loop (32-bit keys only).  The unrolled
@@ -542,9 +583,9 @@ __global__ void __launch_bounds__(R32_NT)
     if ((tid & 31) == 0 && wmax >= 0) atomicMax(&s_wstar, wmax);
     __syncthreads();
     const int tot = nr * w1;
-    copy_out<NT>(out_reach + i0 * w1, sR, tot);
-    if (out_trace) copy_out<NT>(out_trace + i0 * w1, sT, tot);
+    copy_out_rows<NT>(out_reach + i0 * w1, out_trace ? out_trace + i0 * w1 : nullptr, sR, sT, tot);
     if (tid == 0 && s_wstar >= 0) atomicMax(out_wstar, s_wstar);
+    bulk_store_drain();
 }
 
 template <bool FW>
@@ -575,7 +616,8 @@ constexpr int LP_NT = 256, LP_RPT = 4, LP_ROWS = LP_NT * LP_RPT;
 template <typename Key, bool W3>
 __global__ void __launch_bounds__(LP_NT)
     narrow_leafpair_kernel(const CombineDesc *__restrict__ descs, Ctx c, int shift, int32_t bpd) {
-    __shared__ int32_t sR[LP_ROWS * 3], sT[LP_ROWS * 3];
+    __shared__ __align__(16) int32_t sR[LP_ROWS * 3];
+    __shared__ __align__(16) int32_t sT[LP_ROWS * 3];
     __shared__ int32_t s_wstar;
     const int32_t di = blockIdx.x / bpd;
     const int64_t i0 = (int64_t)(blockIdx.x - di * bpd) * LP_ROWS;
@@ -642,9 +684,10 @@ __global__ void __launch_bounds__(LP_NT)
     if ((tid & 31) == 0 && wmax >= 0) atomicMax(&s_wstar, wmax);
     __syncthreads();
     const int tot = nr * w1;
-    copy_out<LP_NT>(out_reach + i0 * w1, sR, tot);
-    if (out_trace) copy_out<LP_NT>(out_trace + i0 * w1, sT, tot);
+    copy_out_rows<LP_NT>(out_reach + i0 * w1, out_trace ? out_trace + i0 * w1 : nullptr, sR, sT,
+                         tot);
     if (tid == 0 && s_wstar >= 0) atomicMax(d.out_wstar, s_wstar);
+    bulk_store_drain();
 }
 
 int launch_narrow_leafpair(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
