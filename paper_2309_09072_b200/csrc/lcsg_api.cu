@@ -22,6 +22,8 @@
 #include "../../include/lcsgrid_b200.h"
 #include "lcsg_internal.cuh"
 
+extern char **environ;
+
 using namespace lcsg;
 
 namespace {
@@ -174,6 +176,8 @@ struct LaunchH {
 
 size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 
+struct SolveEntry;  // per-shape graph cache entry (below)
+
 }  // namespace
 
 struct lcsg_tree_s {
@@ -210,6 +214,8 @@ struct lcsg_tree_s {
     int64_t launches = 0, h2d_bytes = 0, d2h_bytes = 0;
     cudaEvent_t ev[5] = {};
     bool ev_ok = false;
+    bool owns_events = true;
+    SolveEntry *entry = nullptr;  // per-shape graph cache entry this handle runs on
 
     Ctx ctx() const {
         Ctx c;
@@ -294,15 +300,150 @@ struct LayoutCache {
 };
 thread_local LayoutCache t_layout;
 
+// One entry of the level plan on stream s (kernel choice: DESIGN.md 4).
+int launch_plan_entry(lcsg_tree_s *t, const LaunchH &L, cudaStream_t s) {
+    const Ctx c = t->ctx();
+    const int64_t n1 = t->n + 1;
+    const CombineDesc *dd = t->d_descs + L.desc_off;
+    if (L.kind <= 1) return launch_combine(L.kind, dd, L.count, c, L.shift, L.key64, s);
+    if (L.kind == 9) return launch_combine_staged(dd, L.count, c, L.shift, L.key64, s);
+    if (L.kind == 10)
+        return launch_narrow(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s,
+                             L.wpr_log2 != 0);
+    if (L.kind == 11) return launch_narrow_leafpair(dd, L.count, c, L.shift, L.key64, s);
+    if (L.kind == 3)
+        return launch_skeleton(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s);
+    if (L.kind == 6 && L.stride_or_delta > 1 && t->with_trace &&
+        env_int("LCSG_SKEL_WARP_BATCHED", 1))
+        return launch_skeleton_warp(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s);
+    if (L.kind == 5 || L.kind == 6)
+        return launch_combine(L.kind == 5 ? 0 : 1, dd, L.count, c, L.shift, L.key64, s,
+                              L.stride_or_delta);
+    if (L.kind == 7)
+        return launch_block_refine(dd, L.count, c, L.shift, L.key64, L.stride_or_delta,
+                                   L.wpr_log2, L.ustride, s);
+    if (L.kind == 8) return launch_finalize_rows(dd, L.count, c, L.stride_or_delta, s, L.ustride);
+    if (refine_rows(n1, L.stride_or_delta) > 0)
+        return launch_refine(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s);
+    return -1;  // no launch
+}
+
+// Every kernel of a build after the inputs and the plan metadata are in the
+// arena (what build_impl enqueues, minus its host-to-device copies): the
+// sequence a per-shape CUDA graph captures.  Returns a CUDA error or 0.
+int enqueue_build_kernels(lcsg_tree_s *t, cudaStream_t s, int64_t *launches, bool events = true) {
+    const Ctx c = t->ctx();
+    const int32_t nn = (int32_t)t->nodes.size();
+    cudaError_t e = cudaMemsetAsync(t->d_node_wstar, 0, (size_t)nn * 4, s);
+    if (e) return (int)e;
+    int r = launch_nx(t->d_cols, (int32_t)t->n, t->npairs, t->d_nx, t->d_sym_wstar, s);
+    if (r) return r;
+    r = launch_leaf_wstar(t->d_rows, t->d_leaf_nodes, t->d_leaf_rows, t->nleaves,
+                          (int32_t)std::max<int64_t>(t->m_slab, 1), t->d_sym_wstar,
+                          t->d_node_wstar, s);
+    if (r) return r;
+    int64_t nl = 2;
+    if (t->nvirt > 0) {
+        r = launch_virtual_wstar(c, t->d_vnodes, t->nvirt, t->d_node_wstar, s);
+        if (r) return r;
+        ++nl;
+    }
+    if (events && t->timing && t->ev_ok && (e = cudaEventRecord(t->ev[1], s))) return (int)e;
+    for (const LaunchH &L : t->plan) {
+        r = launch_plan_entry(t, L, s);
+        if (r > 0) return r;
+        if (r == 0) ++nl;
+    }
+    if (events && t->timing && t->ev_ok && (e = cudaEventRecord(t->ev[2], s))) return (int)e;
+    if (launches) *launches = nl;
+    return 0;
+}
+
+// ---- per-shape CUDA graphs ---------------------------------------------------
+// A repeated solve of the same shape (rows, columns, pairs, flags, LCSG_*
+// knobs) replays the first solve's kernels as two CUDA graphs -- the build
+// (every level) and the extraction walk -- on the first solve's arena, whose
+// plan metadata (level descriptors, walk nodes with absolute arena pointers)
+// is already resident: per solve the host copies the strings in and launches
+// two graphs instead of planning ~50 launches.  An entry serves
+// one handle at a time (a second concurrent solve of the shape takes the
+// normal path); the next user waits on the previous user's stream through
+// `released`.  Entries are kept only for arenas up to LCSG_GRAPH_MAX_MB
+// (default 8192) and at most 8 of them, LRU-evicted; lcsg_trim() drops them.
+struct SolveEntry {
+    std::string key;
+    int device = 0;
+    bool in_use = false;  // guarded by g_graph_mu
+    uint64_t last_use = 0;
+    lcsg_tree_s *tmpl = nullptr;  // layout, plan and arena pointers of the first solve
+    char *arena = nullptr;
+    size_t arena_bytes = 0;
+    cudaGraphExec_t build = nullptr, walk = nullptr;
+    bool walk_failed = false;
+    cudaStream_t cap = nullptr;     // capture stream (nothing executes on it)
+    cudaEvent_t released = nullptr;  // recorded on the last user's stream
+    bool released_valid = false;
+    cudaEvent_t ev[5] = {};
+    bool ev_ok = false;
+    int64_t build_launches = 0, walk_launches = 0;
+};
+std::mutex g_graph_mu;
+std::vector<SolveEntry *> g_graph_cache;
+uint64_t g_graph_tick = 0;
+constexpr size_t GRAPH_MAX_ENTRIES = 8;
+
+std::string knob_signature() {
+    std::vector<std::string> kv;
+    for (char **e = environ; e && *e; ++e)
+        if (std::strncmp(*e, "LCSG_", 5) == 0 && std::strncmp(*e, "LCSG_LIB_PATH", 13) != 0 &&
+            std::strncmp(*e, "LCSG_HOST_PROFILE", 17) != 0)
+            kv.emplace_back(*e);
+    std::sort(kv.begin(), kv.end());
+    std::string sig;
+    for (auto &x : kv) sig += x + ";";
+    return sig;
+}
+
+void free_entry(SolveEntry *en) {  // caller: entry not in use
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(en->device);
+    if (en->released_valid) cudaEventSynchronize(en->released);
+    if (en->build) cudaGraphExecDestroy(en->build);
+    if (en->walk) cudaGraphExecDestroy(en->walk);
+    if (en->arena) cudaFree(en->arena);  // stream-ordered pool block; all users are done
+    if (en->ev_ok)
+        for (auto &e : en->ev) cudaEventDestroy(e);
+    if (en->released) cudaEventDestroy(en->released);
+    if (en->cap) cudaStreamDestroy(en->cap);
+    delete en->tmpl;
+    delete en;
+    cudaGetLastError();
+    if (prev >= 0) cudaSetDevice(prev);
+}
+
+void release_entry(lcsg_tree_s *t) {
+    SolveEntry *en = t->entry;
+    if (cudaEventRecord(en->released, t->stream) == cudaSuccess) en->released_valid = true;
+    else cudaGetLastError();
+    if (t != en->tmpl) t->nodes.swap(en->tmpl->nodes);  // hand the node list back
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    en->in_use = false;
+}
+
 void destroy(lcsg_tree_s *t) {
     if (!t) return;
-    if (t->nodes.capacity() > t_spare_nodes.capacity()) t->nodes.swap(t_spare_nodes);
     int prev = -1;
     cudaGetDevice(&prev);
     cudaSetDevice(t->device);
     for (auto &kv : t->leaf_cache) cudaFreeAsync(kv.second, t->stream);
-    if (t->arena) cudaFreeAsync(t->arena, t->stream);
-    if (t->ev_ok)
+    if (t->entry) {
+        release_entry(t);  // the arena and the events stay with the cache entry
+    } else {
+        if (t->nodes.capacity() > t_spare_nodes.capacity()) t->nodes.swap(t_spare_nodes);
+        if (t->arena) cudaFreeAsync(t->arena, t->stream);
+    }
+    if (t->ev_ok && t->owns_events)
         for (auto &e : t->ev) cudaEventDestroy(e);
     if (t->own_stream) {
         cudaStreamSynchronize(t->stream);
@@ -386,6 +527,138 @@ struct MetaLease {
     }
 };
 
+std::string graph_key(int device, int64_t m, int32_t top, int32_t bottom, int64_t n, int32_t npairs,
+                      uint32_t flags) {
+    return std::to_string(device) + "|" + std::to_string(m) + "|" + std::to_string(top) + "|" +
+           std::to_string(bottom) + "|" + std::to_string(n) + "|" + std::to_string(npairs) + "|" +
+           std::to_string(flags & (LCSG_WITH_TRACE | LCSG_TIMING)) + "|" + knob_signature();
+}
+
+// A free entry for `key` (marked in use), or nullptr.
+SolveEntry *acquire_entry(const std::string &key) {
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    for (SolveEntry *en : g_graph_cache)
+        if (en->key == key && !en->in_use && en->build) {
+            en->in_use = true;
+            en->last_use = ++g_graph_tick;
+            return en;
+        }
+    return nullptr;
+}
+
+// Build through the shape's graph: the template's layout / plan / pointers,
+// fresh strings, one graph launch.
+int graph_build(lcsg_tree_s *t, SolveEntry *en, const uint8_t *rows, bool rows_dev,
+                const uint8_t *cols, bool cols_dev) {
+    lcsg_tree_s *tp = en->tmpl;
+    std::vector<NodeH> nodes;
+    nodes.swap(tp->nodes);  // the node list travels with the handle while it runs
+    const cudaStream_t st = t->stream;
+    const bool own = t->own_stream;
+    *t = *tp;
+    t->nodes.swap(nodes);
+    t->stream = st;
+    t->own_stream = own;
+    t->entry = en;
+    t->owns_events = false;
+    t->ev_ok = en->ev_ok;
+    for (int q = 0; q < 5; ++q) t->ev[q] = en->ev[q];
+    t->launches = en->build_launches;
+    t->d2h_bytes = 0;
+    const cudaStream_t s = t->stream;
+    const int64_t B = t->npairs;
+    t->h2d_bytes = (rows_dev ? 0 : B * t->m_slab) + (cols_dev ? 0 : B * t->n);
+    CK(en->released_valid ? cudaStreamWaitEvent(s, en->released, 0) : cudaSuccess);
+    if (t->timing && t->ev_ok) CK(cudaEventRecord(t->ev[0], s));
+    if (t->m_slab > 0)
+        CK(cudaMemcpyAsync(t->d_rows, rows + (t->top_row - 1), (size_t)(B * t->m_slab),
+                           rows_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    if (t->n > 0)
+        CK(cudaMemcpyAsync(t->d_cols, cols, (size_t)(B * t->n),
+                           cols_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+    // combine time of a replayed build: the whole graph (the leaf step's three
+    // small kernels included, ~15 us at cfg5 sizes)
+    if (t->timing && t->ev_ok) CK(cudaEventRecord(t->ev[1], s));
+    CK(cudaGraphLaunch(en->build, s));
+    if (t->timing && t->ev_ok) CK(cudaEventRecord(t->ev[2], s));
+    return LCSG_OK;
+}
+
+// After a normal build: keep its arena and capture its kernels as the
+// shape's build graph (best effort: any failure leaves the handle normal).
+void try_create_entry(lcsg_tree_s *t, const std::string &key) {
+    const size_t max_bytes = (size_t)std::max(0, env_int("LCSG_GRAPH_MAX_MB", 8192)) << 20;
+    if (t->arena_bytes > max_bytes) return;
+    const size_t max_total = (size_t)std::max(0, env_int("LCSG_GRAPH_TOTAL_MB", 16384)) << 20;
+    std::vector<SolveEntry *> evict;
+    {
+        std::lock_guard<std::mutex> lk(g_graph_mu);
+        size_t total = t->arena_bytes;
+        for (SolveEntry *en : g_graph_cache) {
+            if (en->key == key) return;  // the shape's entry is busy: no second one
+            total += en->arena_bytes;
+        }
+        while (g_graph_cache.size() >= GRAPH_MAX_ENTRIES || total > max_total) {
+            SolveEntry *lru = nullptr;
+            for (SolveEntry *en : g_graph_cache)
+                if (!en->in_use && (!lru || en->last_use < lru->last_use)) lru = en;
+            if (!lru) break;  // all busy
+            g_graph_cache.erase(std::find(g_graph_cache.begin(), g_graph_cache.end(), lru));
+            total -= lru->arena_bytes;
+            evict.push_back(lru);
+        }
+    }
+    for (SolveEntry *en : evict) free_entry(en);
+    {
+        std::lock_guard<std::mutex> lk(g_graph_mu);
+        if (g_graph_cache.size() >= GRAPH_MAX_ENTRIES) return;
+        size_t total = t->arena_bytes;
+        for (SolveEntry *en : g_graph_cache) total += en->arena_bytes;
+        if (total > max_total) return;
+    }
+    SolveEntry *en = new SolveEntry();
+    en->key = key;
+    en->device = t->device;
+    bool ok = cudaStreamCreateWithFlags(&en->cap, cudaStreamNonBlocking) == cudaSuccess &&
+              cudaEventCreateWithFlags(&en->released, cudaEventDisableTiming) == cudaSuccess;
+    if (ok && t->timing) {
+        en->ev_ok = true;
+        for (auto &e : en->ev)
+            if (cudaEventCreate(&e) != cudaSuccess) en->ev_ok = false;
+    }
+    if (ok) {
+        en->tmpl = new lcsg_tree_s(*t);
+        en->tmpl->leaf_cache.clear();
+        en->tmpl->entry = nullptr;
+        en->tmpl->owns_events = false;
+        en->tmpl->ev_ok = en->ev_ok;
+        for (int q = 0; q < 5; ++q) en->tmpl->ev[q] = en->ev[q];
+        cudaGraph_t g = nullptr;
+        ok = cudaStreamBeginCapture(en->cap, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+        if (ok) {
+            // timing events stay outside the graph (recorded around its launch)
+            const int r = enqueue_build_kernels(en->tmpl, en->cap, &en->build_launches, false);
+            const cudaError_t e = cudaStreamEndCapture(en->cap, &g);
+            ok = r == 0 && e == cudaSuccess && g != nullptr;
+        }
+        if (ok) ok = cudaGraphInstantiate(&en->build, g, 0) == cudaSuccess;
+        if (g) cudaGraphDestroy(g);
+    }
+    cudaGetLastError();
+    if (!ok) {
+        en->arena = nullptr;  // the handle keeps its arena
+        free_entry(en);
+        return;
+    }
+    en->arena = t->arena;
+    en->arena_bytes = t->arena_bytes;
+    en->in_use = true;  // by t
+    en->last_use = ++g_graph_tick;
+    t->entry = en;
+    std::lock_guard<std::mutex> lk(g_graph_mu);
+    g_graph_cache.push_back(en);
+}
+
 int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *cols, bool cols_dev,
                int64_t n, int32_t top_row, int32_t bottom_row, uint32_t flags, int device,
                void *stream, lcsg_handle *out, int32_t npairs = 1) {
@@ -428,6 +701,24 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             if (cudaEventCreate(&e) != cudaSuccess) t->ev_ok = false;
     }
 
+    // a repeated shape replays its CUDA graph (per-shape graph cache above)
+    const bool graph_on = env_int("LCSG_GRAPH", 1) != 0;
+    std::string gkey;
+    if (graph_on) {
+        gkey = graph_key(device, m, top_row, bottom_row, n, npairs, flags);
+        if (SolveEntry *en = acquire_entry(gkey)) {
+            if (t->ev_ok)
+                for (auto &e : t->ev) cudaEventDestroy(e);
+            t->ev_ok = false;
+            const int r = graph_build(t, en, rows, rows_dev, cols, cols_dev);
+            if (r) {
+                destroy(t);
+                return r;
+            }
+            *out = t;
+            return LCSG_OK;
+        }
+    }
     // LCSG_HOST_PROFILE=1: host-side phase times of this call to stderr
     const bool hprof = env_int("LCSG_HOST_PROFILE", 0) != 0;
     auto hclock = [] { return std::chrono::steady_clock::now(); };
@@ -724,30 +1015,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     const Ctx c = t->ctx();
     if (t->nvirt > 0) BCKL(launch_virtual_wstar(c, t->d_vnodes, t->nvirt, t->d_node_wstar, s));
     bool ev1_done = false;  // ev[1]: just before the first level's descriptors
-    auto launch_entry = [&](const LaunchH &L) -> int {
-        const CombineDesc *dd = t->d_descs + L.desc_off;
-        if (L.kind <= 1) return launch_combine(L.kind, dd, L.count, c, L.shift, L.key64, s);
-        if (L.kind == 9) return launch_combine_staged(dd, L.count, c, L.shift, L.key64, s);
-        if (L.kind == 10)
-            return launch_narrow(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s,
-                                 L.wpr_log2 != 0);
-        if (L.kind == 11) return launch_narrow_leafpair(dd, L.count, c, L.shift, L.key64, s);
-        if (L.kind == 3)
-            return launch_skeleton(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s);
-        if (L.kind == 6 && L.stride_or_delta > 1 && t->with_trace &&
-            env_int("LCSG_SKEL_WARP_BATCHED", 1))
-            return launch_skeleton_warp(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s);
-        if (L.kind == 5 || L.kind == 6)
-            return launch_combine(L.kind == 5 ? 0 : 1, dd, L.count, c, L.shift, L.key64, s,
-                                  L.stride_or_delta);
-        if (L.kind == 7)
-            return launch_block_refine(dd, L.count, c, L.shift, L.key64, L.stride_or_delta,
-                                       L.wpr_log2, L.ustride, s);
-        if (L.kind == 8) return launch_finalize_rows(dd, L.count, c, L.stride_or_delta, s, L.ustride);
-        if (refine_rows(n1, L.stride_or_delta) > 0)
-            return launch_refine(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s);
-        return -1;  // no launch
-    };
+    auto launch_entry = [&](const LaunchH &L) -> int { return launch_plan_entry(t, L, s); };
     int32_t maxh = 0;
     for (auto &nd : t->nodes) maxh = std::max(maxh, nd.height);
     const int vbits = bits_for(t->inf);
@@ -930,6 +1198,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
 #undef BCK
 #undef BCKL
     lease.finish();
+    if (graph_on) try_create_entry(t, gkey);
     *out = t;
     return LCSG_OK;
 }
@@ -938,22 +1207,57 @@ bool full_grid(const lcsg_tree_s *t) { return t->top_row == 1 && t->bottom_row =
 
 // recovery walk for weight j from start column i_start (j < 0: the largest
 // weight from i_start, read on the device)
-int run_walk(lcsg_tree_s *t, int32_t j, int32_t i_start = 1) {
-    const cudaStream_t s = t->stream;
+int enqueue_walk(lcsg_tree_s *t, cudaStream_t s, int32_t j, int32_t i_start, int64_t *launches) {
     const Ctx c = t->ctx();
     const TabDev rt = t->tab(t->root);
-    CKL(launch_walk_root(t->d_walk, t->root, c, rt, j, i_start, t->d_wi, t->d_wj, t->d_path,
-                         t->root_batch(), s));
-    ++t->launches;
+    int r = launch_walk_root(t->d_walk, t->root, c, rt, j, i_start, t->d_wi, t->d_wj, t->d_path,
+                             t->root_batch(), s);
+    if (r) return r;
+    int64_t nl = 1;
     const bool retrace = !t->with_trace;
     for (auto &dr : t->depth_ranges) {
-        CKL(launch_walk_level(t->d_walk, t->d_walk_ids + dr.first, dr.second, c, t->d_wi, t->d_wj,
-                              t->d_path, retrace, t->walk_shift, t->walk_key64, s));
-        ++t->launches;
+        r = launch_walk_level(t->d_walk, t->d_walk_ids + dr.first, dr.second, c, t->d_wi, t->d_wj,
+                              t->d_path, retrace, t->walk_shift, t->walk_key64, s);
+        if (r) return r;
+        ++nl;
     }
-    CKL(launch_walk_final(c, rt, i_start, (int32_t)t->m_slab, t->root, t->d_wj, t->d_path,
-                          t->root_batch(), s));
-    ++t->launches;
+    r = launch_walk_final(c, rt, i_start, (int32_t)t->m_slab, t->root, t->d_wj, t->d_path,
+                          t->root_batch(), s);
+    if (r) return r;
+    if (launches) *launches = nl + 1;
+    return 0;
+}
+
+// recovery walk for weight j from start column i_start (j < 0: the largest
+// weight from i_start, read on the device); a handle on a graph-cache entry
+// replays the shape's walk graph for the LCS walk (j < 0 from column 1)
+int run_walk(lcsg_tree_s *t, int32_t j, int32_t i_start = 1) {
+    SolveEntry *en = t->entry;
+    if (en && j < 0 && i_start == 1 && !en->walk_failed) {
+        if (!en->walk) {  // capture once (the entry is in use by this handle only)
+            cudaGraph_t g = nullptr;
+            bool ok = cudaStreamBeginCapture(en->cap, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+            if (ok) {
+                const int r = enqueue_walk(t, en->cap, -1, 1, &en->walk_launches);
+                ok = cudaStreamEndCapture(en->cap, &g) == cudaSuccess && r == 0 && g;
+            }
+            if (ok) ok = cudaGraphInstantiate(&en->walk, g, 0) == cudaSuccess;
+            if (g) cudaGraphDestroy(g);
+            cudaGetLastError();
+            if (!ok) {
+                en->walk = nullptr;
+                en->walk_failed = true;
+            }
+        }
+        if (en->walk) {
+            CK(cudaGraphLaunch(en->walk, t->stream));
+            t->launches += en->walk_launches;
+            return LCSG_OK;
+        }
+    }
+    int64_t nl = 0;
+    CKL(enqueue_walk(t, t->stream, j, i_start, &nl));
+    t->launches += nl;
     return LCSG_OK;
 }
 
@@ -1063,6 +1367,19 @@ int lcsg_trim(int device) {
         if (device < 0 || device >= 64) return fail(LCSG_EINVAL, "device index out of range");
         pool = g_pool[device];
     }
+    std::vector<SolveEntry *> drop;
+    {
+        std::lock_guard<std::mutex> lk(g_graph_mu);
+        for (auto it = g_graph_cache.begin(); it != g_graph_cache.end();) {
+            if ((*it)->device == device && !(*it)->in_use) {
+                drop.push_back(*it);
+                it = g_graph_cache.erase(it);
+            } else {
+                ++it;
+            }
+        }
+    }
+    for (SolveEntry *en : drop) free_entry(en);
     if (!pool) return LCSG_OK;  // nothing allocated on that device yet
     CK(cudaMemPoolTrimTo(pool, 0));
     return LCSG_OK;

@@ -523,3 +523,43 @@ def test_lcs_batch_errors():
         L.lcs_batch([b"ab", b"abc"], [b"x", b"y"])
     assert L.lcs_batch([], []) == []
     assert L.lcs_batch([b"", b""], [b"a", b"b"]) == [L.LcsResult(0, b"", (), ())] * 2
+
+
+def test_graph_replay_repeated_shapes(monkeypatch):
+    """Per-shape CUDA graphs: repeated solves of one shape (new data each time)
+    replay the first solve's build and walk graphs on its arena -- through
+    lcs() in both modes, build_cost_table (every node via the API), batches,
+    a second handle of the shape alive at the same time (normal path), knob
+    changes (a new key) and lcsg_trim -- always bit-exact against the oracle."""
+    rng = np.random.default_rng(2718)
+    lib = _lib.load()
+    for rnd in range(3):
+        for low in (False, True):
+            for _ in range(3):
+                a, b = workloads.random_pair(rng, 90, 130, int(rng.choice([2, 4, 26])))
+                r = L.lcs(a, b, low_memory=low)
+                assert (r.length, r.subsequence, r.row_positions, r.col_positions) == O.lcs(a, b)
+        pairs = [workloads.random_pair(rng, 40, 70, 4) for _ in range(4)]
+        got = L.lcs_batch([p[0] for p in pairs], [p[1] for p in pairs])
+        assert [(r.length, r.subsequence, r.row_positions, r.col_positions) for r in got] == \
+            [O.lcs(a, b) for a, b in pairs]
+        a, b = workloads.random_pair(rng, 70, 160, 4)
+        g = L.GridModel(a, b)
+        held = L.build_cost_table(g, 1, g.m + 1)  # keeps the shape's entry busy
+        a2, b2 = workloads.random_pair(rng, 70, 160, 26)
+        g2 = L.GridModel(a2, b2)
+        second = L.build_cost_table(g2, 1, g2.m + 1)
+        for tab, (x, y) in ((held, (a, b)), (second, (a2, b2))):
+            t = O.OracleTree(x, y)
+            nodes = gpu_tree_nodes(tab)
+            for idx in range(len(t)):
+                np.testing.assert_array_equal(nodes[idx].reach, t.node(idx).reach)
+                if t.node(idx).trace is not None:
+                    np.testing.assert_array_equal(nodes[idx].trace, t.node(idx).trace)
+            length = L.lcs_length(tab)
+            np.testing.assert_array_equal(L.recover_cross_vertices(L.GridModel(x, y), tab, length),
+                                          t.recover(length))
+        del held, second
+        monkeypatch.setenv("LCSG_SKELETON_STRIDE", "16" if rnd == 0 else "8")
+        if rnd == 1:
+            assert lib.lcsg_trim(0) == 0
