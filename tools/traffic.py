@@ -19,7 +19,8 @@ launches = list(recs.values())
 start = max(i for i, d in enumerate(launches) if "nx_kernel" in d["name"])
 launches = launches[start:]
 comb = [d for d in launches
-        if not any(t in d["name"] for t in ("nx_kernel", "leaf_wstar", "walk_", "assemble"))]
+        if not any(t in d["name"] for t in ("nx_kernel", "leaf_wstar", "virtual_wstar", "walk_",
+                                            "assemble"))]
 by = OrderedDict()
 for d in comb:
     k = d["name"].replace("lcsg::", "").split("<")[0]
