@@ -31,6 +31,10 @@ struct NarrowGeom {
     // rows per thread: the per-CTA latency chain (descriptor -> U block -> L
     // window -> fold -> store) is amortised over more rows when the fold is short
     static constexpr int RPT = P <= 2 ? 4 : P == 4 ? 2 : 1;
+    // resident CTAs the register budget is sized for (<= 48 registers for
+    // P <= 4: 5 CTAs per SM, as many as their 40 KB of shared memory allows;
+    // measured 820 -> 776 us (P = 2), 805 -> 742 us (P = 4) at cfg5)
+    static constexpr int MINB = P <= 4 ? 5 : 4;
     static constexpr int ROWS = NT * RPT;  // output rows per CTA
     // split weights k per staged L window
     static constexpr int KC = P <= 16 ? P + 1 : 8;
@@ -268,7 +272,7 @@ __device__ __noinline__ void stage_rows_call(int32_t *dst, const TabAcc &t, int6
 // FW: every combine of the launch has the full output width 2P+1 (each level
 // of a power-of-two tree) -- compile-time row pitch and bounds in the epilogue
 template <int P, typename Key, bool FW = false>
-__global__ void __launch_bounds__(NarrowGeom<P>::NT)
+__global__ void __launch_bounds__(NarrowGeom<P>::NT, NarrowGeom<P>::MINB)
     narrow_combine_kernel(const CombineDesc *__restrict__ descs, Ctx c, int shift, int32_t bpd,
                           int32_t lcap) {
     using G = NarrowGeom<P>;
