@@ -1,6 +1,9 @@
 """Randomised parity sweep on the GPU against the C oracle (test infrastructure):
 lcs() outputs and the final D_G of random pairs over a range of shapes,
 alphabets and orientations (m > n included), until a time budget runs out.
+Round 2 adds: repeated shapes with fresh data (the per-shape CUDA-graph
+replay path), batched solves of equal-shape groups (lcs_batch), and solves
+with forced 64-bit keys (LCSG_FORCE_KEY64=1).
 Usage: python tools/fuzz_parity.py [seconds] [seed]"""
 import os, sys, time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -14,32 +17,70 @@ import workloads
 budget = float(sys.argv[1]) if len(sys.argv) > 1 else 120.0
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 12345)
 t_end = time.time() + budget
-n_cases = 0
+counts = {"single": 0, "repeat": 0, "batch_pairs": 0, "key64": 0, "dg": 0}
 shapes = [(1, 1), (1, 50), (50, 1), (7, 3000), (2, 9000), (130, 130), (257, 300), (600, 700),
           (1100, 900), (300, 9500), (64, 20000), (1500, 1600), (2100, 2100)]
-while time.time() < t_end:
-    m0, n0 = shapes[n_cases % len(shapes)]
-    m = max(1, int(m0 * rng.uniform(0.7, 1.3)))
-    n = max(1, int(n0 * rng.uniform(0.7, 1.3)))
-    sigma = int(rng.choice([2, 4, 20, 26, 200]))
+
+
+def pair(m, n, sigma):
     a, b = workloads.random_pair(rng, m, n, sigma)
     if rng.random() < 0.3:  # planted similarity: long LCS
         k = min(len(a), len(b))
-        bb = bytearray(b)
         src = np.frombuffer(a, np.uint8)[:k]
         mask = rng.random(k) < 0.8
-        arr = np.frombuffer(bytes(bb), np.uint8).copy()
+        arr = np.frombuffer(b, np.uint8).copy()
         arr[:k][mask] = src[mask]
         b = arr.tobytes()
-    low = bool(rng.random() < 0.25)
+    return a, b
+
+
+def check(a, b, low, what):
     got = L.lcs(a, b, low_memory=low)
     exp = O.lcs(a, b)
     assert (got.length, got.subsequence, got.row_positions, got.col_positions) == exp, \
-        f"lcs mismatch m={m} n={n} sigma={sigma} low={low}"
+        f"lcs mismatch ({what}) m={len(a)} n={len(b)} low={low}"
+
+
+i = 0
+prev = None
+while time.time() < t_end:
+    m0, n0 = shapes[i % len(shapes)]
+    i += 1
+    m = max(1, int(m0 * rng.uniform(0.7, 1.3)))
+    n = max(1, int(n0 * rng.uniform(0.7, 1.3)))
+    sigma = int(rng.choice([2, 4, 20, 26, 200]))
+    mode = rng.random()
+    low = bool(rng.random() < 0.25)
+    if mode < 0.15 and prev is not None:  # the previous shape again, fresh data: graph replay
+        m, n = prev
+        for _ in range(2):
+            a, b = pair(m, n, sigma)
+            check(a, b, low, "repeat")
+            counts["repeat"] += 1
+        continue
+    if mode < 0.3 and m * n <= 2_000_000:  # a batch of equal-shape pairs
+        pairs = [pair(m, n, sigma) for _ in range(int(rng.integers(2, 7)))]
+        got = L.lcs_batch([p[0] for p in pairs], [p[1] for p in pairs], low_memory=low)
+        for (a, b), r in zip(pairs, got):
+            assert (r.length, r.subsequence, r.row_positions, r.col_positions) == O.lcs(a, b), \
+                f"batch mismatch m={m} n={n} low={low}"
+        counts["batch_pairs"] += len(pairs)
+        continue
+    a, b = pair(m, n, sigma)
+    if mode < 0.4:
+        os.environ["LCSG_FORCE_KEY64"] = "1"
+        check(a, b, low, "key64")
+        del os.environ["LCSG_FORCE_KEY64"]
+        counts["key64"] += 1
+        continue
+    check(a, b, low, "single")
+    counts["single"] += 1
+    prev = (m, n)
     if m <= n and m * n <= 4_000_000:
         g = L.GridModel(a, b)
         tab = L.build_cost_table(g, 1, g.m + 1, with_trace=not low)
         t = O.OracleTree(a, b)
         assert np.array_equal(tab.reach, t.node(t.root).reach), f"D_G mismatch m={m} n={n}"
-    n_cases += 1
-print(f"fuzz ok: {n_cases} random cases bit-exact vs the oracle")
+        counts["dg"] += 1
+print(f"fuzz ok: {sum(v for k, v in counts.items() if k != 'dg')} random solves bit-exact vs "
+      f"the oracle {counts}")
