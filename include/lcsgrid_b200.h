@@ -67,6 +67,10 @@ int lcsg_free(lcsg_handle h);
  * driver (after lcsg_free of the trees; no reference counterpart -- the
  * reference frees numpy arrays with the CostTable, solver.py:52-53). */
 int lcsg_trim(int device);
+/* Grow the library's pool on `device` by `bytes` now (physical memory mapped
+ * at start-up rather than inside the first large solve, whose arena would
+ * otherwise pay for it -- ~0.2 s for a 16384^2 solve's 34 GB). */
+int lcsg_reserve(int device, int64_t bytes);
 /* Wait for all work enqueued on the handle's stream. */
 int lcsg_sync(lcsg_handle h);
 

@@ -22,6 +22,8 @@ from .solver import (
     lcs,
     lcs_length,
     lcs_batch,
+    reserve,
+    trim,
     lcs_many,
     recover_cross_vertices,
 )
@@ -41,6 +43,8 @@ __all__ = [
     "lcs",
     "lcs_length",
     "lcs_batch",
+    "reserve",
+    "trim",
     "lcs_many",
     "match_positions",
     "recover_cross_vertices",

@@ -55,6 +55,7 @@ SIGNATURES = {
                                          ctypes.c_int, _vp, ctypes.POINTER(_vp)]),
     "lcsg_free": (ctypes.c_int, [_vp]),
     "lcsg_trim": (ctypes.c_int, [ctypes.c_int]),
+    "lcsg_reserve": (ctypes.c_int, [ctypes.c_int, _i64]),
     "lcsg_sync": (ctypes.c_int, [_vp]),
     "lcsg_num_nodes": (_i32, [_vp]),
     "lcsg_root": (_i32, [_vp]),

@@ -1360,6 +1360,26 @@ int lcsg_free(lcsg_handle h) {
     return LCSG_OK;
 }
 
+int lcsg_reserve(int device, int64_t bytes) {
+    if (bytes < 0) return fail(LCSG_EINVAL, "negative size");
+    SaveDevice keep_caller_device;
+    int rc = prepare_device(device);
+    if (rc) return rc;
+    if (bytes == 0) return LCSG_OK;
+    cudaMemPool_t pool;
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        pool = g_pool[device];
+    }
+    // grow the pool once (physical backing mapped now, not inside the first
+    // solve) and hand the block back: it stays in the pool (no release threshold)
+    void *p = nullptr;
+    CK(cudaMallocFromPoolAsync(&p, (size_t)bytes, pool, 0));
+    CK(cudaFreeAsync(p, 0));
+    CK(cudaStreamSynchronize(0));
+    return LCSG_OK;
+}
+
 int lcsg_trim(int device) {
     cudaMemPool_t pool;
     {

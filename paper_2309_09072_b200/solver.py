@@ -272,6 +272,19 @@ def lcs(
                      col_positions=tuple(pb[:L].tolist()))
 
 
+def reserve(nbytes: int, *, device=None) -> None:
+    """Map ``nbytes`` of HBM into the library's memory pool now (a serving
+    process calls this at start-up, so its first large solve does not pay for
+    the pool growth).  No reference counterpart."""
+    _lib.check(_lib.load().lcsg_reserve(_device(device), int(nbytes)), "reserve")
+
+
+def trim(*, device=None) -> None:
+    """Return the pool's unused HBM (and the per-shape graph cache's arenas)
+    to the driver.  No reference counterpart."""
+    _lib.check(_lib.load().lcsg_trim(_device(device)), "trim")
+
+
 # cells (m * n * pairs) per batched launch: bounds the batch's HBM arena
 # (~125 B per cell-equivalent with traces at cfg5-like shapes)
 _BATCH_CELLS = 1 << 28

@@ -563,3 +563,16 @@ def test_graph_replay_repeated_shapes(monkeypatch):
         monkeypatch.setenv("LCSG_SKELETON_STRIDE", "16" if rnd == 0 else "8")
         if rnd == 1:
             assert lib.lcsg_trim(0) == 0
+
+
+def test_reserve_and_trim():
+    """Pool management entry points: reserve maps HBM into the library's pool
+    up front, trim returns it (and drops idle graph-cache entries); solves
+    around them stay exact."""
+    a, b = workloads.generate(1)
+    L.reserve(64 << 20)
+    r1 = L.lcs(a, b)
+    L.trim()
+    assert L.lcs(a, b) == r1
+    with pytest.raises(ValueError, match="negative size"):
+        L.reserve(-1)
