@@ -71,7 +71,10 @@ __device__ __forceinline__ int32_t tcell(const TabAcc &L, int32_t x, int32_t k, 
 // search window then over-covers, which keeps the bound valid.  U and L are
 // always materialised slabs here (never leaves), so plain row pointers are used.
 constexpr int CR_THREADS = 64;
-constexpr int CR_INLINE = 12;  // longer candidate ranges go to the warp-cooperative scan
+#ifndef LCSG_CR_INLINE
+#define LCSG_CR_INLINE 12
+#endif
+constexpr int CR_INLINE = LCSG_CR_INLINE;  // longer candidate ranges go to the warp-cooperative scan
 
 // Interleave-window counts (column kernels): with U[c,.] strictly
 // increasing over finite k, the first k in [lo, hi] with U[c,k] >= Xa is
