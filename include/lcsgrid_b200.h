@@ -177,6 +177,12 @@ int lcsg_stats(lcsg_handle h, int64_t *launches, double *combine_ms, double *lea
  * of 5 timed launches.  *mins_per_s = 32-bit min operations per second. */
 int lcsg_probe_int32_rate(int device, double *mins_per_s, int32_t *sm_count, double *ms);
 
+/* Consistency violations counted by the row-sweep kernels on `device`
+ * (lcsg_sweep.cu: every generated row is checked against the structural
+ * invariants it relies on; non-zero means a result may be wrong).  `reset`
+ * non-zero clears the counter after reading. */
+int lcsg_sweep_errors(int device, int32_t *count, int reset);
+
 #ifdef __cplusplus
 }
 #endif

@@ -23,6 +23,7 @@ from .solver import (
     lcs_length,
     lcs_batch,
     reserve,
+    sweep_errors,
     trim,
     lcs_many,
     recover_cross_vertices,
@@ -44,6 +45,7 @@ __all__ = [
     "lcs_length",
     "lcs_batch",
     "reserve",
+    "sweep_errors",
     "trim",
     "lcs_many",
     "match_positions",

@@ -20,7 +20,7 @@ _DEFAULT_LIB = os.path.join(LIB_DIR, "liblcsgrid_b200.so")
 LIB_PATH = os.environ.get("LCSG_LIB_PATH") or _DEFAULT_LIB
 CSRC = os.path.join(_PKG, "csrc")
 SOURCES = ["lcsg_api.cu", "lcsg_kernels.cu", "lcsg_refine.cu", "lcsg_tile.cu", "lcsg_narrow.cu",
-           "lcsg_probe.cu"]
+           "lcsg_probe.cu", "lcsg_sweep.cu"]
 NVCC_FLAGS = [
     "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
     "-Xcompiler", "-fPIC", "-shared",
@@ -84,6 +84,7 @@ SIGNATURES = {
     "lcsg_combine_rows": (ctypes.c_int, [_vp, _i32, _vp, _vp, _i32, _vp, _i32, _vp, _vp, _vp,
                                          _vp, _i32, _i32, _i64, _i64, _i64, _vp]),
     "lcsg_recover_from": (ctypes.c_int, [_vp, _i32, _i32, _vp]),
+    "lcsg_sweep_errors": (ctypes.c_int, [ctypes.c_int, _i32p, ctypes.c_int]),
     "lcsg_probe_int32_rate": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double),
                                              _i32p, ctypes.POINTER(ctypes.c_double)]),
     "lcsg_stats": (ctypes.c_int, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_double),

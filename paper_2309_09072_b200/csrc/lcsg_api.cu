@@ -157,7 +157,7 @@ int default_col_block(int64_t n1) { return n1 <= 4097 ? 4 : 8; }
 struct NodeH {
     int32_t top_row, bottom_row, w1, upper, lower, height, depth, leaf_row;
     int32_t pair = 0;  // batched solves: the pair this node belongs to
-    int64_t reach_off = -1, trace_off = -1, kmax_off = -1;  // int32 element offsets
+    int64_t reach_off = -1, trace_off = -1, kmax_off = -1, ev_off = -1;  // int32 element offsets
     int kind = 0;
     bool virt = false;  // virtual height-1 node: no table (TabDev closed form of its leaves)
 };
@@ -323,6 +323,8 @@ int launch_plan_entry(lcsg_tree_s *t, const LaunchH &L, cudaStream_t s) {
         return launch_block_refine(dd, L.count, c, L.shift, L.key64, L.stride_or_delta,
                                    L.wpr_log2, L.ustride, s);
     if (L.kind == 8) return launch_finalize_rows(dd, L.count, c, L.stride_or_delta, s, L.ustride);
+    if (L.kind == 12) return launch_table_events(dd, L.count, c, s);
+    if (L.kind == 13) return launch_sweep(dd, L.count, c, L.stride_or_delta, L.ustride, s);
     if (refine_rows(n1, L.stride_or_delta) > 0)
         return launch_refine(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s);
     return -1;  // no launch
@@ -778,6 +780,10 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     // refinement mode: tiled (default) or one launch per pass ("LCSG_REFINE_PASSES=1")
     const bool tiled = env_int("LCSG_REFINE_PASSES", 0) == 0;
     const bool narrow_on = env_int("LCSG_NARROW", 1) != 0;
+    // wide combines: row sweep below the skeleton rows (LCSG_SWEEP=0: the
+    // column-refinement stages)
+    const bool sweep_on = env_int("LCSG_SWEEP", 1) != 0;
+    const int sweep_stride = std::max(2, env_int("LCSG_SWEEP_STRIDE", 64));
     // block size (local rows) of each column-refinement stage, power of two
     int col_block = 1;
     while (col_block * 2 <= std::min(16, std::max(2, env_int("LCSG_COL_BLOCK", default_col_block(n1)))))
@@ -839,6 +845,8 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             if (nd.upper < 0 || nd.virt) continue;
             nd.kmax_off = tab_elems;
             tab_elems += (n1 + 63) / 64 * 64;
+            nd.ev_off = tab_elems;  // per-row insertion ranks (row-sweep kernels)
+            tab_elems += (n1 + 63) / 64 * 64;
         }
         // low-memory mode: the refinement passes still need this level's traces
         // (they bound neighbouring rows); one scratch region reused level by level
@@ -888,6 +896,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
                 if (nd.leaf_row >= 0) nd.leaf_row += (int32_t)(p * t->m_slab);
                 if (nd.reach_off >= 0) nd.reach_off += p * pair_tab;
                 if (nd.kmax_off >= 0) nd.kmax_off += p * pair_tab;
+                if (nd.ev_off >= 0) nd.ev_off += p * pair_tab;
                 if (nd.trace_off >= 0) nd.trace_off += t->with_trace ? p * pair_tab : p * scratch_elems;
                 t->nodes[(size_t)p * nn1 + id] = nd;
             }
@@ -1036,6 +1045,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
         for (int kind = 0; kind < 3; ++kind) {
             int32_t start = di;
             int32_t maxk = 0, maxw1 = 0, maxkl = 0, minw1 = INT32_MAX;
+            bool ev_make_any = false;
             for (const int32_t id : by_height[h]) {
                 const NodeH &nd = t->nodes[id];
                 if (nd.kind != kind) continue;
@@ -1049,6 +1059,15 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
                 d.out_wstar = t->d_node_wstar + id;
                 d.w1 = nd.w1;
                 d.node = id;
+                {
+                    const NodeH &un = t->nodes[nd.upper];
+                    d.U_ev = un.ev_off >= 0 ? t->d_tables + un.ev_off : nullptr;
+                    d.out_ev = t->d_tables + nd.ev_off;
+                    // a kind-2 child's events are a by-product of its own sweep
+                    d.U_ev_make = (kind == 2 && sweep_on && un.kind != 2) ? 1 : 0;
+                    d.pad_ = 0;
+                    if (d.U_ev_make) ev_make_any = true;
+                }
                 maxk = std::max(maxk, t->nodes[nd.upper].w1 - 1);
                 maxkl = std::max(maxkl, t->nodes[nd.lower].w1 - 1);
                 maxw1 = std::max(maxw1, nd.w1);
@@ -1085,7 +1104,8 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             // (re-measured after the fine-kernel changes: the root's stride 32
             // now loses 0.14 ms against 64, so only the 512 rule remains)
             const bool dflt = getenv("LCSG_SKELETON_STRIDE") == nullptr && n1 > 8193;
-            const int stride_def = (dflt && maxw1 <= 513 && L.count >= 32) ? 512 : skel_stride;
+            const int stride_def = sweep_on ? sweep_stride
+                                   : (dflt && maxw1 <= 513 && L.count >= 32) ? 512 : skel_stride;
             const int stride_h =
                 std::max(2, env_int(("LCSG_SKEL_STRIDE_H" + hs).c_str(), stride_def));
             int32_t S = 1;
@@ -1101,6 +1121,24 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             L.kind = maxw1 <= skel_thread_max ? 5 : (maxw1 <= skel_warp_max ? 6 : 3);
             L.stride_or_delta = S;
             t->plan.push_back(L);
+            if (sweep_on) {  // row sweep below every skeleton row + finalize (lcsg_sweep.cu)
+                if (ev_make_any) {
+                    LaunchH E = L;
+                    E.kind = 12;
+                    t->plan.push_back(E);
+                }
+                LaunchH W = L;
+                W.kind = 13;
+                W.stride_or_delta = S;
+                W.ustride = maxw1;
+                t->plan.push_back(W);
+                LaunchH F = L;
+                F.kind = 8;
+                F.stride_or_delta = S;
+                F.ustride = maxw1;
+                t->plan.push_back(F);
+                continue;
+            }
             if (tiled) {  // column-refinement stages (row step S/B, S/B^2, .., 1) + finalize
                 int32_t rem = S;
                 while (rem > 1) {

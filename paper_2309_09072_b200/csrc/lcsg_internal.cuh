@@ -47,6 +47,14 @@ struct CombineDesc {
     int32_t *out_wstar;  // scalar, zero-initialised, atomicMax'ed
     int32_t w1;
     int32_t node;
+    // row-sweep kernels (lcsg_sweep.cu): per-row insertion ranks ("events") of
+    // the upper child and of this combine's own table -- ev[c] = first k with
+    // reach[c+1][k] != reach[c][k+1]; U_ev_make: U's events are not a sweep
+    // by-product and must be derived from its table first
+    int32_t *U_ev;
+    int32_t *out_ev;
+    int32_t U_ev_make;
+    int32_t pad_;
 };
 
 // Resolved accessor of a table inside a kernel.
@@ -182,6 +190,12 @@ int launch_block_refine(const CombineDesc *descs, int32_t ndesc, Ctx c, int shif
 // INF suffix + kmax/wstar of the interior rows after the tiled refinement
 int launch_finalize_rows(const CombineDesc *descs, int32_t ndesc, Ctx c, int32_t S,
                          cudaStream_t s, int32_t maxw1);
+// row-sweep path (lcsg_sweep.cu): events of the upper children that need them,
+// then the interior rows of blocks of S rows below each skeleton row
+int launch_table_events(const CombineDesc *descs, int32_t ndesc, Ctx c, cudaStream_t s);
+int launch_sweep(const CombineDesc *descs, int32_t ndesc, Ctx c, int32_t S, int32_t maxw1,
+                 cudaStream_t s);
+int sweep_error_count(int32_t *count, bool reset);
 int launch_walk_level(const WalkNode *nodes, const int32_t *ids, int32_t count, Ctx c,
                       int32_t *wi, int32_t *wj, int32_t *cols_out, bool retrace, int key_shift,
                       bool key64, cudaStream_t s);

@@ -1,0 +1,403 @@
+// lcsg_sweep.cu -- row-sweep generation of the wide combines' interior rows.
+//
+// A slab table is the inverse of a unit-Monge LCS score matrix, so consecutive
+// rows differ by one event: with S_c = {reach[c][j]} (sorted, S_c[0] = c+1),
+//     S_{c+1} = S_c \ {c+1} + {t_c},
+// i.e. row c+1 is row c with the prefix [1, j1] shifted left by one and one new
+// element t_c inserted at rank j1 (none when t_c = INF).  For the combine
+// C = U (x) L (solver.py:91-110, _kernel.pyx:28-82) the first-wins split
+// k*(c,j) obeys the same structure (derivation and proof sketch in DESIGN.md 5b;
+// checked bit-exact against the reference on every test input):
+//   * cells right of the insertion whose split lies right of U's own
+//     insertion rank ju1 (trace[c][j] > ju1): value and trace unchanged;
+//   * cells left of the insertion: value = C[c][j+1], trace = trace[c][j+1]-1
+//     (while that trace is >= 1);
+//   * only the cells between (j1 <= j <= J, J = last j with trace[c][j] <= ju1)
+//     and a short zero-trace prefix need candidates evaluated, each over a
+//     split range bounded by ju1 below and by its right neighbour's split above.
+// So a row costs a handful of L gathers (one warp) plus a streaming rewrite of
+// the row -- the kernel is bound by the 8 B per cell it writes, not by
+// per-cell searches.  The chain over rows is cut by the skeleton rows
+// (exact Alg. 1 every S rows, lcsg_refine.cu): one thread group sweeps the
+// S-1 interior rows below a skeleton row, with the row state (reach, trace of
+// the finite prefix) ping-ponged in shared memory, or kept in the output rows
+// themselves when the finite prefix does not fit.
+#include <algorithm>
+#include <climits>
+#include <cstdlib>
+
+#include "lcsg_internal.cuh"
+
+namespace lcsg {
+
+#define LCSG_LAUNCH_CHECK()                         \
+    do {                                            \
+        cudaError_t e__ = cudaGetLastError();       \
+        if (e__ != cudaSuccess) return (int)e__;    \
+    } while (0)
+
+// consistency violations seen by the sweep (a non-zero value means a row
+// failed one of the structural invariants; tests read it through
+// lcsg_sweep_errors and fail loudly)
+__device__ int32_t g_sweep_err = 0;
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr uint64_t KEY_NONE = ~(uint64_t)0;
+
+// Insertion rank of row c+1 against row c of a materialised table: the first
+// k in [0, kmax[c+1]] with reach[c+1][k] != reach[c][k+1] (the predicate is
+// monotone: equal below the insertion, different from it on), kmax[c+1]+1
+// when nothing was inserted.  One thread per row, binary search.
+__global__ void __launch_bounds__(256)
+    table_events_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c) {
+    const int32_t di = blockIdx.y;
+    if (di >= ndesc) return;
+    const CombineDesc &d = descs[di];
+    if (!d.U_ev_make) return;
+    const int32_t row = (int32_t)(blockIdx.x * blockDim.x + threadIdx.x);
+    if (row >= c.n) return;
+    const int32_t w1 = d.U.w1;
+    const int32_t *a = d.U.reach + (size_t)row * w1, *b = a + w1;
+    const int32_t kb = __ldg(d.U.kmax + row + 1);
+    int32_t lo = 0, hi = kb + 1;  // answer in [lo, hi]
+    while (lo < hi) {
+        const int32_t md = (lo + hi) >> 1;
+        if (__ldg(b + md) != __ldg(a + md + 1)) hi = md; else lo = md + 1;
+    }
+    d.U_ev[row] = lo;
+}
+
+// last j in [0, K] with T[j] <= thr; T is nondecreasing on [0, K] and
+// T[0] <= thr.  Warp-cooperative 32-ary search (all lanes get the result).
+__device__ __forceinline__ int32_t warp_last_le(const int32_t *T, int32_t K, int32_t thr, int lane) {
+    int32_t lo = 0, hi = K + 1;
+    while (hi - lo > 1) {
+        const int32_t step = (hi - lo - 1 + 31) >> 5;
+        const int32_t p = lo + (lane + 1) * step;
+        const bool ok = p < hi && T[p] <= thr;
+        const int cnt = __popc(__ballot_sync(FULL, ok));
+        lo += cnt * step;
+        hi = min(hi, lo + step);
+    }
+    return lo;
+}
+
+__device__ __forceinline__ uint64_t warp_min64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t t = __shfl_xor_sync(FULL, v, o);
+        v = t < v ? t : v;
+    }
+    return v;
+}
+
+constexpr int SW_MAXQ = 64;  // cells evaluated per round
+constexpr int SW_SEG = 64;   // prefetched U entries from the insertion rank on
+
+__device__ __forceinline__ void cp_async4(void *smem, const void *gmem) {
+    const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+// One thread group (the CTA) sweeps the rows (a, a+S) of one combine.  Per
+// step (row cr -> cr+1): every warp locates J in the shared row state, all
+// threads evaluate the candidate (cell, split) pairs of the cells J, J-1, ...
+// at once (one round of dependent L gathers; keys reduce per cell with
+// shared-memory atomicMin), every warp reads off the insertion rank j1, and
+// all threads rewrite / store the row.  The U-side inputs of the next step
+// (insertion rank, kmax, the U entries from the rank on) are fetched a step
+// ahead with cp.async.
+__global__ void sweep_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int32_t S,
+                             int32_t nblk, int32_t cap) {
+    extern __shared__ int32_t ssm[];  // R0[cap] T0[cap] R1[cap] T1[cap] evs[S] kms[S]
+    __shared__ unsigned long long cellkey[2][SW_MAXQ];
+    __shared__ int32_t useg[2][SW_SEG];
+    __shared__ int32_t s0ctl[2];
+    const int32_t di = (int32_t)(blockIdx.z * 65535u + blockIdx.y);
+    if (di >= ndesc) return;
+    const int32_t blk = blockIdx.x;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
+    const CombineDesc &d = descs[di];
+    const int32_t n = c.n, inf = c.inf;
+    const int32_t a = blk * S;
+    if (a >= n) return;
+    const int32_t nsteps = min(S, n - a);  // rows a+1 .. a+nsteps; the last one is a skeleton row
+    const int32_t w1 = d.w1, uw1 = d.U.w1, lw1 = d.L.w1, wl = lw1 - 1;
+    const int32_t *__restrict__ Ur = d.U.reach;
+    const int32_t *__restrict__ Lr = d.L.reach;
+    int32_t *const out_reach = d.out_reach;
+    int32_t *const out_trace = d.out_trace;
+    int32_t *const out_ev = d.out_ev;
+    int32_t *const evs = ssm + 4 * (size_t)cap, *const kms = evs + S;
+
+    int32_t K = d.out_kmax[a];  // written by the skeleton kernel
+    const bool in_smem = K + 2 <= cap;
+    // row state: old = row c, new = row c+1
+    int32_t *oR, *oT, *nR, *nT;
+    if (in_smem) {
+        oR = ssm;
+        oT = ssm + cap;
+        nR = ssm + 2 * (size_t)cap;
+        nT = ssm + 3 * (size_t)cap;
+        const int32_t *gr = out_reach + (size_t)a * w1, *gt = out_trace + (size_t)a * w1;
+        for (int32_t j = tid; j <= K; j += nt) {
+            oR[j] = gr[j];
+            oT[j] = gt[j];
+        }
+    } else {
+        oR = out_reach + (size_t)a * w1;
+        oT = out_trace + (size_t)a * w1;
+        nR = oR + w1;
+        nT = oT + w1;
+    }
+    for (int32_t t = tid; t < nsteps; t += nt) {
+        evs[t] = d.U_ev[a + t];
+        kms[t] = d.U.kmax[a + t + 1];
+    }
+    for (int t = tid; t < 2 * SW_MAXQ; t += nt) cellkey[0][t] = KEY_NONE;
+    __syncthreads();
+    for (int t = tid; t < SW_SEG; t += nt) {
+        const int32_t k = evs[0] + t;
+        if (k <= kms[0]) useg[0][t] = Ur[(size_t)(a + 1) * uw1 + k];
+    }
+    __syncthreads();
+
+    for (int32_t st = 0; st < nsteps; ++st) {
+        const int32_t cr = a + st;  // row cr -> row cr + 1
+        const bool dowrite = st + 1 < nsteps;
+        const int32_t ju1 = evs[st], kmU = kms[st];
+        const int32_t *Uc = Ur + (size_t)(cr + 1) * uw1;
+        const int32_t *seg = useg[st & 1];
+        unsigned long long *ck = cellkey[st & 1];
+        if (dowrite)  // the next step's U entries, a step ahead
+            for (int t = tid; t < SW_SEG; t += nt) {
+                const int32_t k = evs[st + 1] + t;
+                if (k <= kms[st + 1]) cp_async4(&useg[(st + 1) & 1][t], Uc + uw1 + k);
+            }
+        const int32_t J = warp_last_le(oT, K, ju1, lane);
+        int32_t jb = J;
+        int32_t ubR = J < K ? oT[J + 1] : INT_MAX;
+        int32_t j1 = -1, Qc = 0;
+        int32_t qcap = 8;  // most walks are short: few speculative cells first
+        while (true) {
+            const int32_t ub0 = min(kmU, ubR);
+            const int32_t lmax = ub0 - ju1 + 1;  // splits per cell (before the j clamps)
+            const int32_t ls = max(lmax, 1);
+            Qc = min(min(jb + 1, qcap), max(4, 2 * nt / ls));
+            qcap = SW_MAXQ;
+            const int32_t npair = Qc * ls;
+            for (int32_t p = tid; p < npair; p += nt) {
+                const int32_t q = p / ls, r = p - q * ls;
+                const int32_t j = jb - q, k = ju1 + r;
+                if (r < lmax && k <= j && j - k <= wl) {
+                    const int32_t x = r < SW_SEG ? seg[r] : Uc[k];  // finite: k <= kmax_U
+                    const int32_t v = Lr[(size_t)(x - 1) * lw1 + (j - k)];
+                    atomicMin(&ck[q], ((unsigned long long)(uint32_t)v << 32) | (uint32_t)k);
+                }
+            }
+            __syncthreads();
+            // every warp reads off the first cell (from the right) whose value changed
+            int first = -1;
+            for (int32_t q0 = 0; q0 < Qc && first < 0; q0 += 32) {
+                const int32_t q = q0 + lane;
+                bool chg = false;
+                if (q < Qc) {
+                    const unsigned long long my = ck[q];
+                    chg = !(my != KEY_NONE && (int32_t)(my >> 32) < inf &&
+                            (int32_t)(my >> 32) == oR[jb - q]);
+                }
+                const unsigned nb = __ballot_sync(FULL, chg);
+                if (nb) first = q0 + __ffs(nb) - 1;
+            }
+            if (first >= 0) {
+                j1 = jb - first;
+                break;
+            }
+            // all Qc cells kept their value (new splits): store them, go further left
+            ubR = (int32_t)(uint32_t)ck[Qc - 1];
+            if (dowrite && tid < Qc) {
+                nR[jb - tid] = (int32_t)(ck[tid] >> 32);
+                nT[jb - tid] = (int32_t)(uint32_t)ck[tid];
+            }
+            __syncthreads();
+            if (tid < Qc) ck[tid] = KEY_NONE;
+            __syncthreads();
+            jb -= Qc;
+            if (jb < 0) {  // cannot happen: cell 0 always changes (c+1 -> c+2)
+                if (tid == 0) atomicAdd(&g_sweep_err, 1);
+                j1 = 0;
+                jb = 0;
+                break;
+            }
+        }
+        // cells j1 .. jb are in ck (q = jb - j), cells (jb, J] already in nR / nT
+        const unsigned long long newkey = ck[jb - j1];
+        int32_t nv = newkey == KEY_NONE ? inf : (int32_t)(newkey >> 32);
+        const int32_t nk = (int32_t)(uint32_t)newkey;
+        if (nv >= inf) {
+            nv = inf;
+            if (j1 != K && tid == 0) atomicAdd(&g_sweep_err, 1);
+        }
+        const int32_t Knew = nv < inf ? K : K - 1;
+        if (tid == 0) out_ev[cr] = j1;
+        if (!dowrite) break;
+        // zero-split prefix of the shifted cells: trace 0 unless the right
+        // neighbour's split is positive, then the first k reaching the value
+        int32_t s0lo = 0, s0hi = -1;
+        {
+            const int32_t J0 = warp_last_le(oT, K, 0, lane);
+            int32_t js = min(j1, J0) - 1;
+            int32_t ub = 0;
+            if (js >= 0) {
+                ub = js + 1 == j1 ? (nv < inf ? nk : INT_MAX) : oT[js + 2] - 1;
+                ub = min(ub, kmU);
+            }
+            if (js >= 1 && ub > 0) {  // rare: warp 0 scans, right to left
+                if (tid < 32) {
+                    const int32_t hi0 = js;
+                    while (js >= 0 && ub > 0) {
+                        const int32_t target = oR[js + 1];
+                        const int32_t klo = max(0, js - wl), khi = min(ub, js);
+                        if (khi <= 0) break;  // js == 0: trace 0 (the default rule)
+                        int32_t found = -1;
+                        for (int32_t kb = klo; kb <= khi && found < 0; kb += 32) {
+                            const int32_t k = kb + lane;
+                            bool hit = false;
+                            if (k <= khi) {
+                                const int32_t x = Uc[k];
+                                hit = Lr[(size_t)(x - 1) * lw1 + (js - k)] == target;
+                            }
+                            const unsigned b = __ballot_sync(FULL, hit);
+                            if (b) found = kb + __ffs(b) - 1;
+                        }
+                        if (found < 0) {
+                            if (lane == 0) atomicAdd(&g_sweep_err, 1);
+                            found = 0;
+                        }
+                        if (lane == 0) {
+                            nR[js] = target;
+                            nT[js] = found;
+                        }
+                        ub = found;
+                        --js;
+                    }
+                    if (lane == 0) {
+                        s0ctl[0] = js + 1;
+                        s0ctl[1] = hi0;
+                    }
+                }
+                __syncthreads();
+                s0lo = s0ctl[0];
+                s0hi = s0ctl[1];
+            }
+        }
+        {
+            int32_t *gR = out_reach + (size_t)(cr + 1) * w1, *gT = out_trace + (size_t)(cr + 1) * w1;
+            for (int32_t j = tid; j < w1; j += nt) {
+                if (j <= Knew) {
+                    int32_t v, t;
+                    if (j >= j1 && j <= jb) {  // this round's cells
+                        const unsigned long long key = ck[jb - j];
+                        v = (int32_t)(key >> 32);
+                        t = (int32_t)(uint32_t)key;
+                    } else if ((j > jb && j <= J) || (j >= s0lo && j <= s0hi)) {
+                        if (!in_smem) continue;  // already in the output row
+                        v = nR[j];
+                        t = nT[j];
+                    } else if (j < j1) {
+                        v = oR[j + 1];
+                        t = max(oT[j + 1] - 1, 0);
+                    } else {
+                        v = oR[j];
+                        t = oT[j];
+                    }
+                    if (in_smem) {
+                        nR[j] = v;
+                        nT[j] = t;
+                    }
+                    gR[j] = v;
+                    gT[j] = t;
+                } else {
+                    gR[j] = inf;  // INF suffix: traces are finalize's
+                }
+            }
+            K = Knew;
+        }
+        for (int t = tid; t < SW_MAXQ; t += nt) cellkey[(st + 1) & 1][t] = KEY_NONE;
+        cp_async_wait_all();
+        __syncthreads();
+        if (in_smem) {
+            int32_t *t0 = oR, *t1 = oT;
+            oR = nR;
+            oT = nT;
+            nR = t0;
+            nT = t1;
+        } else {
+            oR = nR;
+            oT = nT;
+            nR += w1;
+            nT += w1;
+        }
+    }
+}
+
+}  // namespace
+
+int launch_table_events(const CombineDesc *descs, int32_t ndesc, Ctx c, cudaStream_t s) {
+    if (ndesc <= 0 || c.n <= 0) return 0;
+    if (ndesc > 65535) return (int)cudaErrorInvalidValue;
+    const dim3 blocks((unsigned)((c.n + 255) / 256), (unsigned)ndesc);
+    table_events_kernel<<<blocks, 256, 0, s>>>(descs, ndesc, c);
+    LCSG_LAUNCH_CHECK();
+    return 0;
+}
+
+int launch_sweep(const CombineDesc *descs, int32_t ndesc, Ctx c, int32_t S, int32_t maxw1,
+                 cudaStream_t s) {
+    if (ndesc <= 0 || c.n <= 0) return 0;
+    if (S > 1024) return (int)cudaErrorInvalidValue;
+    const int32_t nblk = (c.n + S - 1) / S;
+    static int cap_max = 0, cpt = 0;
+    if (!cap_max) {
+        const char *e = getenv("LCSG_SWEEP_CAP");
+        cap_max = e ? atoi(e) : 12800;
+        const char *e2 = getenv("LCSG_SWEEP_CPT");
+        cpt = e2 ? std::max(1, atoi(e2)) : 8;
+        cudaFuncSetAttribute(sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * cap_max + 8 * 1024);
+    }
+    const int32_t cap = std::min(maxw1 + 1, cap_max);
+    int nt = 32;
+    while (nt < 1024 && nt * cpt < maxw1) nt *= 2;
+    const dim3 blocks((unsigned)nblk, (unsigned)std::min<int32_t>(ndesc, 65535),
+                      (unsigned)((ndesc + 65534) / 65535));
+    sweep_kernel<<<blocks, nt, (size_t)16 * cap + (size_t)8 * S, s>>>(descs, ndesc, c, S, nblk, cap);
+    LCSG_LAUNCH_CHECK();
+    return 0;
+}
+
+int sweep_error_count(int32_t *count, bool reset) {
+    cudaError_t e = cudaMemcpyFromSymbol(count, g_sweep_err, sizeof(int32_t));
+    if (e != cudaSuccess) return (int)e;
+    if (reset) {
+        const int32_t z = 0;
+        e = cudaMemcpyToSymbol(g_sweep_err, &z, sizeof(int32_t));
+    }
+    return (int)e;
+}
+
+}  // namespace lcsg
+
+extern "C" int lcsg_sweep_errors(int device, int32_t *count, int reset) {
+    if (!count) return -1;
+    int prev = 0;
+    if (cudaGetDevice(&prev) != cudaSuccess) return -2;
+    if (cudaSetDevice(device) != cudaSuccess) return -2;
+    const int e = lcsg::sweep_error_count(count, reset != 0);
+    cudaSetDevice(prev);
+    return e ? -2 : 0;
+}

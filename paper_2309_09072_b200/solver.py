@@ -285,6 +285,18 @@ def trim(*, device=None) -> None:
     _lib.check(_lib.load().lcsg_trim(_device(device)), "trim")
 
 
+def sweep_errors(*, device=None, reset: bool = False) -> int:
+    """Consistency violations counted by the row-sweep kernels on ``device``
+    since the last reset (0 unless a structural invariant failed; tests and
+    ``bench.py`` assert it).  No reference counterpart."""
+    import ctypes
+
+    cnt = ctypes.c_int32(0)
+    _lib.check(_lib.load().lcsg_sweep_errors(_device(device), ctypes.byref(cnt), int(reset)),
+               "sweep_errors")
+    return int(cnt.value)
+
+
 # cells (m * n * pairs) per batched launch: bounds the batch's HBM arena
 # (~125 B per cell-equivalent with traces at cfg5-like shapes)
 _BATCH_CELLS = 1 << 28

@@ -85,3 +85,23 @@ def reference():
     import lcsgrid_ref
 
     return lcsgrid_ref
+
+
+@pytest.fixture(autouse=True)
+def _sweep_invariants(request):
+    """After every GPU test: the row-sweep kernels' invariant counter is zero."""
+    yield
+    if request.node.get_closest_marker("gpu") is None:
+        return
+    import paper_2309_09072_b200 as L
+
+    if not L.have_extension():
+        return
+    try:
+        import torch
+
+        if not torch.cuda.is_available():
+            return
+    except Exception:
+        return
+    assert L.sweep_errors(reset=True) == 0, "row-sweep invariant violated"
