@@ -158,6 +158,7 @@ struct NodeH {
     int32_t top_row, bottom_row, w1, upper, lower, height, depth, leaf_row;
     int32_t pair = 0;  // batched solves: the pair this node belongs to
     int64_t reach_off = -1, trace_off = -1, kmax_off = -1, ev_off = -1;  // int32 element offsets
+    int64_t flag_off = -1;  // kind 2: block flags of the row sweep (index into d_flags)
     int kind = 0;
     bool virt = false;  // virtual height-1 node: no table (TabDev closed form of its leaves)
 };
@@ -211,6 +212,8 @@ struct lcsg_tree_s {
     std::map<int32_t, int32_t *> leaf_cache;  // materialised leaves / virtual nodes (API only)
     int32_t nvirt = 0;
     int32_t *d_vnodes = nullptr;
+    int32_t *d_flags = nullptr;  // row-sweep block flags of every kind-2 node (zeroed per solve)
+    size_t flags_bytes = 0;
     int64_t launches = 0, h2d_bytes = 0, d2h_bytes = 0;
     cudaEvent_t ev[5] = {};
     bool ev_ok = false;
@@ -324,7 +327,8 @@ int launch_plan_entry(lcsg_tree_s *t, const LaunchH &L, cudaStream_t s) {
                                    L.wpr_log2, L.ustride, s);
     if (L.kind == 8) return launch_finalize_rows(dd, L.count, c, L.stride_or_delta, s, L.ustride);
     if (L.kind == 12) return launch_table_events(dd, L.count, c, s);
-    if (L.kind == 13) return launch_sweep(dd, L.count, c, L.stride_or_delta, L.ustride, s);
+    if (L.kind == 13)
+        return launch_sweep(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, L.ustride, s);
     if (refine_rows(n1, L.stride_or_delta) > 0)
         return launch_refine(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, s);
     return -1;  // no launch
@@ -338,6 +342,7 @@ int enqueue_build_kernels(lcsg_tree_s *t, cudaStream_t s, int64_t *launches, boo
     const int32_t nn = (int32_t)t->nodes.size();
     cudaError_t e = cudaMemsetAsync(t->d_node_wstar, 0, (size_t)nn * 4, s);
     if (e) return (int)e;
+    if (t->flags_bytes && (e = cudaMemsetAsync(t->d_flags, 0, t->flags_bytes, s))) return (int)e;
     int r = launch_nx(t->d_cols, (int32_t)t->n, t->npairs, t->d_nx, t->d_sym_wstar, s);
     if (r) return r;
     r = launch_leaf_wstar(t->d_rows, t->d_leaf_nodes, t->d_leaf_rows, t->nleaves,
@@ -905,6 +910,13 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
         t->nvirt *= npairs;
     }
     off = align_up(o_tab + (size_t)tab_elems * 4);
+    // row-sweep block flags: one int per block of rows (>= 2 rows) of every kind-2 node
+    const int64_t fstride = (n1 / 2 + 64) / 32 * 32;
+    int64_t nflag = 0;
+    for (auto &nd : t->nodes)
+        if (nd.upper >= 0 && nd.kind == 2) nd.flag_off = (nflag++) * fstride;
+    t->flags_bytes = (size_t)(nflag * fstride) * 4;
+    size_t o_flags = take(std::max<size_t>(t->flags_bytes, 4));
     // metadata region (uploaded with one copy)
     size_t o_meta = off;
     size_t o_desc = take((size_t)std::max(ncomb, 1) * sizeof(CombineDesc));
@@ -943,6 +955,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     t->d_leaf_nodes = (int32_t *)(A + o_lnodes);
     t->d_leaf_rows = (int32_t *)(A + o_lrows);
     t->d_vnodes = (int32_t *)(A + o_vnodes);
+    t->d_flags = (int32_t *)(A + o_flags);
 
     // ---- host-side metadata: level plan, descriptors, walk nodes ----
     const size_t meta_bytes = meta_end - o_meta;
@@ -1017,6 +1030,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     t->h2d_bytes = (int64_t)meta_bytes + (rows_dev ? 0 : B * t->m_slab) + (cols_dev ? 0 : B * n);
     // a pageable fallback copy is staged synchronously, so `meta_fallback` may die
     BCK(cudaMemsetAsync(t->d_node_wstar, 0, (size_t)nn * 4, s));
+    if (t->flags_bytes) BCK(cudaMemsetAsync(t->d_flags, 0, t->flags_bytes, s));
     BCKL(launch_nx(t->d_cols, (int32_t)n, npairs, t->d_nx, t->d_sym_wstar, s));
     BCKL(launch_leaf_wstar(t->d_rows, t->d_leaf_nodes, t->d_leaf_rows, t->nleaves,
                            (int32_t)std::max<int64_t>(t->m_slab, 1), t->d_sym_wstar,
@@ -1066,6 +1080,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
                     // a kind-2 child's events are a by-product of its own sweep
                     d.U_ev_make = (kind == 2 && sweep_on && un.kind != 2) ? 1 : 0;
                     d.pad_ = 0;
+                    d.blk_flags = nd.flag_off >= 0 ? t->d_flags + nd.flag_off : nullptr;
                     if (d.U_ev_make) ev_make_any = true;
                 }
                 maxk = std::max(maxk, t->nodes[nd.upper].w1 - 1);

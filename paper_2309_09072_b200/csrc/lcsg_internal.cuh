@@ -55,6 +55,7 @@ struct CombineDesc {
     int32_t *out_ev;
     int32_t U_ev_make;
     int32_t pad_;
+    int32_t *blk_flags;  // per block of rows: 1 = redo with the generic sweep kernel (zeroed per solve)
 };
 
 // Resolved accessor of a table inside a kernel.
@@ -193,8 +194,8 @@ int launch_finalize_rows(const CombineDesc *descs, int32_t ndesc, Ctx c, int32_t
 // row-sweep path (lcsg_sweep.cu): events of the upper children that need them,
 // then the interior rows of blocks of S rows below each skeleton row
 int launch_table_events(const CombineDesc *descs, int32_t ndesc, Ctx c, cudaStream_t s);
-int launch_sweep(const CombineDesc *descs, int32_t ndesc, Ctx c, int32_t S, int32_t maxw1,
-                 cudaStream_t s);
+int launch_sweep(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64, int32_t S,
+                 int32_t maxw1, cudaStream_t s);
 int sweep_error_count(int32_t *count, bool reset);
 int launch_walk_level(const WalkNode *nodes, const int32_t *ids, int32_t count, Ctx c,
                       int32_t *wi, int32_t *wj, int32_t *cols_out, bool retrace, int key_shift,

@@ -12,9 +12,11 @@
 //     insertion rank ju1 (trace[c][j] > ju1): value and trace unchanged;
 //   * cells left of the insertion: value = C[c][j+1], trace = trace[c][j+1]-1
 //     (while that trace is >= 1);
+//     (a zero trace stays zero: k = 0 still reaches the value through L's own
+//     shift);
 //   * only the cells between (j1 <= j <= J, J = last j with trace[c][j] <= ju1)
-//     and a short zero-trace prefix need candidates evaluated, each over a
-//     split range bounded by ju1 below and by its right neighbour's split above.
+//     need candidates evaluated, each over a split range bounded by ju1 below
+//     and by its right neighbour's split above.
 // So a row costs a handful of L gathers (one warp) plus a streaming rewrite of
 // the row -- the kernel is bound by the 8 B per cell it writes, not by
 // per-cell searches.  The chain over rows is cut by the skeleton rows
@@ -40,6 +42,14 @@ namespace lcsg {
 // failed one of the structural invariants; tests read it through
 // lcsg_sweep_errors and fail loudly)
 __device__ int32_t g_sweep_err = 0;
+#ifdef LCSG_SWEEP_STATS
+// per launch-size class (log2 of group threads - 5): steps, main rounds, walk cells,
+// splits per cell, zero-run evaluations, zero-run rounds, case A, zero-run length
+__device__ unsigned long long g_sweep_stat[8][8];
+#define SW_STAT(cls, idx, val) atomicAdd(&g_sweep_stat[cls][idx], (unsigned long long)(val))
+#else
+#define SW_STAT(cls, idx, val) do {} while (0)
+#endif
 
 namespace {
 
@@ -113,11 +123,10 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // (insertion rank, kmax, the U entries from the rank on) are fetched a step
 // ahead with cp.async.
 __global__ void sweep_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int32_t S,
-                             int32_t nblk, int32_t cap) {
+                             int32_t nblk, int32_t cap, int flagged_only) {
     extern __shared__ int32_t ssm[];  // R0[cap] T0[cap] R1[cap] T1[cap] evs[S] kms[S]
     __shared__ unsigned long long cellkey[2][SW_MAXQ];
     __shared__ int32_t useg[2][SW_SEG];
-    __shared__ int32_t s0ctl[2];
     const int32_t di = (int32_t)(blockIdx.z * 65535u + blockIdx.y);
     if (di >= ndesc) return;
     const int32_t blk = blockIdx.x;
@@ -126,6 +135,7 @@ __global__ void sweep_kernel(const CombineDesc *__restrict__ descs, int32_t ndes
     const int32_t n = c.n, inf = c.inf;
     const int32_t a = blk * S;
     if (a >= n) return;
+    if (flagged_only && !d.blk_flags[blk]) return;  // the register kernel did this block
     const int32_t nsteps = min(S, n - a);  // rows a+1 .. a+nsteps; the last one is a skeleton row
     const int32_t w1 = d.w1, uw1 = d.U.w1, lw1 = d.L.w1, wl = lw1 - 1;
     const int32_t *__restrict__ Ur = d.U.reach;
@@ -246,56 +256,6 @@ __global__ void sweep_kernel(const CombineDesc *__restrict__ descs, int32_t ndes
         const int32_t Knew = nv < inf ? K : K - 1;
         if (tid == 0) out_ev[cr] = j1;
         if (!dowrite) break;
-        // zero-split prefix of the shifted cells: trace 0 unless the right
-        // neighbour's split is positive, then the first k reaching the value
-        int32_t s0lo = 0, s0hi = -1;
-        {
-            const int32_t J0 = warp_last_le(oT, K, 0, lane);
-            int32_t js = min(j1, J0) - 1;
-            int32_t ub = 0;
-            if (js >= 0) {
-                ub = js + 1 == j1 ? (nv < inf ? nk : INT_MAX) : oT[js + 2] - 1;
-                ub = min(ub, kmU);
-            }
-            if (js >= 1 && ub > 0) {  // rare: warp 0 scans, right to left
-                if (tid < 32) {
-                    const int32_t hi0 = js;
-                    while (js >= 0 && ub > 0) {
-                        const int32_t target = oR[js + 1];
-                        const int32_t klo = max(0, js - wl), khi = min(ub, js);
-                        if (khi <= 0) break;  // js == 0: trace 0 (the default rule)
-                        int32_t found = -1;
-                        for (int32_t kb = klo; kb <= khi && found < 0; kb += 32) {
-                            const int32_t k = kb + lane;
-                            bool hit = false;
-                            if (k <= khi) {
-                                const int32_t x = Uc[k];
-                                hit = Lr[(size_t)(x - 1) * lw1 + (js - k)] == target;
-                            }
-                            const unsigned b = __ballot_sync(FULL, hit);
-                            if (b) found = kb + __ffs(b) - 1;
-                        }
-                        if (found < 0) {
-                            if (lane == 0) atomicAdd(&g_sweep_err, 1);
-                            found = 0;
-                        }
-                        if (lane == 0) {
-                            nR[js] = target;
-                            nT[js] = found;
-                        }
-                        ub = found;
-                        --js;
-                    }
-                    if (lane == 0) {
-                        s0ctl[0] = js + 1;
-                        s0ctl[1] = hi0;
-                    }
-                }
-                __syncthreads();
-                s0lo = s0ctl[0];
-                s0hi = s0ctl[1];
-            }
-        }
         {
             int32_t *gR = out_reach + (size_t)(cr + 1) * w1, *gT = out_trace + (size_t)(cr + 1) * w1;
             for (int32_t j = tid; j < w1; j += nt) {
@@ -305,13 +265,13 @@ __global__ void sweep_kernel(const CombineDesc *__restrict__ descs, int32_t ndes
                         const unsigned long long key = ck[jb - j];
                         v = (int32_t)(key >> 32);
                         t = (int32_t)(uint32_t)key;
-                    } else if ((j > jb && j <= J) || (j >= s0lo && j <= s0hi)) {
+                    } else if (j > jb && j <= J) {  // cells of earlier rounds
                         if (!in_smem) continue;  // already in the output row
                         v = nR[j];
                         t = nT[j];
                     } else if (j < j1) {
                         v = oR[j + 1];
-                        t = max(oT[j + 1] - 1, 0);
+                        t = max(oT[j + 1] - 1, 0);  // a zero split stays zero (k = 0 still wins)
                     } else {
                         v = oR[j];
                         t = oT[j];
@@ -346,6 +306,309 @@ __global__ void sweep_kernel(const CombineDesc *__restrict__ descs, int32_t ndes
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Register-resident sweep (the fast path).  A group of gn threads (one warp,
+// four groups per CTA; or a whole CTA) owns a block of rows; thread gt keeps
+// the cells j = gt + gn * i (i < CPT) of the current row in registers --
+// reach R[i] and split T[i], (INF, INT_MAX) beyond the finite prefix.  Per
+// step: J and the zero-split prefix come from per-thread counts (the splits
+// are nondecreasing along a row); the few cells around J are published to a
+// shared window; all threads evaluate the (cell, split) pairs of the walk at
+// once (keys reduce with shared-memory atomicMin); every warp reads off j1;
+// the row is rewritten in registers (neighbour cell by shuffle) and stored.
+// Anything outside the fast path's bounds (finite prefix wider than gn * CPT,
+// walks / zero-split runs longer than the patch arrays, a broken invariant)
+// flags the block; the generic kernel above then redoes flagged blocks.
+// ---------------------------------------------------------------------------
+constexpr int RG_SEG = 32;   // prefetched U entries from the insertion rank on
+constexpr int RG_MAXS = 64;  // rows per block
+constexpr uint32_t K32_NONE = 0xffffffffu;
+
+// CKN: evaluated cells per step kept as keys (bounds the walk and the
+// zero-split run)
+template <int CKN>
+struct RegGroupSm {
+    uint32_t ck[2][CKN];   // walk cells: key of cell j at [J - j]
+    int32_t useg[2][RG_SEG];
+    int32_t evs[RG_MAXS], kms[RG_MAXS];
+    int32_t cnt[2][4];     // counts (cA | cZ << 16), min split > ju1, min split > 0, j1
+    int32_t edgeR[2][32], edgeT[2][32];  // first cell of every warp (its left neighbour's neighbour)
+};
+
+template <bool MULTI>
+__device__ __forceinline__ void gsync() {
+    if (MULTI) __syncthreads(); else __syncwarp();
+}
+
+__device__ __forceinline__ int ceil_log2(int32_t x) { return x <= 1 ? 0 : 32 - __clz(x - 1); }
+
+// Cell ownership: warp gw of the group holds the cells [gw*32*CPT, (gw+1)*32*CPT),
+// lane-strided: j = gw*32*CPT + lane + 32*i.  The right neighbour of a cell is
+// the next lane's (same i), or lane 0's cell i+1 -- shuffles only; the warp's
+// very last cell takes the next warp's first cell from shared memory.
+// Keys are 32-bit (value << shift | split): the host routes combines whose
+// keys need 64 bits to the generic kernel.
+//
+// A step costs three group barriers: (A) counts -> J and the split bound
+// right of it (the splits are nondecreasing along a row, so "last cell with
+// split <= x" is a count and "split of the next cell" a minimum); (P) all
+// threads evaluate the (cell, split) pairs of the walk left of J (one round of
+// dependent L gathers, 32-bit shared-memory atomicMin per cell); (D) the
+// owners of the walk cells compare the new value with their old one and the
+// largest changed cell is j1.  Longer walks take further rounds (two barriers
+// each).
+template <int CPT, bool MULTI>
+__global__ void __launch_bounds__(MULTI ? 1024 : 128)
+    sweep_reg_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int32_t S,
+                     int32_t nblk, int shift, int64_t ngroups) {
+    constexpr int GPB = MULTI ? 1 : 4;  // groups per CTA
+    constexpr int CKN = MULTI ? 512 : 128;
+    constexpr int QMAX = MULTI ? 256 : 32;  // cells per round
+    using Sm = RegGroupSm<CKN>;
+    __shared__ Sm gsm_all[GPB];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gi = MULTI ? 0 : warp;
+    const int gt = MULTI ? (int)threadIdx.x : lane;
+    const int gn = MULTI ? (int)blockDim.x : 32;
+    const int gw = MULTI ? warp : 0, nw = gn >> 5;
+    const int64_t g = (int64_t)blockIdx.x * GPB + gi;
+    if (g >= ngroups) return;
+    const int32_t di = (int32_t)(g / nblk);
+    const int32_t blk = (int32_t)(g - (int64_t)di * nblk);
+    Sm &sm = gsm_all[gi];
+    const CombineDesc &d = descs[di];
+    const int32_t n = c.n, inf = c.inf;
+    const int32_t a = blk * S;
+    if (a >= n) return;
+    const int32_t nsteps = min(S, n - a);
+    const int32_t w1 = d.w1, uw1 = d.U.w1, lw1 = d.L.w1, wl = lw1 - 1;
+    const int32_t *__restrict__ Ur = d.U.reach;
+    const int32_t *__restrict__ Lr = d.L.reach;
+    int32_t *const out_reach = d.out_reach;
+    int32_t *const out_trace = d.out_trace;
+    int32_t *const out_ev = d.out_ev;
+    int32_t *const flag = d.blk_flags + blk;
+    const int32_t capc = gn * CPT;        // cells held in registers
+    const int32_t wbase = gw * 32 * CPT;  // first cell of this warp
+    const int32_t jl = wbase + lane;      // this thread's cell 0
+    const uint32_t kmask = (1u << shift) - 1u;
+
+    int32_t K = d.out_kmax[a];  // written by the skeleton kernel
+    if (K + 1 > capc) {
+        if (gt == 0) *flag = 1;
+        return;
+    }
+    int32_t R[CPT], T[CPT];
+    {
+        const int32_t *gr = out_reach + (size_t)a * w1, *gtr = out_trace + (size_t)a * w1;
+#pragma unroll
+        for (int i = 0; i < CPT; ++i) {
+            const int32_t j = jl + 32 * i;
+            R[i] = j <= K ? gr[j] : inf;
+            T[i] = j <= K ? gtr[j] : INT_MAX;
+        }
+    }
+    for (int32_t t = gt; t < nsteps; t += gn) {
+        sm.evs[t] = d.U_ev[a + t];
+        sm.kms[t] = d.U.kmax[a + t + 1];
+    }
+    for (int t = gt; t < 2 * CKN; t += gn) sm.ck[0][t] = K32_NONE;
+    if (gt < 8) sm.cnt[0][gt] = (gt & 3) == 0 ? 0 : ((gt & 3) == 3 ? -1 : INT_MAX);
+    gsync<MULTI>();
+    if (gt < RG_SEG) {
+        const int32_t k = sm.evs[0] + gt;
+        if (k <= sm.kms[0]) sm.useg[0][gt] = Ur[(size_t)(a + 1) * uw1 + k];
+    }
+    gsync<MULTI>();
+
+#define RG_FALLBACK()                 \
+    do {                              \
+        if (gt == 0) *flag = 1;       \
+        cp_async_wait_all();          \
+        return;                       \
+    } while (0)
+
+    for (int32_t st = 0; st < nsteps; ++st) {
+        const int par = st & 1;
+        const int32_t cr = a + st;  // row cr -> row cr + 1
+        const bool dowrite = st + 1 < nsteps;
+        const int32_t ju1 = sm.evs[st], kmU = sm.kms[st];
+        const int32_t *Uc = Ur + (size_t)(cr + 1) * uw1;
+        const int32_t *seg = sm.useg[par];
+        uint32_t *ck = sm.ck[par];
+        // ---- A. J and the split bound right of it ----
+        if (MULTI && lane == 0) {
+            sm.edgeR[par][gw] = R[0];
+            sm.edgeT[par][gw] = T[0];
+        }
+        int32_t J, ubR;
+        {
+            int32_t cA = 0, mA = INT_MAX;
+#pragma unroll
+            for (int i = 0; i < CPT; ++i) {
+                const int32_t t = T[i];
+                cA += t <= ju1;
+                mA = t > ju1 ? min(mA, t) : mA;
+            }
+            cA = __reduce_add_sync(FULL, cA);
+            mA = __reduce_min_sync(FULL, mA);
+            if (MULTI) {
+                if (lane == 0) {
+                    atomicAdd(&sm.cnt[par][0], cA);
+                    atomicMin(&sm.cnt[par][1], mA);
+                }
+                __syncthreads();
+                cA = sm.cnt[par][0];
+                mA = sm.cnt[par][1];
+                if (gt < 4) sm.cnt[par ^ 1][gt] = gt == 0 ? 0 : (gt == 3 ? -1 : INT_MAX);
+            }
+            J = cA - 1;
+            ubR = mA;  // split of cell J + 1 (INT_MAX: none)
+        }
+        if (dowrite && gt < RG_SEG) {  // the next step's U entries, a step ahead
+            const int32_t e1 = sm.evs[st + 1], k1 = sm.kms[st + 1];
+            if (e1 + gt <= k1) cp_async4(&sm.useg[par ^ 1][gt], Uc + uw1 + e1 + gt);
+        }
+        // ---- P / D. the walk left of J: evaluate cells until one changes value ----
+        int32_t jb = J, j1 = -1;
+        for (int round = 0;; ++round) {
+            const int32_t ub0 = min(kmU, ubR);
+            const int32_t lmax = ub0 - ju1 + 1;  // splits per cell (before the j clamps)
+            const int lgs = ceil_log2(lmax);
+            const int32_t qwant =
+                round == 0 ? max(4, min(32, (MULTI ? 2 * gn : gn) >> lgs)) : (round == 1 ? 32 : QMAX);
+            const int32_t Qc = min(min(jb + 1, qwant), CKN - (J - jb));
+            if (Qc <= 0) RG_FALLBACK();
+            const int32_t npA = Qc << lgs;
+            for (int32_t p = gt; p < npA; p += gn) {
+                const int32_t q = p >> lgs, r = p & ((1 << lgs) - 1);
+                const int32_t j = jb - q, k = ju1 + r;
+                if (r < lmax && k <= j && j - k <= wl) {
+                    const int32_t x = r < RG_SEG ? seg[r] : Uc[k];  // finite: k <= kmax_U
+                    const int32_t v = Lr[(size_t)(x - 1) * lw1 + (j - k)];
+                    atomicMin(&ck[J - j], ((uint32_t)v << shift) | (uint32_t)k);
+                }
+            }
+            gsync<MULTI>();
+            // owners: the largest walk cell whose value changed
+            const int32_t lo = jb - Qc + 1;
+            int32_t found = -1;
+            if (Qc <= 32) {  // at most one cell per thread
+                const int32_t i0 = lo > jl ? (lo - jl + 31) >> 5 : 0;
+                const int32_t j0 = jl + 32 * i0;
+                if (i0 < CPT && j0 <= jb) {
+                    int32_t r = inf;
+#pragma unroll
+                    for (int i = 0; i < CPT; ++i)
+                        if (i == i0) r = R[i];
+                    const uint32_t key = ck[J - j0];
+                    const int32_t v = (int32_t)(key >> shift);
+                    if (!(key != K32_NONE && v < inf && v == r)) found = j0;
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < CPT; ++i) {
+                    const int32_t j = jl + 32 * i;
+                    if (j >= lo && j <= jb) {
+                        const uint32_t key = ck[J - j];
+                        const int32_t v = (int32_t)(key >> shift);
+                        if (!(key != K32_NONE && v < inf && v == R[i])) found = max(found, j);
+                    }
+                }
+            }
+            found = __reduce_max_sync(FULL, found);
+            if (MULTI) {
+                if (lane == 0 && found >= 0) atomicMax(&sm.cnt[par][3], found);
+                __syncthreads();
+                found = sm.cnt[par][3];
+            }
+#ifdef LCSG_SWEEP_STATS
+            if (gt == 0) SW_STAT(31 - __clz(gn) - 5, 1, 1);
+#endif
+            if (found >= 0) {
+                j1 = found;
+                break;
+            }
+            // all Qc cells kept their value (new splits): go further left
+            ubR = (int32_t)(ck[J - lo] & kmask);
+            jb = lo - 1;
+            if (jb < 0) RG_FALLBACK();  // cannot happen: cell 0 always changes
+        }
+        const uint32_t newkey = ck[J - j1];
+        const int32_t nv = newkey == K32_NONE ? inf : min((int32_t)(newkey >> shift), inf);
+        const int32_t nk = (int32_t)(newkey & kmask);
+        if (nv >= inf && j1 != K) RG_FALLBACK();
+#ifdef LCSG_SWEEP_STATS
+        if (gt == 0) {
+            const int cls = 31 - __clz(gn) - 5;
+            SW_STAT(cls, 0, 1);
+            SW_STAT(cls, 2, J - j1 + 1);
+            SW_STAT(cls, 3, max(0, min(kmU, ubR) - ju1 + 1));
+        }
+#endif
+        const int32_t Knew = nv < inf ? K : K - 1;
+        if (gt == 0) out_ev[cr] = j1;
+        if (!dowrite) break;
+        // ---- rewrite the row in registers and store it ----
+        {
+            int32_t *gR = out_reach + (size_t)(cr + 1) * w1, *gT = out_trace + (size_t)(cr + 1) * w1;
+            // the next warp's first cell: neighbour of this warp's last cell
+            const int32_t eR = (MULTI && gw + 1 < nw) ? sm.edgeR[par][gw + 1] : inf;
+            const int32_t eT = (MULTI && gw + 1 < nw) ? sm.edgeT[par][gw + 1] : INT_MAX;
+#pragma unroll
+            for (int i = 0; i < CPT; ++i) {
+                const int32_t cb = wbase + 32 * i;  // this warp's cells cb .. cb+31 (warp-uniform)
+                const int32_t j = cb + lane;
+                if (cb > Knew) {  // all INF
+                    R[i] = inf;
+                    T[i] = INT_MAX;
+                    if (j < w1) gR[j] = inf;
+                    continue;
+                }
+                if (cb > J && cb + 31 <= Knew) {  // all unchanged
+                    if (j < w1) {
+                        gR[j] = R[i];
+                        gT[j] = T[i];
+                    }
+                    continue;
+                }
+                int32_t v = R[i], t = T[i];
+                if (cb < j1) {  // some shifted cells: the right neighbour's old cell
+                    const int32_t ra = __shfl_down_sync(FULL, R[i], 1), ta = __shfl_down_sync(FULL, T[i], 1);
+                    const int32_t rb = __shfl_sync(FULL, i + 1 < CPT ? R[i + 1 < CPT ? i + 1 : i] : eR, 0);
+                    const int32_t tb = __shfl_sync(FULL, i + 1 < CPT ? T[i + 1 < CPT ? i + 1 : i] : eT, 0);
+                    if (j < j1) {
+                        v = lane == 31 ? rb : ra;
+                        t = max((lane == 31 ? tb : ta) - 1, 0);  // a zero split stays zero (k = 0 still wins)
+                    }
+                }
+                if (j >= j1 && j <= J) {
+                    const uint32_t key = ck[J - j];
+                    v = (int32_t)(key >> shift);
+                    t = (int32_t)(key & kmask);
+                }
+                if (j > Knew) {
+                    v = inf;
+                    t = INT_MAX;
+                }
+                R[i] = v;
+                T[i] = t;
+                if (j < w1) {
+                    gR[j] = v;
+                    if (j <= Knew) gT[j] = t;
+                }
+            }
+            for (int32_t j = capc + gt; j < w1; j += gn) gR[j] = inf;
+            K = Knew;
+        }
+        for (int t = gt; t < CKN; t += gn) sm.ck[par ^ 1][t] = K32_NONE;
+        cp_async_wait_all();
+        if (!MULTI) __syncwarp();
+    }
+#undef RG_FALLBACK
+}
+
 }  // namespace
 
 int launch_table_events(const CombineDesc *descs, int32_t ndesc, Ctx c, cudaStream_t s) {
@@ -357,25 +620,52 @@ int launch_table_events(const CombineDesc *descs, int32_t ndesc, Ctx c, cudaStre
     return 0;
 }
 
-int launch_sweep(const CombineDesc *descs, int32_t ndesc, Ctx c, int32_t S, int32_t maxw1,
-                 cudaStream_t s) {
+int launch_sweep(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64, int32_t S,
+                 int32_t maxw1, cudaStream_t s) {
     if (ndesc <= 0 || c.n <= 0) return 0;
     if (S > 1024) return (int)cudaErrorInvalidValue;
     const int32_t nblk = (c.n + S - 1) / S;
-    static int cap_max = 0, cpt = 0;
+    static int cap_max = 0, cpt = 0, use_reg = 1, one_warp_max = 0;
     if (!cap_max) {
         const char *e = getenv("LCSG_SWEEP_CAP");
         cap_max = e ? atoi(e) : 12800;
         const char *e2 = getenv("LCSG_SWEEP_CPT");
         cpt = e2 ? std::max(1, atoi(e2)) : 8;
+        const char *e3 = getenv("LCSG_SWEEP_REG");
+        use_reg = e3 ? atoi(e3) : 1;
+        const char *e4 = getenv("LCSG_SWEEP_ONE_WARP_MAXW1");
+        one_warp_max = e4 ? atoi(e4) : 544;
         cudaFuncSetAttribute(sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * cap_max + 8 * 1024);
+    }
+    // register-resident fast path: one warp per block of rows up to 32 * 17
+    // cells, else a CTA of 9 cells per thread (a finite prefix beyond 1024 * 9
+    // cells flags the block for the generic kernel)
+    const bool reg = use_reg && S <= RG_MAXS && !key64 && shift < 32;
+    if (reg) {
+        const int64_t ngroups = (int64_t)ndesc * nblk;
+        if (maxw1 <= one_warp_max && maxw1 <= 32 * 17) {
+            const unsigned nb = (unsigned)((ngroups + 3) / 4);
+            if (maxw1 <= 32 * 5)
+                sweep_reg_kernel<5, false><<<nb, 128, 0, s>>>(descs, ndesc, c, S, nblk, shift, ngroups);
+            else if (maxw1 <= 32 * 9)
+                sweep_reg_kernel<9, false><<<nb, 128, 0, s>>>(descs, ndesc, c, S, nblk, shift, ngroups);
+            else
+                sweep_reg_kernel<17, false><<<nb, 128, 0, s>>>(descs, ndesc, c, S, nblk, shift, ngroups);
+        } else {
+            int lg = 6;
+            while (lg < 10 && (9 << lg) < maxw1) ++lg;
+            sweep_reg_kernel<9, true><<<(unsigned)ngroups, 1 << lg, 0, s>>>(descs, ndesc, c, S, nblk,
+                                                                           shift, ngroups);
+        }
+        LCSG_LAUNCH_CHECK();
     }
     const int32_t cap = std::min(maxw1 + 1, cap_max);
     int nt = 32;
     while (nt < 1024 && nt * cpt < maxw1) nt *= 2;
     const dim3 blocks((unsigned)nblk, (unsigned)std::min<int32_t>(ndesc, 65535),
                       (unsigned)((ndesc + 65534) / 65535));
-    sweep_kernel<<<blocks, nt, (size_t)16 * cap + (size_t)8 * S, s>>>(descs, ndesc, c, S, nblk, cap);
+    sweep_kernel<<<blocks, nt, (size_t)16 * cap + (size_t)8 * S, s>>>(descs, ndesc, c, S, nblk, cap,
+                                                                      reg ? 1 : 0);
     LCSG_LAUNCH_CHECK();
     return 0;
 }
@@ -391,6 +681,12 @@ int sweep_error_count(int32_t *count, bool reset) {
 }
 
 }  // namespace lcsg
+
+#ifdef LCSG_SWEEP_STATS
+extern "C" int lcsg_sweep_stats(unsigned long long *out) {
+    return (int)cudaMemcpyFromSymbol(out, lcsg::g_sweep_stat, sizeof(unsigned long long) * 64);
+}
+#endif
 
 extern "C" int lcsg_sweep_errors(int device, int32_t *count, int reset) {
     if (!count) return -1;
