@@ -325,7 +325,8 @@ int launch_plan_entry(lcsg_tree_s *t, const LaunchH &L, cudaStream_t s) {
     if (L.kind == 7)
         return launch_block_refine(dd, L.count, c, L.shift, L.key64, L.stride_or_delta,
                                    L.wpr_log2, L.ustride, s);
-    if (L.kind == 8) return launch_finalize_rows(dd, L.count, c, L.stride_or_delta, s, L.ustride);
+    if (L.kind == 8)
+        return launch_finalize_rows(dd, L.count, c, L.stride_or_delta, s, L.ustride, L.wpr_log2 != 0);
     if (L.kind == 12) return launch_table_events(dd, L.count, c, s);
     if (L.kind == 13)
         return launch_sweep(dd, L.count, c, L.shift, L.key64, L.stride_or_delta, L.ustride, s);
@@ -1151,6 +1152,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
                 F.kind = 8;
                 F.stride_or_delta = S;
                 F.ustride = maxw1;
+                F.wpr_log2 = 1;  // kmax is the sweep's
                 t->plan.push_back(F);
                 continue;
             }

@@ -190,7 +190,7 @@ int launch_block_refine(const CombineDesc *descs, int32_t ndesc, Ctx c, int shif
                         int32_t S, int32_t rs, int32_t maxw1, cudaStream_t s);
 // INF suffix + kmax/wstar of the interior rows after the tiled refinement
 int launch_finalize_rows(const CombineDesc *descs, int32_t ndesc, Ctx c, int32_t S,
-                         cudaStream_t s, int32_t maxw1);
+                         cudaStream_t s, int32_t maxw1, bool pre = false);
 // row-sweep path (lcsg_sweep.cu): events of the upper children that need them,
 // then the interior rows of blocks of S rows below each skeleton row
 int launch_table_events(const CombineDesc *descs, int32_t ndesc, Ctx c, cudaStream_t s);

@@ -283,9 +283,10 @@ __global__ void sweep_kernel(const CombineDesc *__restrict__ descs, int32_t ndes
                     gR[j] = v;
                     gT[j] = t;
                 } else {
-                    gR[j] = inf;  // INF suffix: traces are finalize's
+                    gR[j] = inf;  // INF suffix: its traces are the finalize kernel's
                 }
             }
+            if (tid == 0) d.out_kmax[cr + 1] = Knew;
             K = Knew;
         }
         for (int t = tid; t < SW_MAXQ; t += nt) cellkey[(st + 1) & 1][t] = KEY_NONE;
@@ -322,7 +323,7 @@ __global__ void sweep_kernel(const CombineDesc *__restrict__ descs, int32_t ndes
 // flags the block; the generic kernel above then redoes flagged blocks.
 // ---------------------------------------------------------------------------
 constexpr int RG_SEG = 32;   // prefetched U entries from the insertion rank on
-constexpr int RG_MAXS = 64;  // rows per block
+constexpr int RG_MAXS = 128;  // rows per block
 constexpr uint32_t K32_NONE = 0xffffffffu;
 
 // CKN: evaluated cells per step kept as keys (bounds the walk and the
@@ -389,6 +390,7 @@ __global__ void __launch_bounds__(MULTI ? 1024 : 128)
     int32_t *const out_trace = d.out_trace;
     int32_t *const out_ev = d.out_ev;
     int32_t *const flag = d.blk_flags + blk;
+    int32_t *const out_kmax = d.out_kmax;
     const int32_t capc = gn * CPT;        // cells held in registers
     const int32_t wbase = gw * 32 * CPT;  // first cell of this warp
     const int32_t jl = wbase + lane;      // this thread's cell 0
@@ -429,6 +431,7 @@ __global__ void __launch_bounds__(MULTI ? 1024 : 128)
         return;                       \
     } while (0)
 
+    int32_t dirty_other = 0;  // key slots of the other buffer that are in use
     for (int32_t st = 0; st < nsteps; ++st) {
         const int par = st & 1;
         const int32_t cr = a + st;  // row cr -> row cr + 1
@@ -471,7 +474,7 @@ __global__ void __launch_bounds__(MULTI ? 1024 : 128)
             if (e1 + gt <= k1) cp_async4(&sm.useg[par ^ 1][gt], Uc + uw1 + e1 + gt);
         }
         // ---- P / D. the walk left of J: evaluate cells until one changes value ----
-        int32_t jb = J, j1 = -1;
+        int32_t jb = J, j1 = -1, dirty_this = 0;
         for (int round = 0;; ++round) {
             const int32_t ub0 = min(kmU, ubR);
             const int32_t lmax = ub0 - ju1 + 1;  // splits per cell (before the j clamps)
@@ -493,6 +496,7 @@ __global__ void __launch_bounds__(MULTI ? 1024 : 128)
             gsync<MULTI>();
             // owners: the largest walk cell whose value changed
             const int32_t lo = jb - Qc + 1;
+            dirty_this = J - lo + 1;  // key slots [0, J - lo] are in use
             int32_t found = -1;
             if (Qc <= 32) {  // at most one cell per thread
                 const int32_t i0 = lo > jl ? (lo - jl + 31) >> 5 : 0;
@@ -560,12 +564,7 @@ __global__ void __launch_bounds__(MULTI ? 1024 : 128)
             for (int i = 0; i < CPT; ++i) {
                 const int32_t cb = wbase + 32 * i;  // this warp's cells cb .. cb+31 (warp-uniform)
                 const int32_t j = cb + lane;
-                if (cb > Knew) {  // all INF
-                    R[i] = inf;
-                    T[i] = INT_MAX;
-                    if (j < w1) gR[j] = inf;
-                    continue;
-                }
+                if (cb > K) continue;  // already (INF, none): the tail loop stores the INF cells
                 if (cb > J && cb + 31 <= Knew) {  // all unchanged
                     if (j < w1) {
                         gR[j] = R[i];
@@ -594,15 +593,33 @@ __global__ void __launch_bounds__(MULTI ? 1024 : 128)
                 }
                 R[i] = v;
                 T[i] = t;
-                if (j < w1) {
+                if (j <= Knew) {
                     gR[j] = v;
-                    if (j <= Knew) gT[j] = t;
+                    gT[j] = t;
                 }
             }
-            for (int32_t j = capc + gt; j < w1; j += gn) gR[j] = inf;
+            // INF suffix (Knew, w1) of the reach row; its traces (the Alg. 1 replay's
+            // and the zeros beyond colhi) are written by the finalize kernel from kmax
+            if (gt == 0) out_kmax[cr + 1] = Knew;
+            if (!MULTI) {
+                for (int32_t j = Knew + 1 + gt; j < w1; j += 32) gR[j] = inf;
+            } else {  // scalar stores up to a 16-byte boundary, then int4
+                const int32_t j0 = Knew + 1;
+                const int32_t head = (int32_t)((4 - ((((size_t)(cr + 1) * w1 + j0)) & 3)) & 3);
+                const int32_t jv = min(j0 + head, w1);  // first aligned cell
+                if (gt < jv - j0) gR[j0 + gt] = inf;
+                const int32_t nv4 = (w1 - jv) >> 2;
+                int4 *g4 = reinterpret_cast<int4 *>(gR + jv);
+                const int4 inf4 = make_int4(inf, inf, inf, inf);
+                for (int32_t q = gt; q < nv4; q += gn) g4[q] = inf4;
+                const int32_t jt = jv + 4 * nv4;
+                if (gt < w1 - jt) gR[jt + gt] = inf;
+            }
             K = Knew;
         }
-        for (int t = gt; t < CKN; t += gn) sm.ck[par ^ 1][t] = K32_NONE;
+        // keys used two steps ago live in the other buffer: clear them for the next step
+        for (int t = gt; t < dirty_other; t += gn) sm.ck[par ^ 1][t] = K32_NONE;
+        dirty_other = dirty_this;
         cp_async_wait_all();
         if (!MULTI) __syncwarp();
     }
@@ -652,8 +669,15 @@ int launch_sweep(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool
             else
                 sweep_reg_kernel<17, false><<<nb, 128, 0, s>>>(descs, ndesc, c, S, nblk, shift, ngroups);
         } else {
+            static int lg_max = 0;
+            if (!lg_max) {
+                const char *e5 = getenv("LCSG_SWEEP_GN_MAX");
+                int v = e5 ? atoi(e5) : 1024;
+                lg_max = 6;
+                while (lg_max < 10 && (1 << (lg_max + 1)) <= v) ++lg_max;
+            }
             int lg = 6;
-            while (lg < 10 && (9 << lg) < maxw1) ++lg;
+            while (lg < lg_max && (9 << lg) < maxw1) ++lg;
             sweep_reg_kernel<9, true><<<(unsigned)ngroups, 1 << lg, 0, s>>>(descs, ndesc, c, S, nblk,
                                                                            shift, ngroups);
         }

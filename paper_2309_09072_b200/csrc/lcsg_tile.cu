@@ -512,7 +512,9 @@ __global__ void __launch_bounds__(CR_THREADS)
 template <int FN_MAXSEG>
 __global__ void __launch_bounds__(32 * FN_WARPS)
     finalize_rows_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int32_t S,
-                         int rpw) {
+                         int rpw, int pre) {
+    // pre != 0 (after the row sweep, lcsg_sweep.cu): kmax of every interior row
+    // is already written -- the replay runs on kmax alone (no reach probes)
     __shared__ int2 seg_all[FN_WARPS][32][FN_MAXSEG];
     __shared__ int nseg_all[FN_WARPS][32];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -544,12 +546,13 @@ __global__ void __launch_bounds__(32 * FN_WARPS)
         // mids are the INF nodes (their segments) and go left; K = left - 1
         int32_t left = 0, right = colhi, fm = -1;
         int ns = 0;
+        const int32_t Kpre = pre ? out_kmax[i] : -1;
         // common at the lower levels: the whole [0, colhi] is finite, every
         // mid goes right and there is no INF node (fm is then unused)
-        if (__ldg(reach + colhi) < inf) left = colhi + 1;
+        if (pre ? Kpre >= colhi : __ldg(reach + colhi) < inf) left = colhi + 1;
         while (right >= left) {
             const int32_t mid = (left + right + 1) >> 1;
-            if (__ldg(reach + mid) < inf) {
+            if (pre ? mid <= Kpre : __ldg(reach + mid) < inf) {
                 fm = mid;
                 left = mid + 1;
             } else {
@@ -558,7 +561,7 @@ __global__ void __launch_bounds__(32 * FN_WARPS)
             }
         }
         K = left - 1;
-        out_kmax[i] = K;
+        if (!pre) out_kmax[i] = K;
         for (int s = 0; s < ns; ++s) {  // resolve tops (independent loads)
             const int32_t f = seg_all[wid][lane][s].y;
             seg_all[wid][lane][s].y = f >= 0 ? __ldg(trace + f) : 0;
@@ -676,7 +679,7 @@ int launch_block_refine(const CombineDesc *descs, int32_t ndesc, Ctx c, int shif
 }
 
 int launch_finalize_rows(const CombineDesc *descs, int32_t ndesc, Ctx c, int32_t S,
-                         cudaStream_t s, int32_t maxw1) {
+                         cudaStream_t s, int32_t maxw1, bool pre) {
     if (ndesc <= 0) return 0;
     const int64_t n1 = (int64_t)c.n + 1;
     const int rpw = maxw1 <= 512 ? 32 : (maxw1 <= 2048 ? 8 : (maxw1 <= 8192 ? 2 : 1));
@@ -691,10 +694,10 @@ int launch_finalize_rows(const CombineDesc *descs, int32_t ndesc, Ctx c, int32_t
         const char *e = getenv("LCSG_FIN_CARVEOUT");
         cudaFuncSetAttribute(finalize_rows_kernel<18>, cudaFuncAttributePreferredSharedMemoryCarveout,
                              e ? atoi(e) : 75);
-        finalize_rows_kernel<18><<<blocks, 32 * FN_WARPS, 0, s>>>(descs, ndesc, c, S, rpw);
+        finalize_rows_kernel<18><<<blocks, 32 * FN_WARPS, 0, s>>>(descs, ndesc, c, S, rpw, pre ? 1 : 0);
     }
     else
-        finalize_rows_kernel<34><<<blocks, 32 * FN_WARPS, 0, s>>>(descs, ndesc, c, S, rpw);
+        finalize_rows_kernel<34><<<blocks, 32 * FN_WARPS, 0, s>>>(descs, ndesc, c, S, rpw, pre ? 1 : 0);
     LCSG_LAUNCH_CHECK();
     return 0;
 }
