@@ -182,6 +182,11 @@ int lcsg_probe_int32_rate(int device, double *mins_per_s, int32_t *sm_count, dou
  * invariants it relies on; non-zero means a result may be wrong).  `reset`
  * non-zero clears the counter after reading. */
 int lcsg_sweep_errors(int device, int32_t *count, int reset);
+/* Path counters of the row-sweep kernels on `device` since the last reset:
+ * blocks of rows redone by the generic kernel after the register-resident
+ * kernel flagged them, and blocks swept with the row state kept in the output
+ * rows (finite prefix wider than the shared-memory capacity). */
+int lcsg_sweep_paths(int device, int64_t *redone_blocks, int64_t *global_state_blocks, int reset);
 
 #ifdef __cplusplus
 }

@@ -24,6 +24,7 @@ from .solver import (
     lcs_batch,
     reserve,
     sweep_errors,
+    sweep_paths,
     trim,
     lcs_many,
     recover_cross_vertices,
@@ -46,6 +47,7 @@ __all__ = [
     "lcs_batch",
     "reserve",
     "sweep_errors",
+    "sweep_paths",
     "trim",
     "lcs_many",
     "match_positions",

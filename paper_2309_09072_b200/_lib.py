@@ -85,6 +85,8 @@ SIGNATURES = {
                                          _vp, _i32, _i32, _i64, _i64, _i64, _vp]),
     "lcsg_recover_from": (ctypes.c_int, [_vp, _i32, _i32, _vp]),
     "lcsg_sweep_errors": (ctypes.c_int, [ctypes.c_int, _i32p, ctypes.c_int]),
+    "lcsg_sweep_paths": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
+                                        ctypes.c_int]),
     "lcsg_probe_int32_rate": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_double),
                                              _i32p, ctypes.POINTER(ctypes.c_double)]),
     "lcsg_stats": (ctypes.c_int, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_double),

@@ -153,6 +153,13 @@ int default_skeleton_stride(int64_t n1) {
     return n1 <= 2049 ? 8 : n1 <= 4097 ? 16 : n1 <= 8193 ? 32 : 64;
 }
 int default_col_block(int64_t n1) { return n1 <= 4097 ? 4 : 8; }
+// Rows per block of the row sweep (= its skeleton stride): a block is a
+// sequential chain of row steps, so short strings (few blocks per level)
+// need short chains (measured: cfg1 256^2 stride 4 0.20 ms vs 64 0.44; cfg2
+// 2048^2 8 0.81 vs 1.89; cfg3 4096^2 16 1.51 vs 2.14; cfg4/cfg5 32..64 equal)
+int default_sweep_stride(int64_t n1) {
+    return n1 <= 513 ? 4 : n1 <= 2049 ? 8 : n1 <= 4097 ? 16 : n1 <= 8193 ? 32 : 64;
+}
 
 struct NodeH {
     int32_t top_row, bottom_row, w1, upper, lower, height, depth, leaf_row;
@@ -789,7 +796,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     // wide combines: row sweep below the skeleton rows (LCSG_SWEEP=0: the
     // column-refinement stages)
     const bool sweep_on = env_int("LCSG_SWEEP", 1) != 0;
-    const int sweep_stride = std::max(2, env_int("LCSG_SWEEP_STRIDE", 64));
+    const int sweep_stride = std::max(2, env_int("LCSG_SWEEP_STRIDE", default_sweep_stride(n + 1)));
     // block size (local rows) of each column-refinement stage, power of two
     int col_block = 1;
     while (col_block * 2 <= std::min(16, std::max(2, env_int("LCSG_COL_BLOCK", default_col_block(n1)))))

@@ -42,6 +42,10 @@ namespace lcsg {
 // failed one of the structural invariants; tests read it through
 // lcsg_sweep_errors and fail loudly)
 __device__ int32_t g_sweep_err = 0;
+// path counters (tests assert the fallback paths really run): blocks redone by
+// the generic kernel after a register-kernel flag, blocks swept with the row
+// state in the output rows (finite prefix beyond the shared-memory capacity)
+__device__ unsigned long long g_sweep_paths[2];
 #ifdef LCSG_SWEEP_STATS
 // per launch-size class (log2 of group threads - 5): steps, main rounds, walk cells,
 // splits per cell, zero-run evaluations, zero-run rounds, case A, zero-run length
@@ -147,6 +151,10 @@ __global__ void sweep_kernel(const CombineDesc *__restrict__ descs, int32_t ndes
 
     int32_t K = d.out_kmax[a];  // written by the skeleton kernel
     const bool in_smem = K + 2 <= cap;
+    if (tid == 0) {
+        if (flagged_only) atomicAdd(&g_sweep_paths[0], 1ull);
+        if (!in_smem) atomicAdd(&g_sweep_paths[1], 1ull);
+    }
     // row state: old = row c, new = row c+1
     int32_t *oR, *oT, *nR, *nT;
     if (in_smem) {
@@ -230,12 +238,13 @@ __global__ void sweep_kernel(const CombineDesc *__restrict__ descs, int32_t ndes
             }
             // all Qc cells kept their value (new splits): store them, go further left
             ubR = (int32_t)(uint32_t)ck[Qc - 1];
-            if (dowrite && tid < Qc) {
-                nR[jb - tid] = (int32_t)(ck[tid] >> 32);
-                nT[jb - tid] = (int32_t)(uint32_t)ck[tid];
-            }
+            if (dowrite)
+                for (int32_t q = tid; q < Qc; q += nt) {  // a round may hold more cells than threads
+                    nR[jb - q] = (int32_t)(ck[q] >> 32);
+                    nT[jb - q] = (int32_t)(uint32_t)ck[q];
+                }
             __syncthreads();
-            if (tid < Qc) ck[tid] = KEY_NONE;
+            for (int32_t q = tid; q < Qc; q += nt) ck[q] = KEY_NONE;
             __syncthreads();
             jb -= Qc;
             if (jb < 0) {  // cannot happen: cell 0 always changes (c+1 -> c+2)
@@ -642,17 +651,21 @@ int launch_sweep(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool
     if (ndesc <= 0 || c.n <= 0) return 0;
     if (S > 1024) return (int)cudaErrorInvalidValue;
     const int32_t nblk = (c.n + S - 1) / S;
-    static int cap_max = 0, cpt = 0, use_reg = 1, one_warp_max = 0;
-    if (!cap_max) {
-        const char *e = getenv("LCSG_SWEEP_CAP");
-        cap_max = e ? atoi(e) : 12800;
-        const char *e2 = getenv("LCSG_SWEEP_CPT");
-        cpt = e2 ? std::max(1, atoi(e2)) : 8;
-        const char *e3 = getenv("LCSG_SWEEP_REG");
-        use_reg = e3 ? atoi(e3) : 1;
-        const char *e4 = getenv("LCSG_SWEEP_ONE_WARP_MAXW1");
-        one_warp_max = e4 ? atoi(e4) : 544;
-        cudaFuncSetAttribute(sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 16 * cap_max + 8 * 1024);
+    // knobs are read at every launch (tests flip them inside one process)
+    auto env_or = [](const char *name, int def) {
+        const char *e = getenv(name);
+        return e && *e ? atoi(e) : def;
+    };
+    constexpr int CAP_LIMIT = 12800;  // 16 B per cell: 200 KB of shared memory
+    const int cap_max = std::max(4, std::min(CAP_LIMIT, env_or("LCSG_SWEEP_CAP", CAP_LIMIT)));
+    const int cpt = std::max(1, env_or("LCSG_SWEEP_CPT", 8));
+    const int use_reg = env_or("LCSG_SWEEP_REG", 1);
+    const int one_warp_max = env_or("LCSG_SWEEP_ONE_WARP_MAXW1", 544);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             16 * CAP_LIMIT + 8 * 1024);
+        attr_set = true;
     }
     // register-resident fast path: one warp per block of rows up to 32 * 17
     // cells, else a CTA of 9 cells per thread (a finite prefix beyond 1024 * 9
@@ -669,11 +682,9 @@ int launch_sweep(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool
             else
                 sweep_reg_kernel<17, false><<<nb, 128, 0, s>>>(descs, ndesc, c, S, nblk, shift, ngroups);
         } else {
-            static int lg_max = 0;
-            if (!lg_max) {
-                const char *e5 = getenv("LCSG_SWEEP_GN_MAX");
-                int v = e5 ? atoi(e5) : 1024;
-                lg_max = 6;
+            int lg_max = 6;
+            {
+                const int v = env_or("LCSG_SWEEP_GN_MAX", 1024);
                 while (lg_max < 10 && (1 << (lg_max + 1)) <= v) ++lg_max;
             }
             int lg = 6;
@@ -711,6 +722,23 @@ extern "C" int lcsg_sweep_stats(unsigned long long *out) {
     return (int)cudaMemcpyFromSymbol(out, lcsg::g_sweep_stat, sizeof(unsigned long long) * 64);
 }
 #endif
+
+extern "C" int lcsg_sweep_paths(int device, int64_t *redone_blocks, int64_t *global_state_blocks,
+                                int reset) {
+    int prev = 0;
+    if (cudaGetDevice(&prev) != cudaSuccess) return -2;
+    if (cudaSetDevice(device) != cudaSuccess) return -2;
+    unsigned long long v[2] = {0, 0};
+    cudaError_t e = cudaMemcpyFromSymbol(v, lcsg::g_sweep_paths, sizeof(v));
+    if (e == cudaSuccess && reset) {
+        const unsigned long long z[2] = {0, 0};
+        e = cudaMemcpyToSymbol(lcsg::g_sweep_paths, z, sizeof(z));
+    }
+    cudaSetDevice(prev);
+    if (redone_blocks) *redone_blocks = (int64_t)v[0];
+    if (global_state_blocks) *global_state_blocks = (int64_t)v[1];
+    return e == cudaSuccess ? 0 : -2;
+}
 
 extern "C" int lcsg_sweep_errors(int device, int32_t *count, int reset) {
     if (!count) return -1;

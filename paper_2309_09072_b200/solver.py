@@ -297,6 +297,18 @@ def sweep_errors(*, device=None, reset: bool = False) -> int:
     return int(cnt.value)
 
 
+def sweep_paths(*, device=None, reset: bool = False):
+    """(blocks redone by the generic sweep kernel after a register-kernel flag,
+    blocks swept with the row state in the output rows) since the last reset.
+    Diagnostic; no reference counterpart."""
+    import ctypes
+
+    a, b = ctypes.c_int64(0), ctypes.c_int64(0)
+    _lib.check(_lib.load().lcsg_sweep_paths(_device(device), ctypes.byref(a), ctypes.byref(b),
+                                            int(reset)), "sweep_paths")
+    return int(a.value), int(b.value)
+
+
 # cells (m * n * pairs) per batched launch: bounds the batch's HBM arena
 # (~125 B per cell-equivalent with traces at cfg5-like shapes)
 _BATCH_CELLS = 1 << 28

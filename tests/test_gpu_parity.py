@@ -349,12 +349,16 @@ def test_dg_rows_by_definition(cfg):
         np.testing.assert_array_equal(R[i - 1], _dg_row_by_definition(rows, cols, i, R.shape[1]))
 
 
+@pytest.mark.parametrize("sweep", ["0", "1"])
 @pytest.mark.parametrize("stride", [1, 2, 4, 16, 64, 512])
-def test_skeleton_refine_strides(stride, monkeypatch):
-    """The wide-table combine (skeleton rows by exact bisection + refinement
-    passes bounded by neighbouring rows) is bit-exact -- reach, kmax, wstar
-    and every trace cell incl. INF artifacts -- for any skeleton stride."""
+def test_skeleton_refine_strides(stride, sweep, monkeypatch):
+    """The wide-table combine (skeleton rows by exact bisection + the row sweep,
+    or with LCSG_SWEEP=0 the refinement passes bounded by neighbouring rows) is
+    bit-exact -- reach, kmax, wstar and every trace cell incl. INF artifacts --
+    for any skeleton stride."""
+    monkeypatch.setenv("LCSG_SWEEP", sweep)
     monkeypatch.setenv("LCSG_SKELETON_STRIDE", str(stride))
+    monkeypatch.setenv("LCSG_SWEEP_STRIDE", str(max(2, stride)))
     rng = np.random.default_rng(100 + stride)
     for _ in range(12):
         m = int(rng.integers(66, 330))
@@ -383,11 +387,11 @@ def test_skeleton_refine_strides(stride, monkeypatch):
 
 @pytest.mark.parametrize("key64", ["0", "1"])
 @pytest.mark.parametrize("env", [
-    {"LCSG_SKELETON_STRIDE": "64", "LCSG_COL_BLOCK": "8"},   # two stages: step 8, step 1
-    {"LCSG_SKELETON_STRIDE": "32", "LCSG_COL_BLOCK": "4"},   # stages: step 8, 2, 1 (B=4,4,2)
-    {"LCSG_SKELETON_STRIDE": "8", "LCSG_COL_BLOCK": "2"},    # three stages of B=2
-    {"LCSG_SKELETON_STRIDE": "32", "LCSG_COL_BLOCK": "32"},  # one stage of 32 rows
-    {"LCSG_REFINE_PASSES": "1"},                            # one launch per refinement pass
+    {"LCSG_SKELETON_STRIDE": "64", "LCSG_COL_BLOCK": "8", "LCSG_SWEEP": "0"},   # two stages: step 8, step 1
+    {"LCSG_SKELETON_STRIDE": "32", "LCSG_COL_BLOCK": "4", "LCSG_SWEEP": "0"},   # stages: step 8, 2, 1 (B=4,4,2)
+    {"LCSG_SKELETON_STRIDE": "8", "LCSG_COL_BLOCK": "2", "LCSG_SWEEP": "0"},    # three stages of B=2
+    {"LCSG_SKELETON_STRIDE": "32", "LCSG_COL_BLOCK": "32", "LCSG_SWEEP": "0"},  # one stage of 32 rows
+    {"LCSG_REFINE_PASSES": "1", "LCSG_SWEEP": "0"},                            # one launch per refinement pass
     {"LCSG_THREAD_MAX_W1": "3", "LCSG_SKEL_THREAD_MAX_W1": "3", "LCSG_SKEL_WARP_MAX_W1": "9"},
     {"LCSG_SKEL_THREAD_MAX_W1": "1", "LCSG_SKEL_WARP_MAX_W1": "1"},  # CTA kernel for every skeleton row
     {"LCSG_NARROW": "0"},                                   # bisection kernel for the narrow tables
@@ -395,8 +399,8 @@ def test_skeleton_refine_strides(stride, monkeypatch):
     {"LCSG_LEAFPAIR": "0"},                                 # height-1 combines through the staged kernel
     {"LCSG_NARROW": "0", "LCSG_THREAD_MAX_W1": "65"},
     {"LCSG_NARROW32_ROLL": "0"},                            # unrolled-fold narrow<32> kernel
-    {"LCSG_FINE_SC_MAXW1": "0"},                            # runtime block size in the fine kernel
-    {"LCSG_SKELETON_STRIDE": "512", "LCSG_COL_BLOCK": "8"},  # row-step 64 / 8 / 1 stages
+    {"LCSG_FINE_SC_MAXW1": "0", "LCSG_SWEEP": "0"},                            # runtime block size in the fine kernel
+    {"LCSG_SKELETON_STRIDE": "512", "LCSG_COL_BLOCK": "8", "LCSG_SWEEP": "0"},  # row-step 64 / 8 / 1 stages
     {"LCSG_SKEL_WARP_BATCHED": "0"},                        # per-node warp DFS for w1 <= 257 skeletons
     {"LCSG_NARROW_FW": "0"},                                # narrow kernels with a runtime row width
     {"LCSG_VIRTUAL_H1": "0"},                               # height-1 tables materialised (leaf-pair kernel)

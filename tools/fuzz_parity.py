@@ -34,7 +34,12 @@ def pair(m, n, sigma):
     return a, b
 
 
+VERBOSE = os.environ.get("FUZZ_VERBOSE") == "1"
+
+
 def check(a, b, low, what):
+    if VERBOSE:
+        print("case", what, len(a), len(b), low, flush=True)
     got = L.lcs(a, b, low_memory=low)
     exp = O.lcs(a, b)
     assert (got.length, got.subsequence, got.row_positions, got.col_positions) == exp, \
@@ -60,6 +65,8 @@ while time.time() < t_end:
         continue
     if mode < 0.3 and m * n <= 2_000_000:  # a batch of equal-shape pairs
         pairs = [pair(m, n, sigma) for _ in range(int(rng.integers(2, 7)))]
+        if VERBOSE:
+            print("case batch", m, n, len(pairs), low, flush=True)
         got = L.lcs_batch([p[0] for p in pairs], [p[1] for p in pairs], low_memory=low)
         for (a, b), r in zip(pairs, got):
             assert (r.length, r.subsequence, r.row_positions, r.col_positions) == O.lcs(a, b), \
@@ -82,5 +89,7 @@ while time.time() < t_end:
         t = O.OracleTree(a, b)
         assert np.array_equal(tab.reach, t.node(t.root).reach), f"D_G mismatch m={m} n={n}"
         counts["dg"] += 1
+assert L.sweep_errors() == 0, "row-sweep invariant violated"
 print(f"fuzz ok: {sum(v for k, v in counts.items() if k != 'dg')} random solves bit-exact vs "
-      f"the oracle {counts}")
+      f"the oracle {counts}; sweep invariant violations 0, (blocks redone by the generic sweep "
+      f"kernel, blocks with global row state) = {L.sweep_paths()}")
