@@ -367,7 +367,7 @@ int enqueue_build_kernels(lcsg_tree_s *t, cudaStream_t s, int64_t *launches, boo
     for (const LaunchH &L : t->plan) {
         r = launch_plan_entry(t, L, s);
         if (r > 0) return r;
-        if (r == 0) ++nl;
+        if (r == 0) nl += L.kind == 13 ? sweep_launch_count(L.shift, L.key64, L.stride_or_delta) : 1;
     }
     if (events && t->timing && t->ev_ok && (e = cudaEventRecord(t->ev[2], s))) return (int)e;
     if (launches) *launches = nl;
@@ -1207,7 +1207,10 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
                 lease.finish(); destroy(t);
                 return r;
             }
-            if (e == 0) ++t->launches;
+            if (e == 0) {
+                const LaunchH &PL = t->plan[pi];
+                t->launches += PL.kind == 13 ? sweep_launch_count(PL.shift, PL.key64, PL.stride_or_delta) : 1;
+            }
         }
         level_di = di;
         level_plan = t->plan.size();
@@ -1862,8 +1865,15 @@ int lcsg_combine_rows(const int32_t *upper_reach, int32_t wu1, const int32_t *up
         CombineDesc d;
         int32_t wstar_l;
     };
-    Scratch *sc = nullptr;
-    CK(pool_alloc((void **)&sc, sizeof(Scratch), dev, s));
+    // scratch after the descriptor: per-row events of the U window and of the
+    // output, block flags (row sweep)
+    const size_t ev_elems = (size_t)(rows + 63) / 64 * 64;
+    const size_t flag_elems = (size_t)(rows / 2 + 64) / 32 * 32;
+    const size_t sc_head = align_up(sizeof(Scratch));
+    char *scbuf = nullptr;
+    CK(pool_alloc((void **)&scbuf, sc_head + (2 * ev_elems + flag_elems) * 4, dev, s));
+    Scratch *sc = (Scratch *)scbuf;
+    int32_t *sc_ints = (int32_t *)(scbuf + sc_head);
     Scratch hs;
     std::memset(&hs, 0, sizeof(hs));
     // the row window [i_lo, i_hi) is addressed as a table of `rows` rows; L
@@ -1875,8 +1885,13 @@ int lcsg_combine_rows(const int32_t *upper_reach, int32_t wu1, const int32_t *up
     hs.d.out_kmax = out_kmax + i_lo;
     hs.d.out_wstar = out_wstar;
     hs.d.w1 = w1;
+    hs.d.U_ev = sc_ints;
+    hs.d.out_ev = sc_ints + ev_elems;
+    hs.d.blk_flags = sc_ints + 2 * ev_elems;
+    hs.d.U_ev_make = 1;
     hs.wstar_l = lower_wstar;
     CK(cudaMemcpyAsync(sc, &hs, sizeof(hs), cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(sc_ints + 2 * ev_elems, 0, flag_elems * 4, s));
     Ctx c;
     c.rows = nullptr;
     c.nx = nullptr;
@@ -1885,8 +1900,11 @@ int lcsg_combine_rows(const int32_t *upper_reach, int32_t wu1, const int32_t *up
     const int shift = bits_for(wu1 - 1);
     const bool key64 = need_key64(bits_for(inf), shift);
     const int thread_max_w1 = env_int("LCSG_THREAD_MAX_W1", 65);
+    const bool sweep_on = env_int("LCSG_SWEEP", 1) != 0;
     int S = 1;
-    while (S * 2 <= std::max(1, env_int("LCSG_SKELETON_STRIDE", default_skeleton_stride(n1)))) S *= 2;
+    while (S * 2 <= std::max(1, sweep_on ? env_int("LCSG_SWEEP_STRIDE", default_sweep_stride(n1))
+                                         : env_int("LCSG_SKELETON_STRIDE", default_skeleton_stride(n1))))
+        S *= 2;
     int col_block = 1;
     while (col_block * 2 <= std::min(16, std::max(2, env_int("LCSG_COL_BLOCK", default_col_block(n1)))))
         col_block *= 2;
@@ -1903,14 +1921,19 @@ int lcsg_combine_rows(const int32_t *upper_reach, int32_t wu1, const int32_t *up
             CKL(launch_combine(1, &sc->d, 1, c, shift, key64, s, S));
         else
             CKL(launch_skeleton(&sc->d, 1, c, shift, key64, S, s));
-        for (int32_t rem = S; rem > 1;) {
-            const int32_t B = std::min<int32_t>(col_block, rem);
-            CKL(launch_block_refine(&sc->d, 1, c, shift, key64, B, rem / B, w1, s));
-            rem /= B;
+        if (sweep_on) {  // row sweep below the skeleton rows (lcsg_sweep.cu)
+            CKL(launch_table_events(&sc->d, 1, c, s));
+            CKL(launch_sweep(&sc->d, 1, c, shift, key64, S, w1, s));
+        } else {
+            for (int32_t rem = S; rem > 1;) {
+                const int32_t B = std::min<int32_t>(col_block, rem);
+                CKL(launch_block_refine(&sc->d, 1, c, shift, key64, B, rem / B, w1, s));
+                rem /= B;
+            }
         }
-        CKL(launch_finalize_rows(&sc->d, 1, c, S, s, w1));
+        CKL(launch_finalize_rows(&sc->d, 1, c, S, s, w1, sweep_on));
     }
-    CK(cudaFreeAsync(sc, s));
+    CK(cudaFreeAsync(scbuf, s));
     return LCSG_OK;
 }
 

@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(MULTI ? 1024 : 128)
                 for (int32_t j = Knew + 1 + gt; j < w1; j += 32) gR[j] = inf;
             } else {  // scalar stores up to a 16-byte boundary, then int4
                 const int32_t j0 = Knew + 1;
-                const int32_t head = (int32_t)((4 - ((((size_t)(cr + 1) * w1 + j0)) & 3)) & 3);
+                const int32_t head = (int32_t)((4 - (((uintptr_t)(gR + j0) >> 2) & 3)) & 3);  // the table base may be a row window
                 const int32_t jv = min(j0 + head, w1);  // first aligned cell
                 if (gt < jv - j0) gR[j0 + gt] = inf;
                 const int32_t nv4 = (w1 - jv) >> 2;
@@ -703,6 +703,13 @@ int launch_sweep(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool
                                                                       reg ? 1 : 0);
     LCSG_LAUNCH_CHECK();
     return 0;
+}
+
+// kernels one launch_sweep call launches (for the handle's launch counter)
+int sweep_launch_count(int shift, bool key64, int32_t S) {
+    const char *e = getenv("LCSG_SWEEP_REG");
+    const bool use_reg = !(e && *e) || atoi(e) != 0;
+    return (use_reg && S <= RG_MAXS && !key64 && shift < 32) ? 2 : 1;
 }
 
 int sweep_error_count(int32_t *count, bool reset) {

@@ -574,9 +574,11 @@ __global__ void __launch_bounds__(32 * FN_WARPS)
     // phase 2: fill the INF suffix traces of each row, coalesced (the reach
     // cells are already written): 0 over (colhi, w], and each INF node's segment
     // [mid_s, hi_s] (hi_0 = colhi, hi_s = mid_{s-1} - 1) with its `top`
-    for (int rr = 0; rr < rpw; ++rr) {
-        const bool ract = __shfl_sync(0xffffffffu, act, rr);
-        if (!ract) continue;
+    // only the rows with INF cells (K < w) have anything to fill
+    unsigned todo = __ballot_sync(0xffffffffu, act && K < w);
+    while (todo) {
+        const int rr = __ffs(todo) - 1;
+        todo &= todo - 1;
         const int32_t Kr = __shfl_sync(0xffffffffu, K, rr);
         const int32_t ch = __shfl_sync(0xffffffffu, colhi, rr);
         const int ns = nseg_all[wid][rr];
