@@ -47,8 +47,8 @@ __device__ int32_t g_sweep_err = 0;
 // state in the output rows (finite prefix beyond the shared-memory capacity)
 __device__ unsigned long long g_sweep_paths[2];
 #ifdef LCSG_SWEEP_STATS
-// per launch-size class (log2 of group threads - 5): steps, main rounds, walk cells,
-// splits per cell, zero-run evaluations, zero-run rounds, case A, zero-run length
+// per launch-size class (log2 of group threads - 5): row steps, evaluation
+// rounds, walk cells, splits per cell
 __device__ unsigned long long g_sweep_stat[8][8];
 #define SW_STAT(cls, idx, val) atomicAdd(&g_sweep_stat[cls][idx], (unsigned long long)(val))
 #else

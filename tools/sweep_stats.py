@@ -16,9 +16,9 @@ lib.lcsg_sweep_stats.argtypes = [ctypes.c_void_p]; lib.lcsg_sweep_stats.restype 
 assert lib.lcsg_sweep_stats(out) == 0
 st = np.array(list(out), dtype=np.float64).reshape(8, 8)
 print("lcs", r.length)
-print("group threads | steps | rounds/step | walk cells/step | splits/cell | zero-run evals/step | zero-run rounds/eval | caseA/step | zero-run len/step")
+print("group threads | row steps | evaluation rounds/step | walk cells/step | splits per cell")
 for c in range(8):
     s = st[c]
     if s[0] == 0:
         continue
-    print(f"{32 << c:5d} | {int(s[0]):8d} | {s[1]/s[0]:.2f} | {s[2]/s[0]:.2f} | {s[3]/s[0]:.1f} | {s[4]/s[0]:.3f} | {s[5]/max(s[4],1):.2f} | {s[6]/s[0]:.3f} | {s[7]/s[0]:.2f}")
+    print(f"{32 << c:5d} | {int(s[0]):8d} | {s[1]/s[0]:.2f} | {s[2]/s[0]:.2f} | {s[3]/s[0]:.1f}")
