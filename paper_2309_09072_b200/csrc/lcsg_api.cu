@@ -367,7 +367,7 @@ int enqueue_build_kernels(lcsg_tree_s *t, cudaStream_t s, int64_t *launches, boo
     for (const LaunchH &L : t->plan) {
         r = launch_plan_entry(t, L, s);
         if (r > 0) return r;
-        if (r == 0) nl += L.kind == 13 ? sweep_launch_count(L.shift, L.key64, L.stride_or_delta) : 1;
+        if (r == 0) nl += L.kind == 13 ? sweep_launch_count(L.shift, L.key64, L.stride_or_delta, L.ustride) : 1;
     }
     if (events && t->timing && t->ev_ok && (e = cudaEventRecord(t->ev[2], s))) return (int)e;
     if (launches) *launches = nl;
@@ -1209,7 +1209,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             }
             if (e == 0) {
                 const LaunchH &PL = t->plan[pi];
-                t->launches += PL.kind == 13 ? sweep_launch_count(PL.shift, PL.key64, PL.stride_or_delta) : 1;
+                t->launches += PL.kind == 13 ? sweep_launch_count(PL.shift, PL.key64, PL.stride_or_delta, PL.ustride) : 1;
             }
         }
         level_di = di;

@@ -371,7 +371,7 @@ __device__ __forceinline__ int ceil_log2(int32_t x) { return x <= 1 ? 0 : 32 - _
 template <int CPT, bool MULTI>
 __global__ void __launch_bounds__(MULTI ? 1024 : 128)
     sweep_reg_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int32_t S,
-                     int32_t nblk, int shift, int64_t ngroups) {
+                     int32_t nblk, int shift, int64_t ngroups, int flagged_only) {
     constexpr int GPB = MULTI ? 1 : 4;  // groups per CTA
     constexpr int CKN = MULTI ? 512 : 128;
     constexpr int QMAX = MULTI ? 256 : 32;  // cells per round
@@ -405,6 +405,12 @@ __global__ void __launch_bounds__(MULTI ? 1024 : 128)
     const int32_t jl = wbase + lane;      // this thread's cell 0
     const uint32_t kmask = (1u << shift) - 1u;
 
+    // second pass of the cascade (wider groups): only the blocks the first flagged
+    if (flagged_only) {
+        if (!*flag) return;
+        gsync<MULTI>();
+        if (gt == 0) *flag = 0;
+    }
     int32_t K = d.out_kmax[a];  // written by the skeleton kernel
     if (K + 1 > capc) {
         if (gt == 0) *flag = 1;
@@ -676,11 +682,11 @@ int launch_sweep(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool
         if (maxw1 <= one_warp_max && maxw1 <= 32 * 17) {
             const unsigned nb = (unsigned)((ngroups + 3) / 4);
             if (maxw1 <= 32 * 5)
-                sweep_reg_kernel<5, false><<<nb, 128, 0, s>>>(descs, ndesc, c, S, nblk, shift, ngroups);
+                sweep_reg_kernel<5, false><<<nb, 128, 0, s>>>(descs, ndesc, c, S, nblk, shift, ngroups, 0);
             else if (maxw1 <= 32 * 9)
-                sweep_reg_kernel<9, false><<<nb, 128, 0, s>>>(descs, ndesc, c, S, nblk, shift, ngroups);
+                sweep_reg_kernel<9, false><<<nb, 128, 0, s>>>(descs, ndesc, c, S, nblk, shift, ngroups, 0);
             else
-                sweep_reg_kernel<17, false><<<nb, 128, 0, s>>>(descs, ndesc, c, S, nblk, shift, ngroups);
+                sweep_reg_kernel<17, false><<<nb, 128, 0, s>>>(descs, ndesc, c, S, nblk, shift, ngroups, 0);
         } else {
             int lg_max = 6;
             {
@@ -689,8 +695,21 @@ int launch_sweep(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool
             }
             int lg = 6;
             while (lg < lg_max && (9 << lg) < maxw1) ++lg;
+            // 1024-thread groups leave one CTA per SM: blocks whose finite prefix
+            // fits 512 threads' registers go first in half-size groups (two CTAs
+            // per SM), the rest (flagged) in a second pass (cfg5, 8192-row level:
+            // 1.17 -> 0.77 ms).  Not for tables wider than 1024 * 9 cells (the
+            // root of cfg5): there the second pass, run after the first, costs more
+            // than the first saves (0.75 -> 1.02 ms)
+            const bool cascade = lg >= env_or("LCSG_SWEEP_CASCADE_MINLG", 10) && maxw1 <= (9 << 10) &&
+                                 env_or("LCSG_SWEEP_CASCADE", 1) != 0;
+            if (cascade) {
+                sweep_reg_kernel<9, true><<<(unsigned)ngroups, 1 << (lg - 1), 0, s>>>(
+                    descs, ndesc, c, S, nblk, shift, ngroups, 0);
+                LCSG_LAUNCH_CHECK();
+            }
             sweep_reg_kernel<9, true><<<(unsigned)ngroups, 1 << lg, 0, s>>>(descs, ndesc, c, S, nblk,
-                                                                           shift, ngroups);
+                                                                           shift, ngroups, cascade ? 1 : 0);
         }
         LCSG_LAUNCH_CHECK();
     }
@@ -706,10 +725,17 @@ int launch_sweep(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool
 }
 
 // kernels one launch_sweep call launches (for the handle's launch counter)
-int sweep_launch_count(int shift, bool key64, int32_t S) {
-    const char *e = getenv("LCSG_SWEEP_REG");
-    const bool use_reg = !(e && *e) || atoi(e) != 0;
-    return (use_reg && S <= RG_MAXS && !key64 && shift < 32) ? 2 : 1;
+int sweep_launch_count(int shift, bool key64, int32_t S, int32_t maxw1) {
+    auto env_or = [](const char *name, int def) {
+        const char *e = getenv(name);
+        return e && *e ? atoi(e) : def;
+    };
+    if (!(env_or("LCSG_SWEEP_REG", 1) && S <= RG_MAXS && !key64 && shift < 32)) return 1;
+    const bool warp = maxw1 <= env_or("LCSG_SWEEP_ONE_WARP_MAXW1", 544) && maxw1 <= 32 * 17;
+    const bool cascade = !warp && (9 << 9) < maxw1 && maxw1 <= (9 << 10) &&
+                         env_or("LCSG_SWEEP_GN_MAX", 1024) >= 1024 &&
+                         env_or("LCSG_SWEEP_CASCADE", 1) != 0;
+    return cascade ? 3 : 2;
 }
 
 int sweep_error_count(int32_t *count, bool reset) {

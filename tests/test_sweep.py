@@ -68,6 +68,8 @@ SWEEP_ENVS = [
     {"LCSG_SWEEP_REG": "0", "LCSG_SWEEP_CPT": "1"},           # ... many threads per row
     {"LCSG_SWEEP_ONE_WARP_MAXW1": "0"},                      # CTA groups for every width
     {"LCSG_SWEEP_ONE_WARP_MAXW1": "0", "LCSG_SWEEP_GN_MAX": "64"},  # 2-warp groups; wide rows overflow -> fallback
+    {"LCSG_SWEEP_CASCADE_MINLG": "7"},                       # half-size CTA groups first, flagged blocks second
+    {"LCSG_SWEEP_CASCADE": "0"},
     {"LCSG_SWEEP_STRIDE": "16", "LCSG_THREAD_MAX_W1": "9"},   # sweep from height 4 on (events of narrow children)
     {"LCSG_SWEEP_STRIDE": "16", "LCSG_NARROW": "0", "LCSG_VIRTUAL_H1": "0"},
 ]
@@ -149,6 +151,19 @@ def test_sweep_long_walks(env, monkeypatch):
             assert (r.length, r.subsequence, r.row_positions, r.col_positions) == exp
     a, b = _planted(rng, 600, 640, 200)
     check_pair(a, b, f"planted {env}")
+
+
+def test_sweep_cascade_second_pass(monkeypatch):
+    """CTA-group cascade (half-size groups first, the blocks whose finite prefix
+    overflows their registers in a second pass of full-size groups): planted
+    near-copies make the upper levels' rows nearly full width."""
+    monkeypatch.setenv("LCSG_SWEEP_CASCADE_MINLG", "7")
+    rng = np.random.default_rng(21)
+    a, b = _planted(rng, 1000, 1100, 26, keep=0.9)
+    check_pair(a, b, "cascade planted")
+    a, b = workloads.random_pair(rng, 1000, 1100, 2)
+    check_pair(a, b, "cascade sigma 2")
+    L.sweep_paths(reset=True)
 
 
 def test_sweep_structured_inputs():
