@@ -369,8 +369,8 @@ __device__ __forceinline__ int ceil_log2(int32_t x) { return x <= 1 ? 0 : 32 - _
 // largest changed cell is j1.  Longer walks take further rounds (two barriers
 // each).
 template <int CPT, bool MULTI>
-__global__ void __launch_bounds__(MULTI ? 1024 : 128)
-    sweep_reg_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int32_t S,
+__device__ __forceinline__ void
+    sweep_reg_body(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int32_t S,
                      int32_t nblk, int shift, int64_t ngroups, int flagged_only) {
     constexpr int GPB = MULTI ? 1 : 4;  // groups per CTA
     constexpr int CKN = MULTI ? 512 : 128;
@@ -641,6 +641,22 @@ __global__ void __launch_bounds__(MULTI ? 1024 : 128)
 #undef RG_FALLBACK
 }
 
+template <int CPT, bool MULTI>
+__global__ void __launch_bounds__(MULTI ? 1024 : 128)
+    sweep_reg_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int32_t S,
+                     int32_t nblk, int shift, int64_t ngroups, int flagged_only) {
+    sweep_reg_body<CPT, MULTI>(descs, ndesc, c, S, nblk, shift, ngroups, flagged_only);
+}
+
+// CTA groups of <= 256 threads: a register cap (48) keeps 40 instead of 32 warps
+// resident per SM (cfg5 levels of 1024 / 2048 rows: -3% / -8%)
+template <int CPT>
+__global__ void __launch_bounds__(256, 5)
+    sweep_reg_small_kernel(const CombineDesc *__restrict__ descs, int32_t ndesc, Ctx c, int32_t S,
+                           int32_t nblk, int shift, int64_t ngroups, int flagged_only) {
+    sweep_reg_body<CPT, true>(descs, ndesc, c, S, nblk, shift, ngroups, flagged_only);
+}
+
 }  // namespace
 
 int launch_table_events(const CombineDesc *descs, int32_t ndesc, Ctx c, cudaStream_t s) {
@@ -708,8 +724,12 @@ int launch_sweep(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool
                     descs, ndesc, c, S, nblk, shift, ngroups, 0);
                 LCSG_LAUNCH_CHECK();
             }
-            sweep_reg_kernel<9, true><<<(unsigned)ngroups, 1 << lg, 0, s>>>(descs, ndesc, c, S, nblk,
-                                                                           shift, ngroups, cascade ? 1 : 0);
+            if (lg <= 8 && env_or("LCSG_SWEEP_SMALL_CAP", 1))
+                sweep_reg_small_kernel<9><<<(unsigned)ngroups, 1 << lg, 0, s>>>(
+                    descs, ndesc, c, S, nblk, shift, ngroups, cascade ? 1 : 0);
+            else
+                sweep_reg_kernel<9, true><<<(unsigned)ngroups, 1 << lg, 0, s>>>(
+                    descs, ndesc, c, S, nblk, shift, ngroups, cascade ? 1 : 0);
         }
         LCSG_LAUNCH_CHECK();
     }
