@@ -416,7 +416,8 @@ def run_ours(args, rank, world, dist):
                 "survey_8d": {"algorithmic_bytes": alg_8d, "achieved": alg_8d / (comb / 1e3) / 1e9,
                               "frac": alg_8d / (comb / 1e3) / 1e9 / peak,
                               "note": "4*G + 8*OUT + 4*IN with the reference's gather count G; "
-                                      "round 1's fraction (0.59) used this figure"}}
+                                      "round 1's fraction (0.59) used this figure; the row sweep does not "
+                                      "perform those gathers, so this can exceed 1"}}
         # INT32 term: C reference cell evaluations, one
         # 32-bit min each, at the IMNMX rate measured live on this GPU
         rate, sms, pms = ctypes.c_double(), ctypes.c_int32(), ctypes.c_double()

@@ -17,18 +17,21 @@ ncu --set full --clock-control none --import-source on -k regex:$2 -s $3 -c 1 -o
 python tools/ncu_summary.py $O/$1.ncu-rep "$1 (cfg5)" > $O/$1.txt
 }
 # ncu matches the base kernel name: the sweep launches of a cfg5 solve are, in
-# order, <5,0> <9,0> <17,0> (warp groups) and five <9,1> (CTA groups, h = 1024 .. root)
+# order, sweep_reg_kernel <5,0> <9,0> <17,0> (warp groups), two sweep_reg_small_kernel
+# (CTA groups of 128 / 256 threads, h = 1024 / 2048) and sweep_reg_kernel <9,1> for
+# h = 4096, h = 8192 (half-size pass, then the flagged pass) and the root
 cap r2s_ncu_sweep_warp5 "sweep_reg_kernel" 0
 cap r2s_ncu_sweep_warp9 "sweep_reg_kernel" 1
 cap r2s_ncu_sweep_warp17 "sweep_reg_kernel" 2
-cap r2s_ncu_sweep_cta_h1024 "sweep_reg_kernel" 3
-cap r2s_ncu_sweep_cta_h4096 "sweep_reg_kernel" 5
-cap r2s_ncu_sweep_cta_top "sweep_reg_kernel" 7
+cap r2s_ncu_sweep_cta_h1024 "sweep_reg_small_kernel" 0
+cap r2s_ncu_sweep_cta_h4096 "sweep_reg_kernel" 3
+cap r2s_ncu_sweep_cta_h8192 "sweep_reg_kernel" 4
+cap r2s_ncu_sweep_cta_top "sweep_reg_kernel" 6
 cap r2s_ncu_skeleton "^skeleton_kernel" 3
 cap r2s_ncu_finalize "finalize_rows_kernel" 4
 cap r2s_ncu_narrow8 "narrow_combine_kernel" 2
 cap r2s_ncu_roll "narrow32_roll_kernel" 0
-python tools/issue_json.py $O/r2s_launches_cfg5_summary.txt "sweep_reg_kernel<5"=$O/r2s_ncu_sweep_warp5.txt "sweep_reg_kernel<9, 0"=$O/r2s_ncu_sweep_warp9.txt "sweep_reg_kernel<17"=$O/r2s_ncu_sweep_warp17.txt "sweep_reg_kernel<9, 1"=$O/r2s_ncu_sweep_cta_h4096.txt "skeleton_kernel"=$O/r2s_ncu_skeleton.txt "finalize_rows"=$O/r2s_ncu_finalize.txt "narrow_combine_kernel"=$O/r2s_ncu_narrow8.txt "narrow32_roll"=$O/r2s_ncu_roll.txt > $O/issue_cfg5.json
+python tools/issue_json.py $O/r2s_launches_cfg5_summary.txt "sweep_reg_kernel<5"=$O/r2s_ncu_sweep_warp5.txt "sweep_reg_kernel<9, 0"=$O/r2s_ncu_sweep_warp9.txt "sweep_reg_kernel<17"=$O/r2s_ncu_sweep_warp17.txt "sweep_reg_small_kernel"=$O/r2s_ncu_sweep_cta_h1024.txt "sweep_reg_kernel<9, 1"=$O/r2s_ncu_sweep_cta_h4096.txt "skeleton_kernel"=$O/r2s_ncu_skeleton.txt "finalize_rows"=$O/r2s_ncu_finalize.txt "narrow_combine_kernel"=$O/r2s_ncu_narrow8.txt "narrow32_roll"=$O/r2s_ncu_roll.txt > $O/issue_cfg5.json
 cat $O/issue_cfg5.json | tail -5
 python tools/fuzz_parity.py 240 2024 > $O/r2s_fuzz.txt 2>&1; tail -1 $O/r2s_fuzz.txt
 rm -f $O/*.ncu-rep
