@@ -310,6 +310,70 @@ struct LayoutCache {
 };
 thread_local LayoutCache t_layout;
 
+// Side stream of a build: after a row sweep, the finalize kernel only writes the
+// INF-suffix traces of the level (kmax is the sweep's, wstar the skeleton
+// kernel's: kmax is nonincreasing in the start column, so row 0 holds the
+// maximum) -- nothing later in the build reads them, so it runs beside the next
+// levels and joins the handle's stream at the end.  Leased per build call from a
+// small per-device pool (a re-recorded event does not disturb waits already
+// enqueued, so a lease can be reused as soon as the call returns).
+struct SideCtx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+std::mutex g_side_mu;
+std::vector<SideCtx *> g_side_free;
+
+struct SideLease {
+    SideCtx *c = nullptr;
+    bool dirty = false;
+    void acquire(int device) {
+        if (env_int("LCSG_FINALIZE_SIDE", 1) == 0) return;
+        {
+            std::lock_guard<std::mutex> lk(g_side_mu);
+            for (size_t i = 0; i < g_side_free.size(); ++i)
+                if (g_side_free[i]->device == device) {
+                    c = g_side_free[i];
+                    g_side_free.erase(g_side_free.begin() + i);
+                    return;
+                }
+        }
+        SideCtx *n = new SideCtx();
+        n->device = device;
+        if (cudaStreamCreateWithFlags(&n->stream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&n->fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&n->join, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            delete n;  // no side stream: the finalize kernels stay on the handle's stream
+            return;
+        }
+        c = n;
+    }
+    // enqueue `fn(stream)` beside the work already on s
+    template <typename F>
+    int fork(cudaStream_t s, F fn) {
+        if (cudaEventRecord(c->fork, s) != cudaSuccess ||
+            cudaStreamWaitEvent(c->stream, c->fork, 0) != cudaSuccess)
+            return (int)cudaGetLastError();
+        dirty = true;
+        return fn(c->stream);
+    }
+    int join(cudaStream_t s) {
+        if (!c || !dirty) return 0;
+        dirty = false;
+        if (cudaEventRecord(c->join, c->stream) != cudaSuccess ||
+            cudaStreamWaitEvent(s, c->join, 0) != cudaSuccess)
+            return (int)cudaGetLastError();
+        return 0;
+    }
+    ~SideLease() {
+        if (!c) return;
+        std::lock_guard<std::mutex> lk(g_side_mu);
+        g_side_free.push_back(c);
+    }
+};
+
 // One entry of the level plan on stream s (kernel choice: DESIGN.md 4).
 int launch_plan_entry(lcsg_tree_s *t, const LaunchH &L, cudaStream_t s) {
     const Ctx c = t->ctx();
@@ -342,6 +406,17 @@ int launch_plan_entry(lcsg_tree_s *t, const LaunchH &L, cudaStream_t s) {
     return -1;  // no launch
 }
 
+// A plan entry, with the finalize kernels that follow a row sweep forked onto the
+// side stream (traced builds) or dropped (low-memory builds keep no traces, and
+// kmax / wstar do not come from that kernel).  Returns like launch_plan_entry.
+int launch_plan_entry_side(lcsg_tree_s *t, const LaunchH &L, cudaStream_t s, SideLease &side) {
+    if (L.kind == 8 && L.wpr_log2 != 0 && side.c) {
+        if (!t->with_trace) return -1;
+        return side.fork(s, [&](cudaStream_t ss) { return launch_plan_entry(t, L, ss); });
+    }
+    return launch_plan_entry(t, L, s);
+}
+
 // Every kernel of a build after the inputs and the plan metadata are in the
 // arena (what build_impl enqueues, minus its host-to-device copies): the
 // sequence a per-shape CUDA graph captures.  Returns a CUDA error or 0.
@@ -364,11 +439,17 @@ int enqueue_build_kernels(lcsg_tree_s *t, cudaStream_t s, int64_t *launches, boo
         ++nl;
     }
     if (events && t->timing && t->ev_ok && (e = cudaEventRecord(t->ev[1], s))) return (int)e;
+    SideLease side;
+    side.acquire(t->device);
     for (const LaunchH &L : t->plan) {
-        r = launch_plan_entry(t, L, s);
-        if (r > 0) return r;
+        r = launch_plan_entry_side(t, L, s, side);
+        if (r > 0) {
+            side.join(s);
+            return r;
+        }
         if (r == 0) nl += L.kind == 13 ? sweep_launch_count(L.shift, L.key64, L.stride_or_delta, L.ustride) : 1;
     }
+    if ((r = side.join(s)) != 0) return r;
     if (events && t->timing && t->ev_ok && (e = cudaEventRecord(t->ev[2], s))) return (int)e;
     if (launches) *launches = nl;
     return 0;
@@ -1046,7 +1127,9 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     const Ctx c = t->ctx();
     if (t->nvirt > 0) BCKL(launch_virtual_wstar(c, t->d_vnodes, t->nvirt, t->d_node_wstar, s));
     bool ev1_done = false;  // ev[1]: just before the first level's descriptors
-    auto launch_entry = [&](const LaunchH &L) -> int { return launch_plan_entry(t, L, s); };
+    SideLease side;
+    side.acquire(device);
+    auto launch_entry = [&](const LaunchH &L) -> int { return launch_plan_entry_side(t, L, s, side); };
     int32_t maxh = 0;
     for (auto &nd : t->nodes) maxh = std::max(maxh, nd.height);
     const int vbits = bits_for(t->inf);
@@ -1204,6 +1287,7 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
             if (e > 0) {
                 const int r = fail(LCSG_ECUDA, std::string("launch: ") +
                                                    cudaGetErrorString((cudaError_t)e));
+                side.join(s);
                 lease.finish(); destroy(t);
                 return r;
             }
@@ -1215,6 +1299,8 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
         level_di = di;
         level_plan = t->plan.size();
     }
+    BCKL(side.join(s));
+    --t->launches;  // the join is not a kernel
     const auto h3 = hclock();
     if (!ev1_done && t->timing && t->ev_ok) BCK(cudaEventRecord(t->ev[1], s));  // no combines
     if (t->timing && t->ev_ok) BCK(cudaEventRecord(t->ev[2], s));

@@ -592,7 +592,10 @@ __global__ void __launch_bounds__(32 * FN_WARPS)
             hi = e.x - 1;
         }
     }
-    if (lane == 0 && kmax_warp >= 0) atomicMax(d.out_wstar, kmax_warp);
+    // wstar = max kmax: most warps bring nothing new (kmax is nonincreasing in the
+    // start column), so look before the atomic -- thousands of warps share the word
+    if (lane == 0 && kmax_warp >= 0 && kmax_warp > *(volatile int32_t *)d.out_wstar)
+        atomicMax(d.out_wstar, kmax_warp);
 }
 
 int launch_block_refine(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool key64,
