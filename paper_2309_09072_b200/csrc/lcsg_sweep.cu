@@ -17,13 +17,14 @@
 //   * only the cells between (j1 <= j <= J, J = last j with trace[c][j] <= ju1)
 //     need candidates evaluated, each over a split range bounded by ju1 below
 //     and by its right neighbour's split above.
-// So a row costs a handful of L gathers (one warp) plus a streaming rewrite of
-// the row -- the kernel is bound by the 8 B per cell it writes, not by
-// per-cell searches.  The chain over rows is cut by the skeleton rows
-// (exact Alg. 1 every S rows, lcsg_refine.cu): one thread group sweeps the
-// S-1 interior rows below a skeleton row, with the row state (reach, trace of
-// the finite prefix) ping-ponged in shared memory, or kept in the output rows
-// themselves when the finite prefix does not fit.
+// So a row costs a handful of L gathers plus a streaming rewrite of the row
+// instead of a search per cell.  The chain over rows is cut by the skeleton
+// rows (exact Alg. 1 every S rows, lcsg_refine.cu): one thread group sweeps
+// the S-1 interior rows below a skeleton row.  Two kernels: the
+// register-resident one (row state in registers; the fast path, below) and a
+// generic one (row state ping-ponged in shared memory, or kept in the output
+// rows themselves when the finite prefix does not fit; 64-bit keys) that
+// also redoes the blocks the fast path flags.
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
@@ -320,16 +321,15 @@ __global__ void sweep_kernel(const CombineDesc *__restrict__ descs, int32_t ndes
 // ---------------------------------------------------------------------------
 // Register-resident sweep (the fast path).  A group of gn threads (one warp,
 // four groups per CTA; or a whole CTA) owns a block of rows; thread gt keeps
-// the cells j = gt + gn * i (i < CPT) of the current row in registers --
-// reach R[i] and split T[i], (INF, INT_MAX) beyond the finite prefix.  Per
-// step: J and the zero-split prefix come from per-thread counts (the splits
-// are nondecreasing along a row); the few cells around J are published to a
-// shared window; all threads evaluate the (cell, split) pairs of the walk at
-// once (keys reduce with shared-memory atomicMin); every warp reads off j1;
-// the row is rewritten in registers (neighbour cell by shuffle) and stored.
-// Anything outside the fast path's bounds (finite prefix wider than gn * CPT,
-// walks / zero-split runs longer than the patch arrays, a broken invariant)
-// flags the block; the generic kernel above then redoes flagged blocks.
+// CPT cells of the current row in registers -- reach R[i] and split T[i],
+// (INF, INT_MAX) beyond the finite prefix.  Per step: J comes from per-thread
+// counts (the splits are nondecreasing along a row); all threads evaluate the
+// (cell, split) pairs of the walk at once (keys reduce with shared-memory
+// atomicMin); the owners of the walk cells compare and the largest changed
+// cell is j1; the row is rewritten in registers (neighbour cell by shuffle)
+// and stored.  Anything outside the fast path's bounds (finite prefix wider
+// than gn * CPT, walks longer than the key array, a broken invariant) flags
+// the block; the generic kernel above then redoes flagged blocks.
 // ---------------------------------------------------------------------------
 constexpr int RG_SEG = 32;   // prefetched U entries from the insertion rank on
 constexpr int RG_MAXS = 128;  // rows per block
