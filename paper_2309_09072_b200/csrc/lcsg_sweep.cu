@@ -633,7 +633,9 @@ __device__ __forceinline__ void
             K = Knew;
         }
         // keys used two steps ago live in the other buffer: clear them for the next step
-        for (int t = gt; t < dirty_other; t += gn) sm.ck[par ^ 1][t] = K32_NONE;
+        if (gt < dirty_other) sm.ck[par ^ 1][gt] = K32_NONE;  // usually a handful of slots
+        if (dirty_other > gn)
+            for (int t = gt + gn; t < dirty_other; t += gn) sm.ck[par ^ 1][t] = K32_NONE;
         dirty_other = dirty_this;
         cp_async_wait_all();
         if (!MULTI) __syncwarp();
