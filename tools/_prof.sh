@@ -2,10 +2,6 @@
 set -x
 O=gpurun_out/prof; mkdir -p $O
 python -m pytest tests -m gpu -x -q > $O/r2s_gpu_tests.txt 2>&1; tail -2 $O/r2s_gpu_tests.txt
-python bench.py > $O/r2s_bench_cfg5.json 2> $O/bench5.err
-python bench.py --impl reference --steps 2 --warmup 1 > $O/r2s_bench_reference_cfg5.json 2> $O/ref.err
-for c in 4 3 2; do python bench.py --config $c --steps 20 > $O/r2s_bench_cfg$c.json 2> $O/bench$c.err; done
-python bench.py --config 1 --steps 400 --warmup 20 > $O/r2s_bench_cfg1.json 2> $O/bench1.err
 python tools/one_solve.py 5 1 > $O/plain.log 2>&1 || exit 1
 for c in 5 4 3 2; do
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $O/r2s_launches_cfg$c.csv python tools/one_solve.py $c 1 > $O/ncu_l$c.log 2>&1
@@ -33,5 +29,13 @@ cap r2s_ncu_narrow8 "narrow_combine_kernel" 2
 cap r2s_ncu_roll "narrow32_roll_kernel" 0
 python tools/issue_json.py $O/r2s_launches_cfg5_summary.txt "sweep_reg_kernel<5"=$O/r2s_ncu_sweep_warp5.txt "sweep_reg_kernel<9, 0"=$O/r2s_ncu_sweep_warp9.txt "sweep_reg_kernel<17"=$O/r2s_ncu_sweep_warp17.txt "sweep_reg_small_kernel"=$O/r2s_ncu_sweep_cta_h1024.txt "sweep_reg_kernel<9, 1"=$O/r2s_ncu_sweep_cta_h4096.txt "skeleton_kernel"=$O/r2s_ncu_skeleton.txt "finalize_rows"=$O/r2s_ncu_finalize.txt "narrow_combine_kernel"=$O/r2s_ncu_narrow8.txt "narrow32_roll"=$O/r2s_ncu_roll.txt > $O/issue_cfg5.json
 cat $O/issue_cfg5.json | tail -5
+# the bench lines embed profiles/traffic_cfg*.json and profiles/issue_cfg5.json: install the fresh ones first
+cp $O/traffic_cfg*.json $O/issue_cfg5.json profiles/
+python bench.py > $O/r2s_bench_cfg5.json 2> $O/bench5.err
+python bench.py --impl reference --steps 2 --warmup 1 > $O/r2s_bench_reference_cfg5.json 2> $O/ref.err
+for c in 4 3 2; do python bench.py --config $c --steps 20 > $O/r2s_bench_cfg$c.json 2> $O/bench$c.err; done
+python bench.py --config 1 --steps 400 --warmup 20 > $O/r2s_bench_cfg1.json 2> $O/bench1.err
+python -c "import __graft_entry__ as g; g.smoke()"
+python tools/batch_throughput.py > $O/r2s_batch_throughput.json 2>&1
 python tools/fuzz_parity.py 240 2024 > $O/r2s_fuzz.txt 2>&1; tail -1 $O/r2s_fuzz.txt
 rm -f $O/*.ncu-rep
