@@ -465,7 +465,7 @@ int enqueue_build_kernels(lcsg_tree_s *t, cudaStream_t s, int64_t *launches, boo
 // one handle at a time (a second concurrent solve of the shape takes the
 // normal path); the next user waits on the previous user's stream through
 // `released`.  Entries are kept only for arenas up to LCSG_GRAPH_MAX_MB
-// (default 8192) and at most 8 of them, LRU-evicted; lcsg_trim() drops them.
+// (default: a quarter of the device's memory) and at most 8 of them, LRU-evicted; lcsg_trim() drops them.
 struct SolveEntry {
     std::string key;
     int device = 0;
@@ -683,9 +683,19 @@ int graph_build(lcsg_tree_s *t, SolveEntry *en, const uint8_t *rows, bool rows_d
 // After a normal build: keep its arena and capture its kernels as the
 // shape's build graph (best effort: any failure leaves the handle normal).
 void try_create_entry(lcsg_tree_s *t, const std::string &key) {
-    const size_t max_bytes = (size_t)std::max(0, env_int("LCSG_GRAPH_MAX_MB", 8192)) << 20;
+    // cache bounds: a quarter of the device's memory per arena, 35% in total (the
+    // library's pool keeps a freed arena mapped anyway until lcsg_trim, so caching
+    // it costs no extra HBM in steady state); LCSG_GRAPH_MAX_MB / _TOTAL_MB override
+    size_t dev_free = 0, dev_total = 0;
+    if (cudaMemGetInfo(&dev_free, &dev_total) != cudaSuccess) {
+        cudaGetLastError();
+        dev_total = (size_t)32 << 30;
+    }
+    const int def_max_mb = (int)std::min<size_t>(dev_total / 4 >> 20, 1u << 30);
+    const int def_total_mb = (int)std::min<size_t>((dev_total / 20 * 7) >> 20, 1u << 30);
+    const size_t max_bytes = (size_t)std::max(0, env_int("LCSG_GRAPH_MAX_MB", def_max_mb)) << 20;
     if (t->arena_bytes > max_bytes) return;
-    const size_t max_total = (size_t)std::max(0, env_int("LCSG_GRAPH_TOTAL_MB", 16384)) << 20;
+    const size_t max_total = (size_t)std::max(0, env_int("LCSG_GRAPH_TOTAL_MB", def_total_mb)) << 20;
     std::vector<SolveEntry *> evict;
     {
         std::lock_guard<std::mutex> lk(g_graph_mu);
