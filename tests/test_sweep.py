@@ -70,6 +70,8 @@ SWEEP_ENVS = [
     {"LCSG_SWEEP_ONE_WARP_MAXW1": "0", "LCSG_SWEEP_GN_MAX": "64"},  # 2-warp groups; wide rows overflow -> fallback
     {"LCSG_SWEEP_CASCADE_MINLG": "7"},                       # half-size CTA groups first, flagged blocks second
     {"LCSG_SWEEP_CASCADE": "0"},
+    {"LCSG_FINALIZE_SIDE": "0"},                             # finalize kernels on the handle's stream
+    {"LCSG_GRAPH": "0", "LCSG_SWEEP_SMALL_CAP": "0"},         # no graph replays; uncapped CTA-group build
     {"LCSG_SWEEP_STRIDE": "16", "LCSG_THREAD_MAX_W1": "9"},   # sweep from height 4 on (events of narrow children)
     {"LCSG_SWEEP_STRIDE": "16", "LCSG_NARROW": "0", "LCSG_VIRTUAL_H1": "0"},
 ]
