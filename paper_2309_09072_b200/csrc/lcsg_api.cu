@@ -887,6 +887,11 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
     // wide combines: row sweep below the skeleton rows (LCSG_SWEEP=0: the
     // column-refinement stages)
     const bool sweep_on = env_int("LCSG_SWEEP", 1) != 0;
+    int sm_count = 0;
+    if (cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) {
+        cudaGetLastError();
+        sm_count = 0;
+    }
     const int sweep_stride = std::max(2, env_int("LCSG_SWEEP_STRIDE", default_sweep_stride(n + 1)));
     // block size (local rows) of each column-refinement stage, power of two
     int col_block = 1;
@@ -1226,6 +1231,12 @@ int build_impl(const uint8_t *rows, bool rows_dev, int64_t m, const uint8_t *col
                 std::max(2, env_int(("LCSG_SKEL_STRIDE_H" + hs).c_str(), stride_def));
             int32_t S = 1;
             while (S * 2 <= stride_h) S *= 2;
+            if (sweep_on) {  // the sweep takes any block size
+                S = std::min(stride_h, 1024);
+                if (getenv(("LCSG_SKEL_STRIDE_H" + hs).c_str()) == nullptr &&
+                    getenv("LCSG_SWEEP_STRIDE") == nullptr)
+                    S = sweep_pick_block(S, maxw1, L.count, (int32_t)n, L.shift, L.key64, sm_count);
+            }
             int32_t cb = col_block;
             const int cb_env = env_int(("LCSG_COL_BLOCK_H" + hs).c_str(), 0);
             if (cb_env > 0) {

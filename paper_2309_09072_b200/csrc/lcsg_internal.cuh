@@ -198,6 +198,8 @@ int launch_sweep(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool
                  int32_t maxw1, cudaStream_t s);
 int sweep_error_count(int32_t *count, bool reset);
 int sweep_launch_count(int shift, bool key64, int32_t S, int32_t maxw1);
+int sweep_pick_block(int32_t S, int32_t maxw1, int32_t count, int32_t n, int shift, bool key64,
+                     int sm_count);
 int launch_walk_level(const WalkNode *nodes, const int32_t *ids, int32_t count, Ctx c,
                       int32_t *wi, int32_t *wj, int32_t *cols_out, bool retrace, int key_shift,
                       bool key64, cudaStream_t s);

@@ -746,6 +746,40 @@ int launch_sweep(const CombineDesc *descs, int32_t ndesc, Ctx c, int shift, bool
     return 0;
 }
 
+// Rows per block for one level: CTA groups of >= 512 threads leave one or two
+// CTAs per SM, so the blocks run in waves of sm_count (or 2 * sm_count) and the
+// last wave is partly empty; pick the block size in [3/4 S, S] with the fewest
+// wave-rows (cfg5 root: 256 blocks of 64 rows = 2 waves = 128 row steps; 293
+// blocks of 56 rows = 2 waves = 112).  Other levels keep S.
+int sweep_pick_block(int32_t S, int32_t maxw1, int32_t count, int32_t n, int shift, bool key64,
+                     int sm_count) {
+    auto env_or = [](const char *name, int def) {
+        const char *e = getenv(name);
+        return e && *e ? atoi(e) : def;
+    };
+    if (S < 16 || sm_count <= 0 || key64 || shift >= 32 || !env_or("LCSG_SWEEP_REG", 1) ||
+        !env_or("LCSG_SWEEP_PICK", 1))
+        return S;
+    if (maxw1 <= env_or("LCSG_SWEEP_ONE_WARP_MAXW1", 544) && maxw1 <= 32 * 17) return S;
+    if (env_or("LCSG_SWEEP_GN_MAX", 1024) < 1024) return S;
+    int lg = 6;
+    while (lg < 10 && (9 << lg) < maxw1) ++lg;
+    if (lg < 9) return S;
+    const bool cascade = lg == 10 && maxw1 <= (9 << 10) && env_or("LCSG_SWEEP_CASCADE", 1) != 0;
+    const int64_t slots = (int64_t)sm_count * ((lg == 9 || cascade) ? 2 : 1);
+    int32_t best = S;
+    int64_t best_cost = INT64_MAX;
+    for (int32_t cand = S; cand >= S - S / 4; cand -= std::max(1, S / 16)) {
+        const int64_t blocks = (int64_t)count * ((n + cand - 1) / cand);
+        const int64_t cost = (blocks + slots - 1) / slots * cand;
+        if (cost < best_cost) {
+            best_cost = cost;
+            best = cand;
+        }
+    }
+    return best;
+}
+
 // kernels one launch_sweep call launches (for the handle's launch counter)
 int sweep_launch_count(int shift, bool key64, int32_t S, int32_t maxw1) {
     auto env_or = [](const char *name, int def) {

@@ -534,7 +534,7 @@ __global__ void __launch_bounds__(32 * FN_WARPS)
     const int32_t w1 = d.w1;
     // phase 1: lane = row
     const int32_t i = r0 + lane;
-    const bool act = lane < rpw && i < n1 - 1 && (i & (S - 1)) != 0;  // S: power of two
+    const bool act = lane < rpw && i < n1 - 1 && (i % S) != 0;  // rows at multiples of S are skeleton rows
     int32_t K = -1, colhi = -1, kmax_warp = -1;
     if (act) {
         colhi = min(w, tab_kmax(U, i, inf) + wstarL);
@@ -688,7 +688,7 @@ int launch_finalize_rows(const CombineDesc *descs, int32_t ndesc, Ctx c, int32_t
     if (ndesc <= 0) return 0;
     const int64_t n1 = (int64_t)c.n + 1;
     const int rpw = maxw1 <= 512 ? 32 : (maxw1 <= 2048 ? 8 : (maxw1 <= 8192 ? 2 : 1));
-    if (S & (S - 1)) return (int)cudaErrorInvalidValue;
+    if (S < 2) return (int)cudaErrorInvalidValue;
     const int64_t warps = (n1 + rpw - 1) / rpw;  // per combine
     const dim3 blocks((unsigned)((warps + FN_WARPS - 1) / FN_WARPS),
                       (unsigned)std::min<int32_t>(ndesc, 65535), (unsigned)((ndesc + 65534) / 65535));

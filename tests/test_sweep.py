@@ -61,6 +61,8 @@ SWEEP_ENVS = [
     {"LCSG_SWEEP_STRIDE": "2"},
     {"LCSG_SWEEP_STRIDE": "8"},
     {"LCSG_SWEEP_STRIDE": "64"},
+    {"LCSG_SWEEP_STRIDE": "56"},                             # any block size, not only powers of two
+    {"LCSG_SWEEP_STRIDE": "7"},
     {"LCSG_SWEEP_STRIDE": "128"},                            # longest register-kernel block
     {"LCSG_SWEEP_STRIDE": "512"},                            # beyond it: generic kernel only
     {"LCSG_SWEEP_REG": "0"},                                 # generic kernel, state in shared memory
