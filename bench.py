@@ -390,6 +390,10 @@ def run_ours(args, rank, world, dist):
     assert r.length == length
     parity = verify_timed_path(lib, _lib, build, m, n, len(a) > len(b),
                                load_digest(args.config, seed))
+    # the row-sweep kernels check the invariants they rely on: none may have failed
+    sweep_bad = lcsgrid.sweep_errors(device=local)
+    if sweep_bad:
+        parity = f"row-sweep invariant violated {sweep_bad} times"
     e2e_t = statistics.mean(e2e_ms)
     if dist is not None:
         tt = torch.tensor([e2e_t], dtype=torch.float64, device=dev)
